@@ -1,0 +1,185 @@
+"""P13: brute force over every admissible interleaving of 2 VW x 3 waves x 8
+params (north_star), DYADIC gradients so fp32 is exact.
+
+Atomic per-VW steps (untimed model):
+  COMPLETE(v): complete the next started minibatch; at a wave end this includes
+               the PUSH; if v is not waiting at its gate, START(p+N_m) too.
+  ADMIT(v):    enabled iff v waits at its gate and the gate holds;
+               gate + pull + gated START + backlog replay.
+Every reachable state is checked once (memoised DFS over the state, which fixes
+the arrays); the number of complete paths is counted by dynamic programming.
+For each transition: every START snapshot equals w0 + the other VWs' pushed
+waves in the held commit prefix + own updates 1..a_v, recomputed from scratch,
+a_v = p - N_m exactly (STRICT), and the clock distance stays <= D+1; every
+terminal state has w_global = w0 + all updates (P9)."""
+import copy
+
+import numpy as np
+import pytest
+
+from oracle.wsp import WSPOracle, gradient, initial_weights, wave_range
+from workloads import (GRAD_DYADIC, LOCAL_AT_LEAST, LOCAL_STRICT, PULL_EAGER,
+                       PULL_LAZY, W0_PHILOX, WSPConfig)
+
+
+def _key(sm):
+    return (tuple(sm.started), tuple(sm.completed), tuple(sm.c_local),
+            tuple(sm.a), tuple(sm.held_g), tuple(sm.held_K), tuple(sm.at_gate),
+            tuple(tuple(b) for b in sm.backlog), tuple(sm.commit))
+
+
+def explore(cfg):
+    idx = np.arange(8)
+    w0 = initial_weights(idx, cfg).astype(np.float64)
+    U = {(v, p): -float(np.float32(cfg.lr)) * gradient(idx, v, p, cfg).astype(np.float64)
+         for v in range(cfg.num_vw) for p in range(1, cfg.waves * cfg.Nm + 1)}
+
+    def version(v, a_v, prefix):
+        tot = w0.copy()
+        for q in range(1, a_v + 1):
+            tot += U[(v, q)]
+        for (vv, c) in prefix:
+            if vv != v:
+                lo, hi = wave_range(c, cfg.Nm)
+                for q in range(lo, hi + 1):
+                    tot += U[(vv, q)]
+        return tot
+
+    root = WSPOracle(cfg, idx, record_snapshots=True)
+    for v in range(cfg.num_vw):
+        for p in range(1, min(cfg.Nm, root.last_p) + 1):
+            root.start(0, v, p)
+    memo = {}
+    stats = {"states": 0, "starts": 0}
+
+    def enabled(sm):
+        steps = []
+        for v in range(cfg.num_vw):
+            if sm.completed[v] < sm.started[v]:
+                steps.append(("C", v))
+            if sm.at_gate[v] and sm.gate_open(v)[0]:
+                steps.append(("A", v))
+        return steps
+
+    def apply(sm, step):
+        kind, v = step
+        if kind == "C":
+            p = sm.completed[v] + 1
+            wave_end, start_next = sm.complete(0, v, p)
+            if wave_end:
+                sm.push(0, v, (p - 1) // cfg.Nm)
+            if start_next:
+                sm.start(0, v, p + cfg.Nm)
+        else:
+            sm.try_admit(0, v)
+
+    def check(sm, n_snap_before):
+        for (t, v, p, snap), (v2, p2, a_v, held_K) in zip(
+                sm.snapshots[n_snap_before:], sm.start_versions[n_snap_before:]):
+            assert (v, p) == (v2, p2)
+            if cfg.local_semantics == LOCAL_STRICT:
+                assert a_v == max(0, p - cfg.Nm)
+            assert np.array_equal(snap.astype(np.float64),
+                                  version(v, a_v, sm.commit[:held_K]))
+            stats["starts"] += 1
+        assert max(sm.c_local) - min(sm.c_local) <= cfg.D + 1
+
+    def count(sm):
+        k = _key(sm)
+        if k in memo:
+            return memo[k]
+        stats["states"] += 1
+        steps = enabled(sm)
+        if not steps:
+            assert sm.done(), "stuck state"
+            allp = [(v, q) for v in range(cfg.num_vw) for q in range(1, sm.last_p + 1)]
+            tot = w0.copy()
+            for vq in allp:
+                tot += U[vq]
+            assert np.array_equal(sm.wg.astype(np.float64), tot)
+            memo[k] = 1
+            return 1
+        total = 0
+        for st in steps:
+            nxt = copy.deepcopy(sm)
+            n0 = len(nxt.snapshots)
+            apply(nxt, st)
+            check(nxt, n0)
+            # drop history that the key does not cover, to keep copies small
+            nxt.snapshots, nxt.start_versions, nxt.trace = [], [], []
+            total += count(nxt)
+        memo[k] = total
+        return total
+
+    n = count(root)
+    return n, stats
+
+
+def _cfg(Nm, D, policy=PULL_EAGER, sem=LOCAL_STRICT):
+    return WSPConfig("bf", 2, Nm, D, 8, 3, (1, 1), lr=2.0 ** -6,
+                     grad_mode=GRAD_DYADIC, w0_mode=W0_PHILOX,
+                     pull_policy=policy, local_semantics=sem)
+
+
+@pytest.mark.parametrize("D,expected", [(0, 72), (1, 240), (2, 252), (3, 252)])
+def test_bruteforce_nm1(D, expected):
+    """N_m=1: D>=2 leaves the two 5-step sequences unconstrained, C(10,5)=252
+    (closed form); D=0/1 counts cross-check SURVEY.md 0.4 [scratch] 6."""
+    n, _ = explore(_cfg(1, D))
+    assert n == expected
+
+
+@pytest.mark.parametrize("D,expected", [(0, 70400), (1, 200704), (2, 205920)])
+def test_bruteforce_nm2(D, expected):
+    """N_m=2, 2 VW x 3 waves x 8 params; counts cross-check SURVEY.md [scratch] 6."""
+    n, stats = explore(_cfg(2, D))
+    assert n == expected
+    assert stats["starts"] > 0
+
+
+@pytest.mark.parametrize("policy,sem", [(PULL_LAZY, LOCAL_STRICT),
+                                        (PULL_EAGER, LOCAL_AT_LEAST),
+                                        (PULL_LAZY, LOCAL_AT_LEAST)])
+@pytest.mark.parametrize("D", [0, 1])
+def test_bruteforce_policies(policy, sem, D):
+    """The same exact version-set checks under LAZY pulls and the
+    paper-literal AT_LEAST local semantics. LAZY admits without a
+    pull when the held version suffices, so the path set is the same."""
+    n, _ = explore(_cfg(2, D, policy, sem))
+    assert n == {0: 70400, 1: 200704}[D]
+
+
+@pytest.mark.parametrize("D,expected", [(0, 22415400), (1, 56362878), (2, 57139992)])
+def test_bruteforce_nm3(D, expected):
+    """N_m=3 (memoised state space); counts cross-check SURVEY.md [scratch] 6
+    (22.4M / 56.4M / 57.1M)."""
+    n, _ = explore(_cfg(3, D))
+    assert n == expected
+
+
+def test_pins_catch_plausible_mistakes(monkeypatch):
+    """The brute-force pin fails for plausible oracle bugs: an off-by-one gate
+    (D+1 instead of D), and a wave aggregate that drops its first minibatch."""
+    orig_gate = WSPOracle.gate_open
+
+    def loose_gate(self, v):
+        ok, pull = orig_gate(self, v)
+        return (self.c_local[v] - self.c_global <= self.cfg.D + 1), pull
+
+    monkeypatch.setattr(WSPOracle, "gate_open", loose_gate)
+    with pytest.raises(AssertionError):
+        n, _ = explore(_cfg(2, 0))
+        assert n == 70400
+    monkeypatch.setattr(WSPOracle, "gate_open", orig_gate)
+
+    orig_complete = WSPOracle.complete
+
+    def dropping_complete(self, t, v, p):
+        out = orig_complete(self, t, v, p)
+        if (p - 1) % self.cfg.Nm == 0:
+            self.acc[v] = np.zeros_like(self.acc[v])     # forgets u of the 1st minibatch
+        return out
+
+    monkeypatch.setattr(WSPOracle, "complete", dropping_complete)
+    with pytest.raises(AssertionError):
+        explore(_cfg(2, 1))
