@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the WSP synchronization hot path (HetPipe, arXiv 2005.14038).
+
+Metric (BASELINE.json): synced params/sec (and wave-sync latency) vs the
+HBM roofline. A STEP is one WSP round of the deterministic schedule: every VW
+completes one wave of N_m minibatches (accumulate + fold), pushes it, the PS
+applies it and the VW pulls under the staleness bound D -- all of SURVEY.md
+8(a) rows a1-a8 -- i.e. the controller advances until N more pushes are
+committed. value = pushes committed in the timed region x P / device time.
+
+Workload at N=1: BASELINE.json configs[1] = C2, 4 VWs with Node-Partition
+speeds, N_m=4, D=0, 60,192,808 params (ResNet-152 size), FLOAT synthetic
+gradients (Philox). At N>1 the same model is sharded ED-local over the ranks
+(each rank owns P/N params of every VW and the PS shard; no exchange exists,
+PAPER.md P:104-106), so scaling is STRONG (fixed model).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hetpipe|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from workloads import CONFIGS, GRAD_EXTERNAL, even_shards  # noqa: E402
+
+METRIC = "synced params/sec"
+UNIT = "params/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _ncu_traffic(cfg_name):
+    """dram read+write bytes per launch of the dominant kernel from the committed
+    `ncu --set full` summary (profiles/ncu_summary.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        return s.get("traffic_bytes_per_launch", {}).get(cfg_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sms, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9 or parts[1] != str(self.index):
+                continue
+            try:
+                sms.append(float(parts[2]))
+                mx.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sms) if sms else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(cfg, params=1 << 21, rounds=4):
+    """The oracle as it stands (numpy, one thread) on a bounded sample of the
+    same workload: the first `params` params of the C2 schedule for `rounds`
+    rounds. Returns synced params/s of the sample."""
+    import numpy as np
+    from oracle import run_schedule
+    c = cfg.replace(waves=rounds)
+    marks = []
+    t0 = time.perf_counter()
+    run_schedule(c, idx=np.arange(min(params, c.nparams)),
+                 on_tick=lambda t, sm: marks.append((time.perf_counter(), len(sm.commit))))
+    dt = time.perf_counter() - t0
+    commits = marks[-1][1]
+    return {"value": commits * min(params, c.nparams) / dt, "unit": UNIT, "cores": 1,
+            "kind": "oracle",
+            "sample": f"{cfg.name} schedule on params [0,{min(params, c.nparams)}) for "
+                      f"{rounds} rounds ({commits} pushes), numpy single thread, {dt:.1f} s"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the CPU oracle timed on the host, each step one WSP
+    round of the same schedule over a bounded param sample."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import numpy as np
+    from oracle import run_schedule
+    sample = args.ref_params
+    c = cfg.replace(waves=args.warmup + args.steps + 1)
+    N = c.num_vw
+    marks = {}
+    t_start = [None]
+
+    def on_tick(t, sm):
+        k = len(sm.commit)
+        if k >= N * args.warmup and t_start[0] is None:
+            t_start[0] = (time.perf_counter(), k)
+        if k >= N * (args.warmup + args.steps) and "end" not in marks:
+            marks["end"] = (time.perf_counter(), k)
+            raise StopIteration
+
+    try:
+        run_schedule(c, idx=np.arange(sample), on_tick=on_tick)
+    except StopIteration:
+        pass
+    (t0, k0), (t1, k1) = t_start[0], marks["end"]
+    dt = t1 - t0
+    value = (k1 - k0) * sample / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "num_vw": N, "Nm": c.Nm, "D": c.D,
+                   "nparams": c.nparams, "sample_params": sample, "tau": list(c.tau)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"first {sample} params of {cfg.name}, one WSP round per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hetpipe", choices=["hetpipe", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-params", type=int, default=1 << 18)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_14038_b200 import hetpipe
+
+    ws, rank, local = _dist()
+    if ws != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    b = even_shards(cfg.nparams, ws)
+    lo, hi = b[rank], b[rank + 1]
+    N = cfg.num_vw
+    waves = args.warmup + args.steps + 2
+    run_cfg = cfg.replace(waves=waves)
+    stream = torch.cuda.current_stream(local)
+    ctx = hetpipe.Context(hetpipe.config_from(
+        run_cfg, param_begin=lo, param_count=hi - lo, device=local,
+        stream=stream.cuda_stream))
+    ctx.trace_enable(False)
+    ctx.schedule_begin(run_cfg.tau, run_cfg.latency())
+    sampler = ClockSampler(local)
+    ctx.schedule_advance(N * args.warmup)
+    torch.cuda.synchronize()
+    barrier()
+    st0 = ctx.stats()
+    ctx.profile_enable(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    ev0.record(stream)
+    for k in range(args.steps):
+        ctx.schedule_advance(N * (args.warmup + k + 1))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    kern_ms, kern_bytes, kern_launches = ctx.profile_read()
+    st1 = ctx.stats()
+    commits = st1.commits - st0.commits
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = commits * cfg.nparams / (ms_max / 1e3)
+    launches = st1.launches - st0.launches
+    sync_waits = [int(x) for x in st1.wait_ticks[:N]]
+    ctx.close()
+    del ctx
+    torch.cuda.empty_cache()
+
+    # ---------------- e2e: host gradients in, w_global out, through the C-ABI
+    e2e = None
+    if not args.no_e2e:
+        e_steps = max(1, args.e2e_steps)
+        ecfg = cfg.replace(waves=3 + e_steps + 1)
+        nloc = hi - lo
+        host = [torch.empty(nloc, dtype=torch.float32, pin_memory=True) for _ in range(4)]
+        rng = np.random.default_rng(cfg.seed)
+        for h in host:
+            h.numpy()[:] = (rng.random(nloc, dtype=np.float32) - np.float32(0.5))
+        out = torch.empty(nloc, dtype=torch.float32, pin_memory=True)
+        ectx = hetpipe.Context(hetpipe.config_from(
+            ecfg, param_begin=lo, param_count=nloc, device=local, grad_mode=GRAD_EXTERNAL,
+            stream=stream.cuda_stream))
+        ectx.trace_enable(False)
+        ectx.schedule_set_host_grads([h.numpy() for h in host])
+        ectx.schedule_begin(ecfg.tau, ecfg.latency())
+        ectx.schedule_advance(N * 3)
+        ectx.read_weights(-1, out=out.numpy())
+        torch.cuda.synchronize()
+        barrier()
+        s0 = ectx.stats()
+        t0 = time.perf_counter()
+        for k in range(e_steps):
+            ectx.schedule_advance(N * (3 + k + 1))
+            ectx.read_weights(-1, out=out.numpy())      # D2H of the step's result
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        s1 = ectx.stats()
+        tt = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+        if ws > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        ecommits = s1.commits - s0.commits
+        completes_per_step = N * cfg.Nm
+        e2e = {"value": ecommits * cfg.nparams / dt, "unit": UNIT,
+               "h2d_bytes_per_step": completes_per_step * nloc * 4 * ws,
+               "d2h_bytes_per_step": nloc * 4 * ws,
+               "steps": e_steps, "ms_per_step": 1e3 * dt / e_steps,
+               "path": "hp_schedule_set_host_grads + hp_schedule_advance + hp_read_weights(-1)"}
+        ectx.close()
+
+    if rank != 0:
+        if ws > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_kind = _peaks()
+    achieved = kern_bytes / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else 0.0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "num_vw": N, "Nm": cfg.Nm, "D": cfg.D,
+                   "nparams": cfg.nparams, "tau": list(cfg.tau), "placement":
+                   "ED-local shards" if ws > 1 else "single GPU",
+                   "grad": "Philox FLOAT in-kernel", "pull": "EAGER", "local": "STRICT",
+                   "l2": "inputs larger than L2 (>= 13 x 230 MiB buffers per GPU)"},
+        "images_per_sec_equiv": commits * 32 * cfg.Nm / (ms_max / 1e3),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _ncu_traffic(cfg.name),
+                     "peak_kind": peak_kind, "kernel": "hp::tick_kernel (all launches)",
+                     "kernel_ms": kern_ms, "launches": kern_launches,
+                     "alg_bytes_per_launch": kern_bytes / max(kern_launches, 1)},
+        "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "wait_ticks_per_vw": sync_waits,
+        "e2e": e2e,
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

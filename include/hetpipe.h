@@ -1,0 +1,198 @@
+/*
+ * hetpipe.h -- C ABI of the B200-native WSP (Wave Synchronous Parallel) hot path
+ * of HetPipe (Park et al., arXiv 2005.14038, USENIX ATC'20).
+ *
+ * Citations: "P:n" = line n of the paper text (/root/reference/PAPER.md, not
+ * shipped); section numbers are the paper's. Readings of silent or ambiguous
+ * passages are DESIGN.md "Readings" Z1..Z20.
+ *
+ * What the library computes (paper sections 4-5):
+ *   COMPLETE(v,p)  u_p = fl(-lr * g_p); the open wave's aggregate
+ *                  u~ (+)= u_p (summed in completion order, Z1);
+ *                  w_local(v) = w_local(v) + u_p, folded "just in
+ *                  time" so that minibatch p reads exactly its own updates
+ *                  1..p-N_m (STRICT, Z3) or at least those (AT_LEAST).
+ *   PUSH(v,c)      at the end of clock c the PS applies w_global = w_global + u~
+ *                  (P:928-929), optionally heavy-ball momentum (Z11); c_local(v)
+ *                  = c+1, c_global = min over VWs.
+ *   GATE/PULL(v)   the next gated minibatch (c+2)*N_m may start iff
+ *                  c_local - c_global <= D (Z7); then w_local(v) =
+ *                  w_global. LAZY pulls only when the held version is
+ *                  older than the bound requires.
+ *
+ * Layout and ownership:
+ *   * All model state lives in device memory owned by the context: w_global and
+ *     (momentum) m of this rank's parameter shard, and per VW w_local plus a ring
+ *     of acc slots (u~ of waves pushed but not yet applied). fp32, contiguous,
+ *     16-byte aligned; the rank owns global params [param_begin, param_begin +
+ *     param_count) of every buffer (ED-local placement).
+ *   * Param i's synthetic gradient is Philox4x32-10(counter = (i>>2, v, p, 0),
+ *     key = (seed lo32, seed hi32)) word i&3, i the GLOBAL index (Z9).
+ *   * Device work is stream-ordered and asynchronous on the context's stream;
+ *     only hp_sync / hp_read_weights / hp_profile_read block the caller.
+ *
+ * Errors: every call validates its arguments and the protocol state before it
+ * changes anything (no partial effects on error). HP_OK and HP_WOULD_BLOCK are
+ * non-errors. A CUDA failure is sticky: every later call returns HP_ERR_CUDA and
+ * hp_last_error() holds the text. No C++ exception crosses this ABI. A context
+ * is single-threaded (one host controller thread per rank).
+ */
+#ifndef HETPIPE_H_
+#define HETPIPE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hp_ctx hp_ctx; /* opaque; owns all device state of one rank */
+
+typedef enum {
+  HP_OK = 0,
+  HP_WOULD_BLOCK = 1,     /* gate closed: nothing changed */
+  HP_ERR_INVALID = -1,    /* bad argument */
+  HP_ERR_PROTOCOL = -2,   /* out-of-order / duplicate / incomplete */
+  HP_ERR_CUDA = -3,       /* sticky CUDA failure */
+  HP_ERR_COMM = -4,       /* reserved: inter-GPU transport failure */
+  HP_ERR_OOM = -5,        /* device allocation failed */
+  HP_ERR_STATE = -6       /* call not valid in this context state */
+} hp_status;
+
+enum { HP_GRAD_FLOAT = 0, HP_GRAD_DYADIC = 1, HP_GRAD_EXTERNAL = 2 };
+enum { HP_W0_ZERO = 0, HP_W0_PHILOX = 1 };
+enum { HP_PULL_EAGER = 0, HP_PULL_LAZY = 1 };
+enum { HP_LOCAL_STRICT = 0, HP_LOCAL_AT_LEAST = 1 };
+enum { HP_APPLY_DEFERRED = 0, HP_APPLY_ON_ARRIVAL = 1 };
+
+typedef struct {
+  int32_t num_vw;          /* N virtual workers, 1..8 */
+  int32_t Nm;              /* minibatches per wave, s_local = Nm-1, 1..64 */
+  int32_t D;               /* clock-distance threshold, >= 0 */
+  int32_t waves;           /* W: minibatches > W*Nm never start (Z16); default 2^30 */
+  int64_t nparams;         /* P, global model size */
+  int64_t param_begin;     /* first global param owned by this rank (multiple of 32) */
+  int64_t param_count;     /* params owned by this rank; -1 = nparams - param_begin */
+  float lr;                /* u = fl(-lr*g) (Z2) */
+  float momentum;          /* PS heavy-ball mu; 0 = plain SGD apply (Z11) */
+  uint64_t seed;           /* Philox key */
+  int32_t grad_mode;       /* HP_GRAD_* */
+  int32_t w0_mode;         /* HP_W0_* (Z8) */
+  int32_t pull_policy;     /* HP_PULL_* (Z6) */
+  int32_t local_semantics; /* HP_LOCAL_* (Z3) */
+  int32_t apply_mode;      /* HP_APPLY_* (Z4): defer applies to the observing pull */
+  int32_t acc_slots;       /* acc ring depth R per VW, 2..8 (default 2) */
+  int32_t device;          /* CUDA device ordinal */
+  void* stream;            /* cudaStream_t to run on; NULL = library-owned stream */
+} hp_config;
+
+/* Fill cfg with defaults (N=1, Nm=1, D=0, lr=0.01, FLOAT grads, PHILOX w0,
+   EAGER, STRICT, deferred applies, R=2, device 0, library stream). */
+void hp_config_default(hp_config* cfg);
+
+/* north_star entry point: hp_init(num_vw, Nm, D, nparams, lr) with the other
+   fields at their defaults. Allocates ~ (N*(1+R) + 1 (+1 momentum)) * 4 * P
+   bytes of device memory and initialises w_global = w_local(v) = w0.
+   Errors: HP_ERR_INVALID, HP_ERR_OOM, HP_ERR_CUDA. On error *out = NULL. */
+hp_status hp_init(hp_ctx** out, int32_t num_vw, int32_t Nm, int32_t D,
+                  int64_t nparams, float lr);
+hp_status hp_init_ex(hp_ctx** out, const hp_config* cfg);
+
+/* COMPLETE(vw, p). Requires p == completed(vw)+1 and p
+   already started, else HP_ERR_PROTOCOL. grad: HP_GRAD_EXTERNAL only -- device
+   fp32[param_count] for this rank's shard, BORROWED until vw's next admission
+   (a deferred STRICT fold may re-read it); must be NULL otherwise. If p ends a
+   wave the caller must push that wave next (hp_push_wave). The START of
+   p+N_m (when not gated) is implicit in this call. */
+hp_status hp_accumulate_minibatch(hp_ctx* ctx, int32_t vw, int64_t p, const float* grad);
+
+/* As above with a HOST gradient buffer (pinned for overlap): copied into a
+   library-owned device slot on the context stream before the kernel reads it. */
+hp_status hp_accumulate_minibatch_host(hp_ctx* ctx, int32_t vw, int64_t p,
+                                       const float* host_grad);
+
+/* PUSH(vw, c): requires c == c_local(vw) and all N_m minibatches of
+   wave c completed, else HP_ERR_PROTOCOL (duplicate, out-of-order or
+   incomplete push). Appends (vw,c) to the commit log; the PS apply runs in
+   commit order, either immediately or deferred to the first pull / read that
+   observes w_global (bit-identical either way, Z4). Advances c_local(vw) and
+   c_global. */
+hp_status hp_push_wave(hp_ctx* ctx, int32_t vw, int64_t c);
+
+/* CLOCK: report c_local(vw) and c_global (either pointer may be NULL). Returns
+   HP_WOULD_BLOCK iff vw waits at its gate and the gate is closed. */
+hp_status hp_clock(hp_ctx* ctx, int32_t vw, int64_t* c_local, int64_t* c_global);
+
+/* GATE/PULL(vw): only valid while vw waits at its gate (HP_ERR_PROTOCOL
+   otherwise). If the gate is closed returns HP_WOULD_BLOCK and changes nothing
+   but the trace (first BLOCK). Otherwise pulls per the policy (EAGER always;
+   LAZY only if held_g < c_local - D), starts minibatch (c+2)*N_m and replays the
+   minibatches that completed while it waited (Z17). Never waits inside. */
+hp_status hp_pull(hp_ctx* ctx, int32_t vw);
+
+/* End of a tick: launch the fused kernel for the ops issued since the last tick
+   (one launch per tick, Z5 phase order) and emit the tick's START records. */
+hp_status hp_tick_end(hp_ctx* ctx);
+
+/* Stamp subsequent trace records with tick t (wait accounting uses it). */
+hp_status hp_set_tick(hp_ctx* ctx, int64_t t);
+
+/* The deterministic tick controller: START(p) for
+   p <= N_m at t=0, complete(p) = max(start(p) + lat[v], complete(p-1) + tau[v]);
+   phases COMPLETE -> PUSH/APPLY -> GATE/PULL -> START per tick (Z5).
+   tau, lat: host int64[num_vw]; lat NULL = N_m * tau. */
+hp_status hp_schedule_begin(hp_ctx* ctx, const int64_t* tau, const int64_t* lat);
+/* Run ticks until the commit log holds >= target_commits pushes or the run is
+   complete; *commits (may be NULL) receives the count reached. */
+hp_status hp_schedule_advance(hp_ctx* ctx, int64_t target_commits, int64_t* commits);
+/* Whole run: begin + advance to num_vw*waves pushes + final apply flush. */
+hp_status hp_run_schedule(hp_ctx* ctx, const int64_t* tau, const int64_t* lat);
+/* HP_GRAD_EXTERNAL under the controller: COMPLETE(v,p) copies host buffer
+   host_bufs[(v*W*N_m + p) % n] (each fp32[param_count]) to the device. */
+hp_status hp_schedule_set_host_grads(hp_ctx* ctx, const float* const* host_bufs, int32_t n);
+
+/* Flush every pending op and apply, then synchronise the stream. */
+hp_status hp_sync(hp_ctx* ctx);
+
+/* Copy count fp32 of a buffer, from local offset `offset`, to host memory.
+   which = -1: w_global (pending applies are flushed first); -2: momentum m;
+   0..N-1: w_local(which) as its next START will read it (while that VW waits at
+   its gate, STRICT folds deferred to admission are not yet in it). Blocking. */
+hp_status hp_read_weights(hp_ctx* ctx, int32_t which, int64_t offset, int64_t count,
+                          float* host_dst);
+
+/* Version trace, one line per event "t phase vw kind p c c_local c_global a_v
+   held_g held_K\n". Writes to path (NULL/"" = keep). */
+hp_status hp_trace_dump(hp_ctx* ctx, const char* path);
+hp_status hp_trace_enable(hp_ctx* ctx, int32_t enable);
+
+typedef struct {
+  int64_t commits;          /* pushes committed */
+  int64_t applied;          /* pushes applied on the device */
+  int64_t launches;         /* kernel launches issued */
+  int64_t ticks;            /* ticks processed by the controller */
+  double alg_bytes;         /* algorithmic HBM bytes of all launches */
+  int64_t wait_ticks[8];    /* per VW simulated wait */
+  int64_t pulls[8];         /* per VW pulls */
+} hp_stats;
+hp_status hp_get_stats(hp_ctx* ctx, hp_stats* out);
+
+/* Per-launch CUDA events on the context stream (enable before the timed region;
+   read after it): total kernel ms, algorithmic bytes and launches since enable. */
+hp_status hp_profile_enable(hp_ctx* ctx, int32_t enable);
+hp_status hp_profile_read(hp_ctx* ctx, double* kernel_ms, double* alg_bytes,
+                          int64_t* launches);
+
+/* Closed forms of section 5 (no context needed). */
+int64_t hp_s_global(int32_t Nm, int32_t D);                  /* (D+1)*Nm + Nm - 2 */
+int64_t hp_version_floor(int64_t p, int32_t Nm, int32_t D);  /* max(0, p - s_global - 1) */
+
+const char* hp_last_error(const hp_ctx* ctx);   /* NULL ctx: last init error */
+const char* hp_version(void);
+void hp_finalize(hp_ctx* ctx);                  /* frees everything; NULL ok */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HETPIPE_H_ */

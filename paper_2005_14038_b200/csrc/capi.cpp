@@ -1,0 +1,369 @@
+// capi.cpp -- extern "C" boundary of libhetpipe (include/hetpipe.h) and the
+// deterministic tick controller (reading Z13).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/hetpipe.h"
+#include "engine.h"
+
+namespace hp {
+
+// Tick controller: complete(p) = max(start(p) + lat_v, complete(p-1) + tau_v);
+// the events of one tick run in the phases COMPLETE -> PUSH/APPLY -> GATE/PULL ->
+// START, ascending VW inside a phase (reading Z5). A blocked VW is re-examined
+// at every later tick ("may need to wait").
+class Controller {
+ public:
+  explicit Controller(Engine* e) : e_(e) {}
+  hp_status begin(const int64_t* tau, const int64_t* lat) {
+    const auto& cfg = e_->cfg();
+    const int N = cfg.num_vw;
+    tau_.assign(tau, tau + N);
+    lat_.resize(N);
+    for (int v = 0; v < N; ++v) {
+      if (tau_[v] < 1) return e_->fail(HP_ERR_INVALID, "tau must be >= 1");
+      lat_[v] = lat ? lat[v] : (int64_t)cfg.Nm * tau_[v];
+      if (lat_[v] < 1) return e_->fail(HP_ERR_INVALID, "lat must be >= 1");
+    }
+    ctime_.assign(N, std::vector<int64_t>((size_t)e_->last_p() + 2, -1));
+    events_.clear();
+    for (int v = 0; v < N; ++v)
+      for (int64_t p = 1; p <= std::min<int64_t>(cfg.Nm, e_->last_p()); ++p) schedule(0, v, p);
+    active_ = true;
+    return HP_OK;
+  }
+  hp_status advance(int64_t target) {
+    if (!active_) return e_->fail(HP_ERR_STATE, "hp_schedule_begin not called");
+    while (!e_->done() && e_->commits() < target) {
+      if (events_.empty()) return e_->fail(HP_ERR_STATE, "deadlock: no pending completion");
+      if (hp_status st = tick()) return st;
+    }
+    return HP_OK;
+  }
+  void set_host_grads(const float* const* bufs, int n) { host_.assign(bufs, bufs + n); }
+
+ private:
+  void schedule(int64_t t, int v, int64_t p) {
+    int64_t ct = t + lat_[v];
+    if (p > 1 && ctime_[v][p - 1] >= 0) ct = std::max(ct, ctime_[v][p - 1] + tau_[v]);
+    ctime_[v][p] = ct;
+    events_[ct].push_back({v, p});
+  }
+  hp_status tick() {
+    auto it = events_.begin();
+    const int64_t t = it->first;
+    std::vector<std::pair<int, int64_t>> comps = std::move(it->second);
+    events_.erase(it);
+    std::sort(comps.begin(), comps.end());
+    e_->set_tick(t);
+    const auto& cfg = e_->cfg();
+    std::vector<std::pair<int, int64_t>> pushes;
+    for (auto& vp : comps) {  // COMPLETE phase
+      bool wave_end = false;
+      const float* hg = nullptr;
+      if (!host_.empty()) {
+        const int64_t k = ((int64_t)vp.first * e_->last_p() + vp.second) % (int64_t)host_.size();
+        hg = host_[k];
+      }
+      if (hp_status st = e_->complete(vp.first, vp.second, nullptr, hg, &wave_end)) return st;
+      if (wave_end) pushes.push_back({vp.first, (vp.second - 1) / cfg.Nm});
+    }
+    for (auto& vc : pushes)  // PUSH/APPLY phase
+      if (hp_status st = e_->push(vc.first, vc.second)) return st;
+    for (int v = 0; v < cfg.num_vw; ++v) {  // GATE/PULL phase
+      if (!e_->at_gate(v)) continue;
+      std::vector<int64_t> started;
+      hp_status st = e_->admit(v, &started);
+      if (st < 0) return st;
+      for (int64_t p : started) schedule(t, v, p);
+    }
+    std::vector<std::pair<int, int64_t>> ungated;  // START phase
+    if (hp_status st = e_->tick_end(&ungated)) return st;
+    for (auto& vp : ungated) schedule(t, vp.first, vp.second);
+    return HP_OK;
+  }
+
+  Engine* e_;
+  std::vector<int64_t> tau_, lat_;
+  std::vector<std::vector<int64_t>> ctime_;
+  std::map<int64_t, std::vector<std::pair<int, int64_t>>> events_;
+  std::vector<const float*> host_;
+  bool active_ = false;
+};
+
+}  // namespace hp
+
+struct hp_ctx {
+  std::unique_ptr<hp::Engine> eng;
+  std::unique_ptr<hp::Controller> ctl;
+};
+
+namespace {
+std::string g_init_error;
+
+hp_status guard_device(hp_ctx* ctx) {
+  if (!ctx || !ctx->eng) return HP_ERR_INVALID;
+  if (ctx->eng->sticky()) return ctx->eng->sticky();
+  cudaSetDevice(ctx->eng->cfg().device);
+  return HP_OK;
+}
+}  // namespace
+
+#define HP_ENTRY(ctx)                              \
+  if (hp_status _s = guard_device(ctx)) return _s; \
+  try {
+#define HP_EXIT(ctx)                                                  \
+  }                                                                   \
+  catch (const std::bad_alloc&) {                                     \
+    return ctx->eng->fail(HP_ERR_OOM, "host allocation failed");      \
+  }                                                                   \
+  catch (...) {                                                       \
+    return ctx->eng->fail(HP_ERR_INVALID, "unexpected C++ exception"); \
+  }
+
+extern "C" {
+
+void hp_config_default(hp_config* c) {
+  if (!c) return;
+  memset(c, 0, sizeof *c);
+  c->num_vw = 1;
+  c->Nm = 1;
+  c->D = 0;
+  c->waves = 1 << 30;
+  c->nparams = 0;
+  c->param_begin = 0;
+  c->param_count = -1;
+  c->lr = 0.01f;
+  c->momentum = 0.f;
+  c->seed = 200514038ull;
+  c->grad_mode = HP_GRAD_FLOAT;
+  c->w0_mode = HP_W0_PHILOX;
+  c->pull_policy = HP_PULL_EAGER;
+  c->local_semantics = HP_LOCAL_STRICT;
+  c->apply_mode = HP_APPLY_DEFERRED;
+  c->acc_slots = 2;
+  c->device = 0;
+  c->stream = nullptr;
+}
+
+hp_status hp_init_ex(hp_ctx** out, const hp_config* cfg_in) {
+  if (!out || !cfg_in) return HP_ERR_INVALID;
+  *out = nullptr;
+  hp_config cfg = *cfg_in;
+  if (cfg.param_count < 0) cfg.param_count = cfg.nparams - cfg.param_begin;
+  const char* bad = nullptr;
+  if (cfg.num_vw < 1 || cfg.num_vw > 8) bad = "num_vw must be 1..8";
+  else if (cfg.Nm < 1 || cfg.Nm > 32) bad = "Nm must be 1..32";
+  else if (cfg.D < 0) bad = "D must be >= 0";
+  else if (cfg.waves < 1) bad = "waves must be >= 1";
+  else if (cfg.nparams < 0 || cfg.nparams >= (1ll << 34)) bad = "nparams must be in [0, 2^34)";
+  else if (cfg.param_begin < 0 || cfg.param_begin % 32) bad = "param_begin must be a multiple of 32";
+  else if (cfg.param_count < 0 || cfg.param_begin + cfg.param_count > cfg.nparams) bad = "bad shard";
+  else if (cfg.acc_slots < 2 || cfg.acc_slots > 8) bad = "acc_slots must be 2..8";
+  else if (cfg.grad_mode < 0 || cfg.grad_mode > 2) bad = "bad grad_mode";
+  else if (cfg.w0_mode < 0 || cfg.w0_mode > 1) bad = "bad w0_mode";
+  else if (cfg.pull_policy < 0 || cfg.pull_policy > 1) bad = "bad pull_policy";
+  else if (cfg.local_semantics < 0 || cfg.local_semantics > 1) bad = "bad local_semantics";
+  else if (cfg.apply_mode < 0 || cfg.apply_mode > 1) bad = "bad apply_mode";
+  if (bad) {
+    g_init_error = bad;
+    return HP_ERR_INVALID;
+  }
+  hp_ctx* ctx = nullptr;
+  try {
+    ctx = new hp_ctx;
+    ctx->eng.reset(new hp::Engine(cfg));
+    ctx->ctl.reset(new hp::Controller(ctx->eng.get()));
+  } catch (...) {
+    delete ctx;
+    g_init_error = "host allocation failed";
+    return HP_ERR_OOM;
+  }
+  hp_status st = ctx->eng->init();
+  if (st != HP_OK) {
+    g_init_error = ctx->eng->error();
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return HP_OK;
+}
+
+hp_status hp_init(hp_ctx** out, int32_t num_vw, int32_t Nm, int32_t D, int64_t nparams,
+                  float lr) {
+  hp_config c;
+  hp_config_default(&c);
+  c.num_vw = num_vw;
+  c.Nm = Nm;
+  c.D = D;
+  c.nparams = nparams;
+  c.lr = lr;
+  return hp_init_ex(out, &c);
+}
+
+hp_status hp_accumulate_minibatch(hp_ctx* ctx, int32_t vw, int64_t p, const float* grad) {
+  HP_ENTRY(ctx)
+  return ctx->eng->complete(vw, p, grad, nullptr, nullptr);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_accumulate_minibatch_host(hp_ctx* ctx, int32_t vw, int64_t p,
+                                       const float* host_grad) {
+  HP_ENTRY(ctx)
+  if (!host_grad) return ctx->eng->fail(HP_ERR_INVALID, "host_grad is NULL");
+  return ctx->eng->complete(vw, p, nullptr, host_grad, nullptr);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_push_wave(hp_ctx* ctx, int32_t vw, int64_t c) {
+  HP_ENTRY(ctx)
+  return ctx->eng->push(vw, c);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_clock(hp_ctx* ctx, int32_t vw, int64_t* c_local, int64_t* c_global) {
+  HP_ENTRY(ctx)
+  return ctx->eng->clock(vw, c_local, c_global);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_pull(hp_ctx* ctx, int32_t vw) {
+  HP_ENTRY(ctx)
+  return ctx->eng->admit(vw, nullptr);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_tick_end(hp_ctx* ctx) {
+  HP_ENTRY(ctx)
+  return ctx->eng->tick_end(nullptr);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_set_tick(hp_ctx* ctx, int64_t t) {
+  HP_ENTRY(ctx)
+  ctx->eng->set_tick(t);
+  return HP_OK;
+  HP_EXIT(ctx)
+}
+
+hp_status hp_schedule_begin(hp_ctx* ctx, const int64_t* tau, const int64_t* lat) {
+  HP_ENTRY(ctx)
+  if (!tau) return ctx->eng->fail(HP_ERR_INVALID, "tau is NULL");
+  return ctx->ctl->begin(tau, lat);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_schedule_advance(hp_ctx* ctx, int64_t target, int64_t* commits) {
+  HP_ENTRY(ctx)
+  hp_status st = ctx->ctl->advance(target);
+  if (commits) *commits = ctx->eng->commits();
+  return st;
+  HP_EXIT(ctx)
+}
+
+hp_status hp_run_schedule(hp_ctx* ctx, const int64_t* tau, const int64_t* lat) {
+  HP_ENTRY(ctx)
+  if (!tau) return ctx->eng->fail(HP_ERR_INVALID, "tau is NULL");
+  if (hp_status st = ctx->ctl->begin(tau, lat)) return st;
+  if (hp_status st = ctx->ctl->advance(INT64_MAX)) return st;
+  return ctx->eng->flush_applies();
+  HP_EXIT(ctx)
+}
+
+hp_status hp_schedule_set_host_grads(hp_ctx* ctx, const float* const* bufs, int32_t n) {
+  HP_ENTRY(ctx)
+  if (ctx->eng->cfg().grad_mode != HP_GRAD_EXTERNAL)
+    return ctx->eng->fail(HP_ERR_STATE, "host gradients need HP_GRAD_EXTERNAL");
+  if (!bufs || n < 1) return ctx->eng->fail(HP_ERR_INVALID, "no host buffers");
+  for (int i = 0; i < n; ++i)
+    if (!bufs[i]) return ctx->eng->fail(HP_ERR_INVALID, "NULL host buffer");
+  ctx->ctl->set_host_grads(bufs, n);
+  return HP_OK;
+  HP_EXIT(ctx)
+}
+
+hp_status hp_sync(hp_ctx* ctx) {
+  HP_ENTRY(ctx)
+  return ctx->eng->sync();
+  HP_EXIT(ctx)
+}
+
+hp_status hp_read_weights(hp_ctx* ctx, int32_t which, int64_t offset, int64_t count,
+                          float* host_dst) {
+  HP_ENTRY(ctx)
+  return ctx->eng->read(which, offset, count, host_dst);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_trace_dump(hp_ctx* ctx, const char* path) {
+  HP_ENTRY(ctx)
+  if (!path || !*path) return HP_OK;
+  FILE* f = fopen(path, "w");
+  if (!f) return ctx->eng->fail(HP_ERR_INVALID, "cannot open trace path");
+  const std::string& t = ctx->eng->trace();
+  size_t w = fwrite(t.data(), 1, t.size(), f);
+  fclose(f);
+  if (w != t.size()) return ctx->eng->fail(HP_ERR_INVALID, "short trace write");
+  return HP_OK;
+  HP_EXIT(ctx)
+}
+
+hp_status hp_trace_enable(hp_ctx* ctx, int32_t enable) {
+  HP_ENTRY(ctx)
+  ctx->eng->set_trace(enable != 0);
+  return HP_OK;
+  HP_EXIT(ctx)
+}
+
+hp_status hp_get_stats(hp_ctx* ctx, hp_stats* out) {
+  HP_ENTRY(ctx)
+  if (!out) return ctx->eng->fail(HP_ERR_INVALID, "out is NULL");
+  ctx->eng->stats(out);
+  return HP_OK;
+  HP_EXIT(ctx)
+}
+
+hp_status hp_profile_enable(hp_ctx* ctx, int32_t enable) {
+  HP_ENTRY(ctx)
+  return ctx->eng->profile_enable(enable != 0);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_profile_read(hp_ctx* ctx, double* kernel_ms, double* alg_bytes, int64_t* launches) {
+  HP_ENTRY(ctx)
+  return ctx->eng->profile_read(kernel_ms, alg_bytes, launches);
+  HP_EXIT(ctx)
+}
+
+int64_t hp_s_global(int32_t Nm, int32_t D) {
+  // s_global = (D+1)(s_local+1) + s_local - 1 with s_local = Nm-1
+  return (int64_t)(D + 1) * Nm + (Nm - 1) - 1;
+}
+
+int64_t hp_version_floor(int64_t p, int32_t Nm, int32_t D) {
+  const int64_t f = p - (hp_s_global(Nm, D) + 1);
+  return f > 0 ? f : 0;
+}
+
+const char* hp_last_error(const hp_ctx* ctx) {
+  if (!ctx || !ctx->eng) return g_init_error.c_str();
+  return ctx->eng->error().c_str();
+}
+
+const char* hp_version(void) { return "hetpipe-wsp-b200 0.1 (sm_100a)"; }
+
+void hp_finalize(hp_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->eng) cudaSetDevice(ctx->eng->cfg().device);
+  delete ctx;
+}
+
+}  // extern "C"

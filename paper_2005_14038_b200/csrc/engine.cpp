@@ -1,0 +1,507 @@
+// engine.cpp -- WSP protocol engine (see engine.h). Host C++; device work is
+// one fused kernel launch per flushed batch (kernels.cu).
+#include "engine.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+namespace hp {
+
+namespace {
+int64_t wave_of(int64_t p, int Nm) { return (p - 1) / Nm; }
+}  // namespace
+
+Engine::Engine(const hp_config& cfg) : cfg_(cfg) {
+  N_ = cfg.num_vw;
+  Nm_ = cfg.Nm;
+  R_ = cfg.acc_slots;
+  W_ = cfg.waves;
+  last_p_ = W_ * (int64_t)Nm_;
+  begin_ = cfg.param_begin;
+  n_ = cfg.param_count;
+  vw_.resize(N_);
+}
+
+Engine::~Engine() {
+  for (auto e : ev_) cudaEventDestroy(e);
+  if (arena_) cudaFree(arena_);
+  for (auto& v : vw_)
+    for (float* g : v.grad_ring) cudaFree(g);
+  if (own_stream_ && stream_) cudaStreamDestroy(stream_);
+}
+
+hp_status Engine::fail(hp_status s, const std::string& msg) {
+  err_ = msg;
+  if (s == HP_ERR_CUDA) sticky_ = s;
+  return s;
+}
+
+hp_status Engine::check_cuda(int err, const char* what) {
+  if (err == cudaSuccess) return HP_OK;
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString((cudaError_t)err));
+  return fail(HP_ERR_CUDA, buf);
+}
+
+hp_status Engine::init() {
+  if (cudaSetDevice(cfg_.device) != cudaSuccess) return check_cuda(cudaGetLastError(), "cudaSetDevice");
+  if (cfg_.stream) {
+    stream_ = (cudaStream_t)cfg_.stream;
+  } else {
+    if (int e = cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking)) return check_cuda(e, "stream");
+    own_stream_ = true;
+  }
+  // arena: w_global, [m], per VW w_local + R acc slots; each 256-byte aligned
+  const size_t stride = ((size_t)std::max<int64_t>(n_, 1) * 4 + 255) / 256 * 256;
+  const size_t nbuf = 1 + (cfg_.momentum != 0.f ? 1 : 0) + (size_t)N_ * (1 + R_);
+  if (cudaMalloc(&arena_, stride * nbuf) != cudaSuccess) {
+    cudaGetLastError();
+    arena_ = nullptr;
+    return fail(HP_ERR_OOM, "device arena allocation failed");
+  }
+  char* base = (char*)arena_;
+  size_t k = 0;
+  wg_ = (float*)(base + stride * k++);
+  if (cfg_.momentum != 0.f) m_ = (float*)(base + stride * k++);
+  for (auto& v : vw_) {
+    v.wl = (float*)(base + stride * k++);
+    for (int r = 0; r < R_; ++r) v.acc.push_back((float*)(base + stride * k++));
+    v.grad_of_slot.assign(Nm_, nullptr);
+  }
+  const uint32_t k0 = (uint32_t)(cfg_.seed & 0xffffffffu), k1 = (uint32_t)(cfg_.seed >> 32);
+  hp_status st = check_cuda(
+      launch_init(wg_, n_, begin_, cfg_.w0_mode, cfg_.grad_mode, k0, k1, stream_), "init");
+  for (auto& v : vw_)
+    if (st == HP_OK)
+      st = check_cuda(launch_init(v.wl, n_, begin_, cfg_.w0_mode, cfg_.grad_mode, k0, k1, stream_),
+                      "init");
+  if (st == HP_OK && m_) st = check_cuda(cudaMemsetAsync(m_, 0, (size_t)n_ * 4, stream_), "memset");
+  if (st != HP_OK) return st;
+  // minibatches 1..Nm of every VW start at t=0 with w0
+  for (int v = 0; v < N_; ++v) {
+    for (int64_t p = 1; p <= std::min<int64_t>(Nm_, last_p_); ++p) {
+      vw_[v].started = p;
+      rec('S', v, "START", p, wave_of(p, Nm_));
+    }
+  }
+  return check_cuda(cudaStreamSynchronize(stream_), "init sync");
+}
+
+void Engine::rec(char phase, int v, const char* kind, int64_t p, int64_t c) {
+  if (!trace_on_) return;
+  const VW& s = vw_[v];
+  char buf[192];
+  int n = snprintf(buf, sizeof buf, "%lld %c %d %s %lld %lld %lld %lld %lld %lld %lld\n",
+                   (long long)tick_, phase, v, kind, (long long)p, (long long)c,
+                   (long long)s.c_local, (long long)c_global_, (long long)s.a,
+                   (long long)s.held_g, (long long)s.held_K);
+  trace_.append(buf, n);
+}
+
+std::pair<bool, bool> Engine::gate_open(int v) const {
+  const VW& s = vw_[v];
+  const bool within = s.c_local - c_global_ <= cfg_.D;
+  if (cfg_.pull_policy == HP_PULL_EAGER) return {within, true};
+  if (s.held_g >= s.c_local - cfg_.D) return {true, false}; // held version suffices
+  return {within, true};
+}
+
+bool Engine::done() const {
+  for (const auto& s : vw_)
+    if (s.c_local < W_) return false;
+  return true;
+}
+
+const float* Engine::fold_grad(int v, int64_t p) const {
+  if (cfg_.grad_mode != HP_GRAD_EXTERNAL) return nullptr;
+  return vw_[v].grad_of_slot[(p - 1) % Nm_];
+}
+
+// ---------------------------------------------------------------------------
+hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float* grad_host,
+                           bool* wave_end_out) {
+  if (sticky_) return sticky_;
+  if (v < 0 || v >= N_) return fail(HP_ERR_INVALID, "vw out of range");
+  VW& s = vw_[v];
+  if (p != s.completed + 1 || p > s.started || p > last_p_)
+    return fail(HP_ERR_PROTOCOL, "COMPLETE out of order or minibatch not started");
+  const bool ext = cfg_.grad_mode == HP_GRAD_EXTERNAL;
+  if (ext && !grad_dev && !grad_host) return fail(HP_ERR_INVALID, "EXTERNAL mode needs a gradient");
+  if (!ext && (grad_dev || grad_host)) return fail(HP_ERR_INVALID, "gradient given in synthetic mode");
+  if (grad_dev && ((uintptr_t)grad_dev & 15)) return fail(HP_ERR_INVALID, "gradient not 16-byte aligned");
+  // phase order inside a batch: COMPLETE < PUSH < PULL; one COMPLETE per VW
+  bool again = phase_ > kPhComplete;
+  for (auto& b : bc_) again |= b.v == v;
+  if (again || (int)bc_.size() >= kMaxC)
+    if (hp_status st = flush()) return st;
+  const int64_t c = wave_of(p, Nm_);
+  const int slot = (int)(c % R_);
+  const bool first = (p - 1) % Nm_ == 0;
+  if (first) {  // the slot must not hold a pushed wave that is not applied yet
+    bool busy = false;
+    for (auto& a : pending_applies_) busy |= (a.v == v && a.slot == slot);
+    for (auto& a : ba_) busy |= (a.v == v && a.slot == slot);
+    if (busy) {
+      if (hp_status st = flush()) return st;
+      if (hp_status st = flush_applies()) return st;
+    }
+  }
+  const float* g = grad_dev;
+  if (grad_host) {  // library-owned device copy of a host gradient
+    if (s.grad_ring.empty()) {
+      s.grad_ring.assign(Nm_, nullptr);
+    }
+    float*& dst = s.grad_ring[(p - 1) % Nm_];
+    if (!dst && cudaMalloc(&dst, (size_t)std::max<int64_t>(n_, 1) * 4) != cudaSuccess) {
+      cudaGetLastError();
+      dst = nullptr;
+      return fail(HP_ERR_OOM, "gradient staging allocation failed");
+    }
+    if (hp_status st = check_cuda(cudaMemcpyAsync(dst, grad_host, (size_t)n_ * 4,
+                                                  cudaMemcpyHostToDevice, stream_), "H2D grad"))
+      return st;
+    g = dst;
+  }
+  if (ext) s.grad_of_slot[(p - 1) % Nm_] = g;
+  phase_ = kPhComplete;
+  const bool wave_end = p % Nm_ == 0;
+  bc_.push_back({v, p, slot, first, wave_end, g});
+  s.completed = p;
+  s.acc_count = first ? 1 : s.acc_count + 1;
+  if (!s.at_gate) {
+    s.pending_folds.push_back(p);          // w_local = w_local + u_p
+    s.a = p;
+    if (!wave_end && p + Nm_ <= last_p_) {  // START(p+Nm) without waiting
+      s.started = p + Nm_;
+      ungated_.push_back({v, p + Nm_});
+    }
+  } else {                                  // waiting at the gate (Z17)
+    s.backlog.push_back(p);
+    if (cfg_.local_semantics == HP_LOCAL_AT_LEAST) {
+      s.pending_folds.push_back(p);
+      s.a = p;
+    }
+  }
+  rec('C', v, "COMPLETE", p, c);
+  if (wave_end_out) *wave_end_out = wave_end;
+  return HP_OK;
+}
+
+hp_status Engine::push(int v, int64_t c) {
+  if (sticky_) return sticky_;
+  if (v < 0 || v >= N_) return fail(HP_ERR_INVALID, "vw out of range");
+  VW& s = vw_[v];
+  if (c != s.c_local) return fail(HP_ERR_PROTOCOL, "duplicate or out-of-order push");
+  if (s.completed < (c + 1) * Nm_) return fail(HP_ERR_PROTOCOL, "push of an incomplete wave");
+  if (phase_ > kPhPush)
+    if (hp_status st = flush()) return st;
+  phase_ = kPhPush;
+  commit_.push_back({v, c});
+  pending_applies_.push_back({v, c, (int)(c % R_)});
+  s.c_local = c + 1;
+  int64_t mn = vw_[0].c_local;
+  for (auto& x : vw_) mn = std::min(mn, x.c_local);
+  c_global_ = mn;
+  s.acc_count = 0;
+  if (c + 2 <= W_) s.at_gate = true;                   // a gated START remains
+  if (cfg_.apply_mode == HP_APPLY_ON_ARRIVAL) {        // apply on receipt
+    for (auto& a : pending_applies_) ba_.push_back(a);
+    pending_applies_.clear();
+  }
+  rec('P', v, "PUSH", (c + 1) * Nm_, c);
+  return HP_OK;
+}
+
+hp_status Engine::clock(int v, int64_t* cl, int64_t* cg) {
+  if (sticky_) return sticky_;
+  if (v < 0 || v >= N_) return fail(HP_ERR_INVALID, "vw out of range");
+  if (cl) *cl = vw_[v].c_local;
+  if (cg) *cg = c_global_;
+  if (vw_[v].at_gate && !gate_open(v).first) return HP_WOULD_BLOCK;
+  return HP_OK;
+}
+
+hp_status Engine::admit(int v, std::vector<int64_t>* started) {
+  if (sticky_) return sticky_;
+  if (v < 0 || v >= N_) return fail(HP_ERR_INVALID, "vw out of range");
+  VW& s = vw_[v];
+  if (!s.at_gate) return fail(HP_ERR_PROTOCOL, "pull outside the gate");
+  const auto open = gate_open(v);
+  const int64_t c = s.c_local - 1;
+  const int64_t gated_p = s.c_local * Nm_ + Nm_;     // (c+2)*Nm
+  if (!open.first) {
+    if (!s.blocked) {
+      s.blocked = true;
+      s.t_block = tick_;
+      rec('G', v, "BLOCK", gated_p, c);
+    }
+    return HP_WOULD_BLOCK;
+  }
+  phase_ = kPhPull;
+  if (s.blocked) {
+    s.wait += tick_ - s.t_block;
+    s.blocked = false;
+  }
+  s.at_gate = false;
+  if (open.second) {                                  // PULL
+    for (auto& a : pending_applies_) ba_.push_back(a); // w_global must be current
+    pending_applies_.clear();
+    bpull_.push_back(v);
+    auto& pf = s.pending_folds;
+    if (cfg_.local_semantics == HP_LOCAL_STRICT) {
+      const int64_t pushed_to = s.c_local * Nm_;      // folds inside pushed waves die
+      pf.erase(std::remove_if(pf.begin(), pf.end(), [&](int64_t q) { return q <= pushed_to; }),
+               pf.end());
+      s.a = pushed_to;
+    } else {
+      pf.clear();                                     // in w_global or the partial u~
+      s.a = s.completed;
+    }
+    s.held_g = c_global_;
+    s.held_K = (int64_t)commit_.size();
+    s.pulls++;
+    rec('G', v, "PULL", gated_p, c);
+  } else {
+    rec('G', v, "ADMIT", gated_p, c);
+  }
+  s.started = gated_p;
+  rec('G', v, "START", gated_p, wave_of(gated_p, Nm_));
+  if (started) started->push_back(gated_p);
+  for (int64_t q : s.backlog) {                       // Z17: replay in order
+    if (cfg_.local_semantics == HP_LOCAL_STRICT) {
+      s.pending_folds.push_back(q);
+      s.a = q;
+      rec('G', v, "FOLD", q, wave_of(q, Nm_));
+    }
+    if (q + Nm_ <= last_p_) {
+      s.started = q + Nm_;
+      rec('G', v, "START", q + Nm_, wave_of(q + Nm_, Nm_));
+      if (started) started->push_back(q + Nm_);
+    }
+  }
+  s.backlog.clear();
+  return HP_OK;
+}
+
+hp_status Engine::tick_end(std::vector<std::pair<int, int64_t>>* ungated) {
+  if (sticky_) return sticky_;
+  for (auto& vp : ungated_) {
+    rec('S', vp.first, "START", vp.second, wave_of(vp.second, Nm_));
+    if (ungated) ungated->push_back(vp);
+  }
+  ungated_.clear();
+  ticks++;
+  return flush();
+}
+
+// ---------------------------------------------------------------------------
+// Batch -> TickDesc(s). Algorithmic bytes are counted from the descriptor: each
+// buffer read or written once per launch = 4 bytes per param.
+hp_status Engine::emit(TickDesc& d) {
+  d.n = n_;
+  d.blk_base = begin_ >> 2;
+  d.wg = wg_;
+  d.m = m_;
+  d.neg_lr = -cfg_.lr;
+  d.mu = cfg_.momentum;
+  d.key0 = (uint32_t)(cfg_.seed & 0xffffffffu);
+  d.key1 = (uint32_t)(cfg_.seed >> 32);
+  bool any_pull = false;
+  for (int g = 0; g < d.ng; ++g) any_pull |= d.g[g].pull != 0;
+  d.wg_load = (d.na > 0 || any_pull) ? 1 : 0;
+  int streams = 0;  // buffer passes
+  for (int j = 0; j < d.nc; ++j) {
+    streams += (d.c[j].flags & kLoadAcc) ? 1 : 0;
+    streams += (d.c[j].flags & kStoreAcc) ? 1 : 0;
+    streams += d.c[j].grad ? 1 : 0;
+  }
+  for (int k = 0; k < d.na; ++k) streams += d.a[k].reg < 0 ? 1 : 0;
+  streams += d.wg_load + (d.na > 0 ? 1 : 0);
+  if (m_ && d.na > 0) streams += 2;
+  for (int g = 0; g < d.ng; ++g) {
+    streams += 1 + (d.g[g].pull ? 0 : 1) + (d.g[g].partial ? 1 : 0);
+    for (int f = d.g[g].f_begin; f < d.g[g].f_end; ++f) streams += d.f[f].grad ? 1 : 0;
+  }
+  const double bytes = 4.0 * (double)n_ * streams;
+  if (d.nc == 0 && d.na == 0 && d.ng == 0) return HP_OK;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof_on_) {
+    while (ev_.size() < ev_used_ + 2) {
+      cudaEvent_t e;
+      if (int err = cudaEventCreate(&e)) return check_cuda(err, "event");
+      ev_.push_back(e);
+    }
+    e0 = ev_[ev_used_];
+    e1 = ev_[ev_used_ + 1];
+    ev_used_ += 2;
+    cudaEventRecord(e0, stream_);
+  }
+  int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, stream_);
+  if (prof_on_) {
+    cudaEventRecord(e1, stream_);
+    prof_bytes_ += bytes;
+    prof_launches_++;
+  }
+  launches_++;
+  alg_bytes_ += bytes;
+  return check_cuda(err, "tick kernel");
+}
+
+hp_status Engine::flush() {
+  if (sticky_) return sticky_;
+  const bool strict = cfg_.local_semantics == HP_LOCAL_STRICT;
+  // 1. applies beyond kMaxA (oldest first) go out in apply-only launches
+  size_t a0 = 0;
+  while (ba_.size() - a0 > (size_t)kMaxA) {
+    TickDesc d;
+    memset(&d, 0, sizeof d);
+    for (int k = 0; k < kMaxA; ++k, ++a0) {
+      d.a[k].src = vw_[ba_[a0].v].acc[ba_[a0].slot];
+      d.a[k].reg = -1;
+    }
+    d.na = kMaxA;
+    applied_ += kMaxA;
+    if (hp_status st = emit(d)) return st;
+  }
+  TickDesc d;
+  memset(&d, 0, sizeof d);
+  // 2. completes
+  d.nc = (int)bc_.size();
+  for (int j = 0; j < d.nc; ++j) {
+    const BComplete& b = bc_[j];
+    DComplete& c = d.c[j];
+    c.acc = vw_[b.v].acc[b.slot];
+    c.grad = b.grad;
+    c.v = (uint32_t)b.v;
+    c.p = (uint32_t)b.p;
+    c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc;
+  }
+  // 3. applies in commit order; a wave completed in this batch comes from its register
+  for (size_t k = a0; k < ba_.size(); ++k) {
+    DApply& a = d.a[d.na++];
+    a.reg = -1;
+    a.src = vw_[ba_[k].v].acc[ba_[k].slot];
+    for (int j = 0; j < d.nc; ++j) {
+      if (bc_[j].v == ba_[k].v && bc_[j].wave_end && wave_of(bc_[j].p, Nm_) == ba_[k].c) {
+        a.reg = j;
+        d.c[j].flags &= ~kStoreAcc;   // applied here: u~ never needs to reach HBM
+      }
+    }
+    applied_++;
+  }
+  // 4. w_local groups: pulled VWs and VWs whose folds are due now
+  for (int v = 0; v < N_; ++v) {
+    VW& s = vw_[v];
+    const bool pulled = std::find(bpull_.begin(), bpull_.end(), v) != bpull_.end();
+    const bool hold = strict && s.at_gate;   // deferred to admission (Z3)
+    if (!pulled && (hold || s.pending_folds.empty())) continue;
+    std::vector<int64_t> folds;
+    if (!hold) folds.swap(s.pending_folds);
+    size_t fi = 0;
+    do {  // split a group whose folds overflow the descriptor
+      if (d.ng == kMaxG || d.nf == kMaxF) {
+        if (hp_status st = emit(d)) return st;
+        TickDesc nd;
+        memset(&nd, 0, sizeof nd);
+        d = nd;
+      }
+      DGroup& g = d.g[d.ng++];
+      g.wl = s.wl;
+      g.pull = (pulled && fi == 0) ? 1 : 0;
+      g.partial = nullptr;
+      g.partial_reg = -1;
+      if (g.pull && !strict && s.acc_count > 0) {  // AT_LEAST: w_global + partial u~
+        const int64_t open = s.c_local;
+        g.partial = s.acc[open % R_];
+        for (int j = 0; j < d.nc; ++j)
+          if (bc_[j].v == v && wave_of(bc_[j].p, Nm_) == open) g.partial_reg = j;
+        if (g.partial_reg >= 0) g.partial = nullptr;
+      }
+      g.f_begin = d.nf;
+      for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
+        DFold& f = d.f[d.nf++];
+        f.v = (uint32_t)v;
+        f.p = (uint32_t)folds[fi];
+        f.reg = -1;
+        f.grad = nullptr;
+        for (int j = 0; j < d.nc; ++j)
+          if (bc_[j].v == v && bc_[j].p == folds[fi]) f.reg = j;
+        if (f.reg < 0) f.grad = fold_grad(v, folds[fi]);
+      }
+      g.f_end = d.nf;
+    } while (fi < folds.size());
+  }
+  bc_.clear();
+  ba_.clear();
+  bpull_.clear();
+  phase_ = kNone;
+  return emit(d);
+}
+
+hp_status Engine::flush_applies() {
+  if (hp_status st = flush()) return st;
+  if (pending_applies_.empty()) return HP_OK;
+  for (auto& a : pending_applies_) ba_.push_back(a);
+  pending_applies_.clear();
+  return flush();
+}
+
+hp_status Engine::sync() {
+  if (sticky_) return sticky_;
+  for (auto& vp : ungated_) rec('S', vp.first, "START", vp.second, wave_of(vp.second, Nm_));
+  ungated_.clear();
+  if (hp_status st = flush_applies()) return st;
+  return check_cuda(cudaStreamSynchronize(stream_), "sync");
+}
+
+hp_status Engine::read(int which, int64_t off, int64_t cnt, float* dst) {
+  if (sticky_) return sticky_;
+  if (which < -2 || which >= N_) return fail(HP_ERR_INVALID, "bad buffer id");
+  if (off < 0 || cnt < 0 || off + cnt > n_ || (cnt && !dst)) return fail(HP_ERR_INVALID, "bad range");
+  if (which == -2 && !m_) return fail(HP_ERR_INVALID, "no momentum buffer");
+  if (hp_status st = sync()) return st;
+  const float* src = which == -1 ? wg_ : which == -2 ? m_ : vw_[which].wl;
+  if (int e = cudaMemcpy(dst, src + off, (size_t)cnt * 4, cudaMemcpyDeviceToHost))
+    return check_cuda(e, "read");
+  return HP_OK;
+}
+
+void Engine::stats(hp_stats* out) const {
+  memset(out, 0, sizeof *out);
+  out->commits = (int64_t)commit_.size();
+  out->applied = applied_;
+  out->launches = launches_;
+  out->ticks = ticks;
+  out->alg_bytes = alg_bytes_;
+  for (int v = 0; v < N_ && v < 8; ++v) {
+    out->wait_ticks[v] = vw_[v].wait;
+    out->pulls[v] = vw_[v].pulls;
+  }
+}
+
+hp_status Engine::profile_enable(bool on) {
+  if (sticky_) return sticky_;
+  prof_on_ = on;
+  ev_used_ = 0;
+  prof_bytes_ = 0;
+  prof_launches_ = 0;
+  return HP_OK;
+}
+
+hp_status Engine::profile_read(double* ms, double* bytes, int64_t* launches) {
+  if (sticky_) return sticky_;
+  if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "profile sync")) return st;
+  double tot = 0;
+  for (size_t i = 0; i + 1 < ev_used_; i += 2) {
+    float t = 0;
+    if (int e = cudaEventElapsedTime(&t, ev_[i], ev_[i + 1])) return check_cuda(e, "elapsed");
+    tot += t;
+  }
+  if (ms) *ms = tot;
+  if (bytes) *bytes = prof_bytes_;
+  if (launches) *launches = prof_launches_;
+  return HP_OK;
+}
+
+}  // namespace hp

@@ -1,0 +1,130 @@
+// engine.h -- WSP protocol engine of libhetpipe: host-side clocks, gate,
+// commit log and version trace, plus the per-tick batch that becomes one fused
+// kernel launch (tick_desc.h). Independent of oracle/ (shares no code).
+//
+// Paper mapping (P:n = PAPER.md line n):
+//   complete()  COMPLETE(v,p): u_p into the open wave's acc slot and a
+//               pending fold w_local += u_p, materialised before the
+//               next START that reads w_local (JIT fold, reading Z3).
+//   push()      PUSH(v,c): commit log append, c_local = c+1, c_global = min
+//               (P:917-930). The PS apply is deferred to the first observer
+//               (a pull or a read) unless apply_mode = ON_ARRIVAL (reading Z4).
+//   admit()     GATE/PULL(v) for the gated START (c+2)*Nm (Z7, Z17).
+//   tick_end()  START phase records + one fused launch (Z5).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/hetpipe.h"
+#include "tick_desc.h"
+
+namespace hp {
+
+struct VW {
+  int64_t started = 0, completed = 0, c_local = 0;
+  int64_t a = 0;                 // own-update cursor a_v (logical)
+  int64_t held_g = 0, held_K = 0;
+  bool at_gate = false, blocked = false;
+  int64_t t_block = 0, wait = 0, pulls = 0;
+  int64_t acc_count = 0;         // completions in the open wave
+  std::vector<int64_t> backlog;  // completions while waiting at the gate (Z17)
+  std::vector<int64_t> pending_folds;  // u_p not yet folded into w_local on device
+  float* wl = nullptr;
+  std::vector<float*> acc;       // ring of R slots; wave c -> slot c % R
+  std::vector<const float*> grad_of_slot;  // EXTERNAL: grad of minibatch p in slot (p-1)%Nm
+  std::vector<float*> grad_ring;           // library-owned copies of host gradients
+};
+
+class Engine {
+ public:
+  explicit Engine(const hp_config& cfg);
+  ~Engine();
+  hp_status init();
+
+  hp_status complete(int v, int64_t p, const float* grad_dev, const float* grad_host,
+                     bool* wave_end);
+  hp_status push(int v, int64_t c);
+  hp_status clock(int v, int64_t* c_local, int64_t* c_global);
+  hp_status admit(int v, std::vector<int64_t>* started);
+  hp_status tick_end(std::vector<std::pair<int, int64_t>>* ungated);
+  hp_status flush_applies();
+  hp_status sync();
+  hp_status read(int which, int64_t off, int64_t cnt, float* dst);
+
+  void set_tick(int64_t t) { tick_ = t; }
+  bool at_gate(int v) const { return vw_[v].at_gate; }
+  bool done() const;
+  int64_t commits() const { return (int64_t)commit_.size(); }
+  const hp_config& cfg() const { return cfg_; }
+  int64_t last_p() const { return last_p_; }
+  hp_status fail(hp_status s, const std::string& msg);
+  hp_status sticky() const { return sticky_; }
+  const std::string& error() const { return err_; }
+  std::string& trace() { return trace_; }
+  void set_trace(bool on) { trace_on_ = on; }
+  void stats(hp_stats* out) const;
+  hp_status profile_enable(bool on);
+  hp_status profile_read(double* ms, double* bytes, int64_t* launches);
+  int64_t ticks = 0;
+
+ private:
+  struct BComplete {
+    int v;
+    int64_t p;
+    int slot;
+    bool first, wave_end;
+    const float* grad;
+  };
+  struct BApply {
+    int v;
+    int64_t c;
+    int slot;
+  };
+  enum Phase { kNone = 0, kPhComplete = 1, kPhPush = 2, kPhPull = 3 };
+
+  hp_status flush();
+  hp_status emit(TickDesc& d);
+  hp_status check_cuda(int err, const char* what);
+  void rec(char phase, int v, const char* kind, int64_t p, int64_t c);
+  std::pair<bool, bool> gate_open(int v) const;
+  const float* fold_grad(int v, int64_t p) const;
+
+  hp_config cfg_;
+  int N_, Nm_, R_;
+  int64_t W_, last_p_, n_, begin_;
+  cudaStream_t stream_ = nullptr;
+  bool own_stream_ = false;
+  void* arena_ = nullptr;
+  float* wg_ = nullptr;
+  float* m_ = nullptr;
+  std::vector<VW> vw_;
+  std::vector<std::pair<int, int64_t>> commit_;
+  std::vector<BApply> pending_applies_;
+  int64_t c_global_ = 0, applied_ = 0, tick_ = 0;
+
+  // current batch (one tick)
+  Phase phase_ = kNone;
+  std::vector<BComplete> bc_;
+  std::vector<BApply> ba_;
+  std::vector<int> bpull_;              // VWs admitted with a pull in this batch
+  std::vector<std::pair<int, int64_t>> ungated_;
+
+  // accounting
+  int64_t launches_ = 0;
+  double alg_bytes_ = 0;
+  bool prof_on_ = false;
+  std::vector<cudaEvent_t> ev_;
+  size_t ev_used_ = 0;
+  double prof_bytes_ = 0;
+  int64_t prof_launches_ = 0;
+
+  std::string trace_;
+  bool trace_on_ = true;
+  hp_status sticky_ = HP_OK;
+  std::string err_;
+};
+
+}  // namespace hp

@@ -1,0 +1,265 @@
+// kernels.cu -- sm_100a kernels of the WSP hot path (libhetpipe).
+//
+// One fused, element-wise, HBM-streaming kernel per controller tick
+// (tick_desc.h). No tensor cores: the path is a streaming reduction with < 0.2
+// flop/byte; the design levers are 128-bit accesses, all loads
+// of a chunk issued before any arithmetic (memory-level parallelism), streaming
+// cache hints, a persistent grid sized from the occupancy calculator x 148 SMs,
+// and fusing every op of a tick so each buffer crosses HBM at most once per tick.
+//
+// Rounding: every float op is an explicit __fmul_rn / __fadd_rn (no FMA
+// contraction), which is the order and precision the paper's updates state
+// (P:839 w_local + u_p, P:929 w_global + u~) under reading Z10.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tick_desc.h"
+
+namespace hp {
+namespace {
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11): 10 rounds of two 32x32->64 multiplies
+// and a Feistel-like mix, key bumped by the Weyl constants between rounds.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
+                                               uint32_t c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0;
+    const uint32_t n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+// FLOAT: (x>>8)*2^-24 - 0.5 ; DYADIC: (x>>28) - 8. Both exact in fp32.
+template <int GM>
+__device__ __forceinline__ float grad_of(uint32_t x) {
+  if (GM == 1) return (float)((int)(x >> 28) - 8);
+  return __fsub_rn(__fmul_rn((float)(x >> 8), 0x1p-24f), 0.5f);
+}
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                     __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 f4scale(float s, float4 a) {
+  return make_float4(__fmul_rn(s, a.x), __fmul_rn(s, a.y), __fmul_rn(s, a.z),
+                     __fmul_rn(s, a.w));
+}
+
+// Chunk access: CNT == 4 is a full aligned float4; CNT < 4 the ragged tail
+// (element-wise, zero-filled), only ever executed by one thread.
+template <int CNT>
+__device__ __forceinline__ float4 ld4(const float* base, int64_t q) {
+  if (CNT == 4) return __ldcs(reinterpret_cast<const float4*>(base) + q);
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* p = base + 4 * q;
+  r.x = p[0];
+  if (CNT > 1) r.y = p[1];
+  if (CNT > 2) r.z = p[2];
+  return r;
+}
+template <int CNT>
+__device__ __forceinline__ void st4(float* base, int64_t q, float4 v) {
+  if (CNT == 4) {
+    __stcs(reinterpret_cast<float4*>(base) + q, v);
+    return;
+  }
+  float* p = base + 4 * q;
+  p[0] = v.x;
+  if (CNT > 1) p[1] = v.y;
+  if (CNT > 2) p[2] = v.z;
+}
+
+template <int K>
+__device__ __forceinline__ float4 pick(const float4 (&arr)[K], int r) {
+  float4 x = arr[0];
+#pragma unroll
+  for (int j = 1; j < K; ++j)
+    if (r == j) x = arr[j];
+  return x;
+}
+
+// u = fl(-lr * g) for the 4 params of global block blk.
+template <int GM, int CNT>
+__device__ __forceinline__ float4 synth_u(const TickDesc& d, uint32_t v, uint32_t p,
+                                          uint64_t blk) {
+  const uint4 x = philox4x32_10((uint32_t)blk, v, p, 0u, d.key0, d.key1);
+  return make_float4(__fmul_rn(d.neg_lr, grad_of<GM>(x.x)), __fmul_rn(d.neg_lr, grad_of<GM>(x.y)),
+                     __fmul_rn(d.neg_lr, grad_of<GM>(x.z)), __fmul_rn(d.neg_lr, grad_of<GM>(x.w)));
+}
+
+// One chunk (4 params) of the tick program. K bounds nc, na and ng.
+template <int GM, bool MOM, int K, int CNT>
+__device__ __forceinline__ void tick_chunk(const TickDesc& d, int64_t q) {
+  const uint64_t blk = (uint64_t)(d.blk_base + q);
+  // ---- 1. every load of the chunk first (they are independent) -------------
+  float4 acc_in[K], grad_in[K], src_in[K], wl_in[K], part_in[K];
+  float4 wg = make_float4(0.f, 0.f, 0.f, 0.f), mm = wg;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (j < d.nc) {
+      if (d.c[j].flags & kLoadAcc) acc_in[j] = ld4<CNT>(d.c[j].acc, q);
+      if (GM == 2) grad_in[j] = ld4<CNT>(d.c[j].grad, q);
+    }
+    if (j < d.na && d.a[j].reg < 0) src_in[j] = ld4<CNT>(d.a[j].src, q);
+    if (j < d.ng) {
+      if (!d.g[j].pull) wl_in[j] = ld4<CNT>(d.g[j].wl, q);
+      else if (d.g[j].partial) part_in[j] = ld4<CNT>(d.g[j].partial, q);
+    }
+  }
+  if (d.wg_load) wg = ld4<CNT>(d.wg, q);
+  if (MOM && d.na > 0) mm = ld4<CNT>(d.m, q);
+
+  // ---- 2. completes: u_j, wave aggregate a_j ------------------------
+  float4 u[K], a[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if (j < d.nc) {
+      const DComplete& c = d.c[j];
+      if (GM == 2) u[j] = f4scale(d.neg_lr, grad_in[j]);
+      else u[j] = synth_u<GM, CNT>(d, c.v, c.p, blk);
+      a[j] = (c.flags & kFirst) ? u[j] : f4add(acc_in[j], u[j]);
+      if (c.flags & kStoreAcc) st4<CNT>(c.acc, q, a[j]);
+    }
+  }
+  // ---- 3. PS applies in commit order (momentum Z11) -----------------
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (k < d.na) {
+      const float4 x = d.a[k].reg >= 0 ? pick<K>(a, d.a[k].reg) : src_in[k];
+      if (MOM) {
+        mm = f4add(f4scale(d.mu, mm), x);
+        wg = f4add(wg, mm);
+      } else {
+        wg = f4add(wg, x);
+      }
+    }
+  }
+  if (d.na > 0) {
+    st4<CNT>(d.wg, q, wg);
+    if (MOM) st4<CNT>(d.m, q, mm);
+  }
+  // ---- 4. w_local groups: pull base then due folds ---------
+#pragma unroll
+  for (int gi = 0; gi < K; ++gi) {
+    if (gi < d.ng) {
+      const DGroup& g = d.g[gi];
+      float4 w;
+      if (g.pull) {
+        w = wg;
+        if (g.partial_reg >= 0) w = f4add(wg, pick<K>(a, g.partial_reg));
+        else if (g.partial) w = f4add(wg, part_in[gi]);
+      } else {
+        w = wl_in[gi];
+      }
+      for (int fi = g.f_begin; fi < g.f_end; ++fi) {
+        const DFold& f = d.f[fi];
+        float4 uf;
+        if (f.reg >= 0) uf = pick<K>(u, f.reg);
+        else if (GM == 2) uf = f4scale(d.neg_lr, ld4<CNT>(f.grad, q));
+        else uf = synth_u<GM, CNT>(d, f.v, f.p, blk);
+        w = f4add(w, uf);
+      }
+      st4<CNT>(g.wl, q, w);
+    }
+  }
+}
+
+template <int GM, bool MOM, int K>
+__global__ void __launch_bounds__(256) tick_kernel(const __grid_constant__ TickDesc d) {
+  const int64_t nfull = d.n >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t q = t0; q < nfull; q += stride) tick_chunk<GM, MOM, K, 4>(d, q);
+  if (t0 == 0) {
+    switch (d.n & 3) {
+      case 1: tick_chunk<GM, MOM, K, 1>(d, nfull); break;
+      case 2: tick_chunk<GM, MOM, K, 2>(d, nfull); break;
+      case 3: tick_chunk<GM, MOM, K, 3>(d, nfull); break;
+      default: break;
+    }
+  }
+}
+
+// w0 (Z8): zero or Philox stream 1, counter (i>>2, 0, 0, 1).
+__global__ void init_kernel(float* out, int64_t n, int64_t param_begin, int w0_mode,
+                            int grad_mode, uint32_t k0, uint32_t k1) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t gi = param_begin + i;
+    float w = 0.f;
+    if (w0_mode == 1) {
+      const uint4 x4 = philox4x32_10((uint32_t)(gi >> 2), 0u, 0u, 1u, k0, k1);
+      const uint32_t words[4] = {x4.x, x4.y, x4.z, x4.w};
+      const uint32_t x = words[gi & 3];
+      if (grad_mode == 1) w = __fsub_rn(__fmul_rn((float)(x >> 25), 0x1p-6f), 1.0f);
+      else w = __fsub_rn(__fmul_rn(2.0f, __fmul_rn((float)(x >> 8), 0x1p-24f)), 1.0f);
+    }
+    out[i] = w;
+  }
+}
+
+template <int GM, bool MOM, int K>
+int launch_k(const TickDesc& d, cudaStream_t s) {
+  static int grid_max = 0;
+  if (grid_max == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tick_kernel<GM, MOM, K>, 256, 0);
+    grid_max = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int64_t chunks = (d.n + 3) >> 2;
+  int64_t blocks = (chunks + 255) / 256;
+  if (blocks > grid_max) blocks = grid_max;
+  if (blocks < 1) blocks = 1;
+  tick_kernel<GM, MOM, K><<<(unsigned)blocks, 256, 0, s>>>(d);
+  return (int)cudaGetLastError();
+}
+
+template <int GM, bool MOM>
+int launch_gm(const TickDesc& d, cudaStream_t s) {
+  int k = d.nc;
+  if (d.na > k) k = d.na;
+  if (d.ng > k) k = d.ng;
+  if (k <= 1) return launch_k<GM, MOM, 1>(d, s);
+  if (k <= 2) return launch_k<GM, MOM, 2>(d, s);
+  if (k <= 4) return launch_k<GM, MOM, 4>(d, s);
+  return launch_k<GM, MOM, 8>(d, s);
+}
+
+}  // namespace
+
+int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d.n <= 0) return 0;
+  switch (grad_mode) {
+    case 0: return momentum ? launch_gm<0, true>(d, s) : launch_gm<0, false>(d, s);
+    case 1: return momentum ? launch_gm<1, true>(d, s) : launch_gm<1, false>(d, s);
+    default: return momentum ? launch_gm<2, true>(d, s) : launch_gm<2, false>(d, s);
+  }
+}
+
+int launch_init(float* out, int64_t n, int64_t param_begin, int w0_mode, int grad_mode,
+                uint32_t key0, uint32_t key1, void* stream) {
+  if (n <= 0) return 0;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  init_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      out, n, param_begin, w0_mode, grad_mode, key0, key1);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace hp

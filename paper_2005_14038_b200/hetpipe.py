@@ -1,0 +1,238 @@
+"""Thin ctypes binding of libhetpipe (include/hetpipe.h): argument marshalling
+only -- every step of the WSP path runs in the library's C++ controller and
+sm_100a kernels. There is no CPU fallback: if the library is missing or no
+CUDA device is usable, these calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhetpipe.so")
+
+HP_OK, HP_WOULD_BLOCK = 0, 1
+HP_ERR_INVALID, HP_ERR_PROTOCOL, HP_ERR_CUDA = -1, -2, -3
+HP_ERR_COMM, HP_ERR_OOM, HP_ERR_STATE = -4, -5, -6
+STATUS_NAMES = {0: "HP_OK", 1: "HP_WOULD_BLOCK", -1: "HP_ERR_INVALID",
+                -2: "HP_ERR_PROTOCOL", -3: "HP_ERR_CUDA", -4: "HP_ERR_COMM",
+                -5: "HP_ERR_OOM", -6: "HP_ERR_STATE"}
+
+
+class hp_config(C.Structure):
+    _fields_ = [("num_vw", C.c_int32), ("Nm", C.c_int32), ("D", C.c_int32),
+                ("waves", C.c_int32), ("nparams", C.c_int64),
+                ("param_begin", C.c_int64), ("param_count", C.c_int64),
+                ("lr", C.c_float), ("momentum", C.c_float), ("seed", C.c_uint64),
+                ("grad_mode", C.c_int32), ("w0_mode", C.c_int32),
+                ("pull_policy", C.c_int32), ("local_semantics", C.c_int32),
+                ("apply_mode", C.c_int32), ("acc_slots", C.c_int32),
+                ("device", C.c_int32), ("stream", C.c_void_p)]
+
+
+class hp_stats(C.Structure):
+    _fields_ = [("commits", C.c_int64), ("applied", C.c_int64),
+                ("launches", C.c_int64), ("ticks", C.c_int64),
+                ("alg_bytes", C.c_double), ("wait_ticks", C.c_int64 * 8),
+                ("pulls", C.c_int64 * 8)]
+
+
+class HetPipeError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+EXPORTS = {
+    "hp_config_default": (None, [C.POINTER(hp_config)]),
+    "hp_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32,
+                          C.c_int64, C.c_float]),
+    "hp_init_ex": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(hp_config)]),
+    "hp_accumulate_minibatch": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]),
+    "hp_accumulate_minibatch_host": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]),
+    "hp_push_wave": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
+    "hp_clock": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "hp_pull": (C.c_int, [C.c_void_p, C.c_int32]),
+    "hp_tick_end": (C.c_int, [C.c_void_p]),
+    "hp_set_tick": (C.c_int, [C.c_void_p, C.c_int64]),
+    "hp_schedule_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hp_schedule_advance": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
+    "hp_run_schedule": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hp_schedule_set_host_grads": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "hp_sync": (C.c_int, [C.c_void_p]),
+    "hp_read_weights": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]),
+    "hp_trace_dump": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "hp_trace_enable": (C.c_int, [C.c_void_p, C.c_int32]),
+    "hp_get_stats": (C.c_int, [C.c_void_p, C.POINTER(hp_stats)]),
+    "hp_profile_enable": (C.c_int, [C.c_void_p, C.c_int32]),
+    "hp_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                  C.POINTER(C.c_int64)]),
+    "hp_s_global": (C.c_int64, [C.c_int32, C.c_int32]),
+    "hp_version_floor": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
+    "hp_last_error": (C.c_char_p, [C.c_void_p]),
+    "hp_version": (C.c_char_p, []),
+    "hp_finalize": (None, [C.c_void_p]),
+}
+
+
+def load() -> C.CDLL:
+    """Load libhetpipe.so (built by paper_2005_14038_b200.build); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2005_14038_b200.build`")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def config_from(cfg, **overrides) -> hp_config:
+    """hp_config from a workloads.WSPConfig (plus keyword overrides)."""
+    lib = load()
+    c = hp_config()
+    lib.hp_config_default(C.byref(c))
+    c.num_vw, c.Nm, c.D, c.waves = cfg.num_vw, cfg.Nm, cfg.D, cfg.waves
+    c.nparams = cfg.nparams
+    c.lr, c.momentum, c.seed = cfg.lr, cfg.momentum, cfg.seed
+    c.grad_mode, c.w0_mode = cfg.grad_mode, cfg.w0_mode
+    c.pull_policy, c.local_semantics = cfg.pull_policy, cfg.local_semantics
+    for k, v in overrides.items():
+        setattr(c, k, v)
+    return c
+
+
+class Context:
+    """One hp_ctx (one rank). Methods carry the C names without the prefix."""
+
+    def __init__(self, cfg: hp_config):
+        self.lib = load()
+        self.cfg = cfg
+        h = C.c_void_p()
+        st = self.lib.hp_init_ex(C.byref(h), C.byref(cfg))
+        if st != HP_OK:
+            raise HetPipeError(st, self.lib.hp_last_error(None).decode())
+        self.h = h
+
+    # -- status handling ------------------------------------------------------
+    def _chk(self, st: int, allow_block: bool = False) -> int:
+        if st == HP_OK or (allow_block and st == HP_WOULD_BLOCK):
+            return st
+        raise HetPipeError(st, (self.lib.hp_last_error(self.h) or b"").decode())
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.hp_finalize(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- protocol -------------------------------------------------------------
+    def accumulate_minibatch(self, vw: int, p: int, grad_ptr: int = 0) -> int:
+        return self._chk(self.lib.hp_accumulate_minibatch(self.h, vw, p, grad_ptr or None))
+
+    def accumulate_minibatch_host(self, vw: int, p: int, host: np.ndarray) -> int:
+        assert host.dtype == np.float32 and host.flags.c_contiguous
+        return self._chk(self.lib.hp_accumulate_minibatch_host(
+            self.h, vw, p, host.ctypes.data_as(C.c_void_p)))
+
+    def push_wave(self, vw: int, c: int) -> int:
+        return self._chk(self.lib.hp_push_wave(self.h, vw, c))
+
+    def clock(self, vw: int):
+        cl, cg = C.c_int64(), C.c_int64()
+        st = self._chk(self.lib.hp_clock(self.h, vw, C.byref(cl), C.byref(cg)), True)
+        return cl.value, cg.value, st == HP_WOULD_BLOCK
+
+    def pull(self, vw: int) -> int:
+        return self._chk(self.lib.hp_pull(self.h, vw), allow_block=True)
+
+    def tick_end(self) -> int:
+        return self._chk(self.lib.hp_tick_end(self.h))
+
+    def set_tick(self, t: int) -> int:
+        return self._chk(self.lib.hp_set_tick(self.h, t))
+
+    # -- controller -----------------------------------------------------------
+    def schedule_begin(self, tau: Sequence[int], lat: Optional[Sequence[int]] = None) -> None:
+        self._tau = np.ascontiguousarray(tau, dtype=np.int64)
+        self._lat = None if lat is None else np.ascontiguousarray(lat, dtype=np.int64)
+        self._chk(self.lib.hp_schedule_begin(
+            self.h, self._tau.ctypes.data_as(C.c_void_p),
+            None if self._lat is None else self._lat.ctypes.data_as(C.c_void_p)))
+
+    def schedule_advance(self, target_commits: int) -> int:
+        n = C.c_int64()
+        self._chk(self.lib.hp_schedule_advance(self.h, target_commits, C.byref(n)))
+        return n.value
+
+    def run_schedule(self, tau: Sequence[int], lat: Optional[Sequence[int]] = None) -> None:
+        t = np.ascontiguousarray(tau, dtype=np.int64)
+        l_ = None if lat is None else np.ascontiguousarray(lat, dtype=np.int64)
+        self._chk(self.lib.hp_run_schedule(
+            self.h, t.ctypes.data_as(C.c_void_p),
+            None if l_ is None else l_.ctypes.data_as(C.c_void_p)))
+
+    def schedule_set_host_grads(self, bufs: Sequence[np.ndarray]) -> None:
+        self._host_bufs = list(bufs)
+        arr = (C.c_void_p * len(bufs))(*[b.ctypes.data for b in bufs])
+        self._host_ptrs = arr
+        self._chk(self.lib.hp_schedule_set_host_grads(self.h, arr, len(bufs)))
+
+    # -- data -----------------------------------------------------------------
+    def sync(self) -> None:
+        self._chk(self.lib.hp_sync(self.h))
+
+    def read_weights(self, which: int, offset: int = 0, count: Optional[int] = None,
+                     out: Optional[np.ndarray] = None) -> np.ndarray:
+        if count is None:
+            count = self.cfg.param_count - offset
+        if out is None:
+            out = np.empty(count, dtype=np.float32)
+        self._chk(self.lib.hp_read_weights(self.h, which, offset, count,
+                                           out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def trace_dump(self, path: str) -> None:
+        self._chk(self.lib.hp_trace_dump(self.h, path.encode()))
+
+    def trace_lines(self, tmp_path: str) -> list:
+        self.trace_dump(tmp_path)
+        with open(tmp_path) as f:
+            return f.read().splitlines()
+
+    def trace_enable(self, on: bool) -> None:
+        self._chk(self.lib.hp_trace_enable(self.h, 1 if on else 0))
+
+    def stats(self) -> hp_stats:
+        s = hp_stats()
+        self._chk(self.lib.hp_get_stats(self.h, C.byref(s)))
+        return s
+
+    def profile_enable(self, on: bool) -> None:
+        self._chk(self.lib.hp_profile_enable(self.h, 1 if on else 0))
+
+    def profile_read(self):
+        ms, b, n = C.c_double(), C.c_double(), C.c_int64()
+        self._chk(self.lib.hp_profile_read(self.h, C.byref(ms), C.byref(b), C.byref(n)))
+        return ms.value, b.value, n.value
+
+
+def s_global(Nm: int, D: int) -> int:
+    return load().hp_s_global(Nm, D)
+
+
+def version_floor(p: int, Nm: int, D: int) -> int:
+    return load().hp_version_floor(p, Nm, D)

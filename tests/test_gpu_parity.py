@@ -1,0 +1,214 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs. Same summation order on both sides, so the bar is
+bit-exact fp32 weights (stronger than the north_star's 1e-5 relative) and
+byte-identical clock/version traces."""
+import os
+import random
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle import gradient, run_schedule
+from workloads import (C1, C1_SKEW, C2, C3, C4, C5, GRAD_DYADIC, GRAD_EXTERNAL,
+                       GRAD_FLOAT, LOCAL_AT_LEAST, LOCAL_STRICT, PULL_EAGER,
+                       PULL_LAZY, W0_PHILOX, W0_ZERO, WSPConfig, sample_indices)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2005_14038_b200 import build, hetpipe
+    build.build()
+    return hetpipe
+
+
+def run_device(hp, cfg, apply_mode=0, acc_slots=2, **over):
+    ctx = hp.Context(hp.config_from(cfg, apply_mode=apply_mode, acc_slots=acc_slots, **over))
+    ctx.run_schedule(cfg.tau, cfg.latency())
+    with tempfile.NamedTemporaryFile(suffix=".trace") as f:
+        trace = ctx.trace_lines(f.name)
+    wg = ctx.read_weights(-1)
+    wl = [ctx.read_weights(v) for v in range(cfg.num_vw)]
+    m = ctx.read_weights(-2) if cfg.momentum else None
+    st = ctx.stats()
+    ctx.close()
+    return trace, wg, wl, m, st
+
+
+def assert_same(o, trace, wg, wl, idx=None):
+    assert trace == o.trace
+    sel = (lambda a: a) if idx is None else (lambda a: a[idx])
+    assert np.array_equal(sel(wg), o.wg)
+    for v, w in enumerate(wl):
+        assert np.array_equal(sel(w), o.wl[v]), f"w_local({v})"
+
+
+@pytest.mark.parametrize("cfg", [C1, C1_SKEW], ids=["C1", "C1-skew"])
+@pytest.mark.parametrize("apply_mode", [0, 1])
+def test_c1_bsp_limit_bit_exact(hp, cfg, apply_mode):
+    o = run_schedule(cfg)
+    trace, wg, wl, _, st = run_device(hp, cfg, apply_mode)
+    assert_same(o, trace, wg, wl)
+    assert st.commits == cfg.num_vw * cfg.waves == st.applied
+    assert list(st.wait_ticks[:cfg.num_vw]) == o.wait
+    assert list(st.pulls[:cfg.num_vw]) == o.pulls
+
+
+def _rand_cfg(seed):
+    rng = random.Random(seed)
+    N = rng.randint(1, 5)
+    Nm = rng.randint(1, 5)
+    tau = tuple(rng.randint(1, 12) for _ in range(N))
+    mode = rng.choice([GRAD_FLOAT, GRAD_DYADIC])
+    return WSPConfig(
+        "rand", N, Nm, rng.randint(0, 3), rng.choice([1, 3, 4, 61, 256, 1027, 4099]),
+        rng.randint(1, 7), tau, lr=(0.01 if mode == GRAD_FLOAT else 2.0 ** -6),
+        momentum=rng.choice([0.0, 0.0, 0.9]), seed=rng.randint(0, 2 ** 64 - 1),
+        grad_mode=mode, w0_mode=rng.choice([W0_ZERO, W0_PHILOX]),
+        pull_policy=rng.choice([PULL_EAGER, PULL_LAZY]),
+        local_semantics=rng.choice([LOCAL_STRICT, LOCAL_AT_LEAST]),
+        lat=tuple(t * rng.randint(1, Nm + 1) for t in tau))
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_random_configs_bit_exact(hp, seed):
+    """Random N, Nm, D, P (ragged tails), W, speeds, momentum, EAGER/LAZY,
+    STRICT/AT_LEAST, apply modes and ring depths: identical traces and arrays."""
+    cfg = _rand_cfg(seed)
+    o = run_schedule(cfg)
+    rng = random.Random(1000 + seed)
+    trace, wg, wl, m, _ = run_device(hp, cfg, apply_mode=rng.randint(0, 1),
+                                     acc_slots=rng.choice([2, 3, 8]))
+    assert_same(o, trace, wg, wl)
+    if cfg.momentum:
+        assert np.array_equal(m, o.m)
+
+
+def test_per_tick_states(hp):
+    """Advance the device controller commit by commit (forcing early applies)
+    and compare w_global and every w_local not waiting at its gate with the
+    oracle's state after the same tick."""
+    cfg = C2.replace(nparams=2053, waves=6, D=1, tau=(5, 7, 9, 12))
+    states = []
+
+    def on_tick(t, sm):
+        states.append((t, len(sm.commit), sm.wg.copy(), [w.copy() for w in sm.wl],
+                       list(sm.at_gate)))
+
+    run_schedule(cfg, on_tick=on_tick)
+    ctx = hp.Context(hp.config_from(cfg))
+    ctx.schedule_begin(cfg.tau, cfg.latency())
+    checked = 0
+    for target in range(1, cfg.num_vw * cfg.waves + 1):
+        reached = ctx.schedule_advance(target)
+        t, ncommit, wg, wl, at_gate = next(s for s in states if s[1] >= target)
+        assert reached == ncommit
+        assert np.array_equal(ctx.read_weights(-1), wg)
+        for v in range(cfg.num_vw):
+            if not at_gate[v]:
+                assert np.array_equal(ctx.read_weights(v), wl[v]), (target, v)
+                checked += 1
+    assert checked > 10
+    ctx.close()
+
+
+def test_external_gradients_match_synthetic(hp):
+    """EXTERNAL mode: the same Philox gradients, supplied as host buffers
+    (hp_accumulate_minibatch_host via the controller), give the same result."""
+    cfg = C2.replace(nparams=1030, waves=3, D=0, tau=(3, 4, 6, 7))
+    o = run_schedule(cfg)
+    idx = np.arange(cfg.nparams)
+    last_p = cfg.waves * cfg.Nm
+    bufs = []
+    for v in range(cfg.num_vw):
+        for p in range(0, last_p):
+            bufs.append(None)
+    # host buffer k = (v*last_p + p) % n  ->  n = N*last_p + 1 keeps them distinct
+    n = cfg.num_vw * last_p + 1
+    bufs = [np.zeros(cfg.nparams, dtype=np.float32) for _ in range(n)]
+    for v in range(cfg.num_vw):
+        for p in range(1, last_p + 1):
+            bufs[(v * last_p + p) % n][:] = gradient(idx, v, p, cfg)
+    ctx = hp.Context(hp.config_from(cfg, grad_mode=GRAD_EXTERNAL))
+    ctx.schedule_set_host_grads(bufs)
+    ctx.run_schedule(cfg.tau, cfg.latency())
+    assert np.array_equal(ctx.read_weights(-1), o.wg)
+    for v in range(cfg.num_vw):
+        assert np.array_equal(ctx.read_weights(v), o.wl[v])
+    ctx.close()
+
+
+def test_event_api_protocol_errors(hp):
+    """Negative ABI tests: duplicate / out-of-order / incomplete push,
+    out-of-order completion, pull outside the gate, WOULD_BLOCK without effect."""
+    cfg = C1.replace(nparams=64, waves=4)
+    ctx = hp.Context(hp.config_from(cfg))
+    E = hp.HetPipeError
+    with pytest.raises(E) as e:
+        ctx.accumulate_minibatch(0, 2)              # minibatch 2 not started
+    assert e.value.status == hp.HP_ERR_PROTOCOL
+    with pytest.raises(E):
+        ctx.push_wave(0, 0)                          # incomplete wave
+    with pytest.raises(E):
+        ctx.pull(0)                                  # not at the gate
+    ctx.accumulate_minibatch(0, 1)
+    with pytest.raises(E):
+        ctx.push_wave(0, 1)                          # out of order
+    ctx.push_wave(0, 0)
+    with pytest.raises(E):
+        ctx.push_wave(0, 0)                          # duplicate
+    cl, cg, blocked = ctx.clock(0)
+    assert (cl, cg, blocked) == (1, 0, True)         # D=0: waits for vw 1
+    before = ctx.read_weights(0)
+    assert ctx.pull(0) == hp.HP_WOULD_BLOCK
+    assert np.array_equal(ctx.read_weights(0), before)
+    ctx.accumulate_minibatch(1, 1)
+    ctx.push_wave(1, 0)
+    assert ctx.pull(0) == hp.HP_OK and ctx.pull(1) == hp.HP_OK
+    ctx.tick_end()
+    assert ctx.clock(0)[:2] == (1, 1)
+    ctx.close()
+
+
+def test_zero_and_tiny_sizes(hp):
+    for P in (0, 1, 2, 3, 5):
+        cfg = C1.replace(nparams=P, waves=3)
+        o = run_schedule(cfg)
+        trace, wg, wl, _, _ = run_device(hp, cfg)
+        assert_same(o, trace, wg, wl)
+
+
+@pytest.mark.parametrize("cfg", [C2.replace(waves=3), C3.replace(waves=3),
+                                 C5.replace(waves=2, D=4)], ids=["C2", "C3", "C5"])
+def test_full_size_sampled(hp, cfg):
+    """Full model sizes in the bench's launch configuration: sampled params
+    (stride 4099 + both ends) against the oracle restricted to that sample."""
+    idx = np.array(sample_indices(cfg.nparams), dtype=np.int64)
+    o = run_schedule(cfg, idx=idx)
+    trace, wg, wl, m, _ = run_device(hp, cfg)
+    assert_same(o, trace, wg, wl, idx=idx)
+    if cfg.momentum:
+        assert np.array_equal(m[idx], o.m)
+
+
+def test_c4_sharded_ranks_sampled(hp):
+    """ED-local placement: two rank-shards of C4 run as separate
+    contexts on one GPU reproduce the oracle at sampled params of each shard."""
+    from workloads import even_shards
+    cfg = C4.replace(waves=2)
+    b = even_shards(cfg.nparams, 2)
+    for r in range(2):
+        lo, hi = b[r], b[r + 1]
+        idx = np.array(sorted(set(list(range(lo, hi, 7919)) + [lo, lo + 1, hi - 1])), dtype=np.int64)
+        o = run_schedule(cfg, idx=idx)
+        ctx = hp.Context(hp.config_from(cfg, param_begin=lo, param_count=hi - lo))
+        ctx.run_schedule(cfg.tau, cfg.latency())
+        assert np.array_equal(ctx.read_weights(-1)[idx - lo], o.wg)
+        for v in range(cfg.num_vw):
+            assert np.array_equal(ctx.read_weights(v)[idx - lo], o.wl[v])
+        ctx.close()
