@@ -210,7 +210,8 @@ def main():
     N = cfg.num_vw
     waves = args.warmup + args.steps + 2
     run_cfg = cfg.replace(waves=waves)
-    stream = torch.cuda.current_stream(local)
+    stream = torch.cuda.Stream(local)          # a real stream: the library launches on it
+    torch.cuda.set_stream(stream)              # and the timing events below record on it
     ctx = hetpipe.Context(hetpipe.config_from(
         run_cfg, param_begin=lo, param_count=hi - lo, device=local,
         stream=stream.cuda_stream))
@@ -234,6 +235,16 @@ def main():
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
     kern_ms, kern_bytes, kern_launches = ctx.profile_read()
+    l_ms, l_bytes, l_shape = ctx.profile_launches()
+    mix = {}
+    for t_ms, by, sh in zip(l_ms, l_bytes, l_shape):
+        key = f"c{sh & 255}a{(sh >> 8) & 255}g{(sh >> 16) & 255}f{(sh >> 24) & 255}"
+        e = mix.setdefault(key, [0, 0.0, 0.0])
+        e[0] += 1
+        e[1] += float(t_ms)
+        e[2] += float(by)
+    launch_mix = {k: {"n": n, "us_mean": 1e3 * t / n, "GBps": b / (t / 1e3) / 1e9}
+                  for k, (n, t, b) in sorted(mix.items(), key=lambda kv: -kv[1][1])}
     st1 = ctx.stats()
     commits = st1.commits - st0.commits
     t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
@@ -313,6 +324,7 @@ def main():
                      "kernel_ms": kern_ms, "launches": kern_launches,
                      "alg_bytes_per_launch": kern_bytes / max(kern_launches, 1)},
         "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
+        "launch_mix": launch_mix,
         "gpu_launches": launches,
         "clocks": clocks,
         "wait_ticks_per_vw": sync_waits,

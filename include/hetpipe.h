@@ -183,6 +183,11 @@ hp_status hp_get_stats(hp_ctx* ctx, hp_stats* out);
 hp_status hp_profile_enable(hp_ctx* ctx, int32_t enable);
 hp_status hp_profile_read(hp_ctx* ctx, double* kernel_ms, double* alg_bytes,
                           int64_t* launches);
+/* Per-launch detail of the same window, up to max records: duration (ms),
+   algorithmic bytes, and shape = nc | na<<8 | ng<<16 | nf<<24 (completes,
+   applies, w_local groups, folds of the fused launch). *n = records written. */
+hp_status hp_profile_launches(hp_ctx* ctx, int64_t max, float* ms, double* alg_bytes,
+                              int32_t* shape, int64_t* n);
 
 /* Closed forms of section 5 (no context needed). */
 int64_t hp_s_global(int32_t Nm, int32_t D);                  /* (D+1)*Nm + Nm - 2 */

@@ -342,6 +342,8 @@ hp_status Engine::emit(TickDesc& d) {
     cudaEventRecord(e1, stream_);
     prof_bytes_ += bytes;
     prof_launches_++;
+    prof_launch_bytes_.push_back(bytes);
+    prof_launch_shape_.push_back(d.nc | (d.na << 8) | (d.ng << 16) | (d.nf << 24));
   }
   launches_++;
   alg_bytes_ += bytes;
@@ -486,6 +488,24 @@ hp_status Engine::profile_enable(bool on) {
   ev_used_ = 0;
   prof_bytes_ = 0;
   prof_launches_ = 0;
+  prof_launch_bytes_.clear();
+  prof_launch_shape_.clear();
+  return HP_OK;
+}
+
+hp_status Engine::profile_launches(int64_t max, float* ms, double* bytes, int32_t* shape,
+                                   int64_t* n) {
+  if (sticky_) return sticky_;
+  if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "profile sync")) return st;
+  const int64_t cnt = std::min<int64_t>(max, (int64_t)prof_launch_bytes_.size());
+  for (int64_t i = 0; i < cnt; ++i) {
+    float t = 0;
+    if (int e = cudaEventElapsedTime(&t, ev_[2 * i], ev_[2 * i + 1])) return check_cuda(e, "elapsed");
+    if (ms) ms[i] = t;
+    if (bytes) bytes[i] = prof_launch_bytes_[i];
+    if (shape) shape[i] = prof_launch_shape_[i];
+  }
+  if (n) *n = cnt;
   return HP_OK;
 }
 

@@ -68,6 +68,7 @@ class Engine {
   void stats(hp_stats* out) const;
   hp_status profile_enable(bool on);
   hp_status profile_read(double* ms, double* bytes, int64_t* launches);
+  hp_status profile_launches(int64_t max, float* ms, double* bytes, int32_t* shape, int64_t* n);
   int64_t ticks = 0;
 
  private:
@@ -119,6 +120,8 @@ class Engine {
   std::vector<cudaEvent_t> ev_;
   size_t ev_used_ = 0;
   double prof_bytes_ = 0;
+  std::vector<double> prof_launch_bytes_;
+  std::vector<int32_t> prof_launch_shape_;
   int64_t prof_launches_ = 0;
 
   std::string trace_;

@@ -100,94 +100,109 @@ __device__ __forceinline__ float4 synth_u(const TickDesc& d, uint32_t v, uint32_
                      __fmul_rn(d.neg_lr, grad_of<GM>(x.z)), __fmul_rn(d.neg_lr, grad_of<GM>(x.w)));
 }
 
-// One chunk (4 params) of the tick program. K bounds nc, na and ng.
-template <int GM, bool MOM, int K, int CNT>
-__device__ __forceinline__ void tick_chunk(const TickDesc& d, int64_t q) {
-  const uint64_t blk = (uint64_t)(d.blk_base + q);
-  // ---- 1. every load of the chunk first (they are independent) -------------
-  float4 acc_in[K], grad_in[K], src_in[K], wl_in[K], part_in[K];
-  float4 wg = make_float4(0.f, 0.f, 0.f, 0.f), mm = wg;
+// U chunks (4 params each) of the tick program, chunk u at q0 + u*qs. Every
+// load of all U chunks is issued before any arithmetic or store, so a thread
+// keeps up to U*(2K+2) 16-byte requests in flight. K bounds nc, na and ng.
+template <int GM, bool MOM, int K, int U, int CNT>
+__device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64_t qs) {
+  float4 acc_in[U][K], grad_in[U][K], src_in[U][K], wl_in[U][K], part_in[U][K];
+  float4 wg[U], mm[U];
+  // ---- 1. loads ------------------------------------------------------------
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    if (j < d.nc) {
-      if (d.c[j].flags & kLoadAcc) acc_in[j] = ld4<CNT>(d.c[j].acc, q);
-      if (GM == 2) grad_in[j] = ld4<CNT>(d.c[j].grad, q);
-    }
-    if (j < d.na && d.a[j].reg < 0) src_in[j] = ld4<CNT>(d.a[j].src, q);
-    if (j < d.ng) {
-      if (!d.g[j].pull) wl_in[j] = ld4<CNT>(d.g[j].wl, q);
-      else if (d.g[j].partial) part_in[j] = ld4<CNT>(d.g[j].partial, q);
-    }
-  }
-  if (d.wg_load) wg = ld4<CNT>(d.wg, q);
-  if (MOM && d.na > 0) mm = ld4<CNT>(d.m, q);
-
-  // ---- 2. completes: u_j, wave aggregate a_j ------------------------
-  float4 u[K], a[K];
+  for (int x = 0; x < U; ++x) {
+    const int64_t q = q0 + x * qs;
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    if (j < d.nc) {
-      const DComplete& c = d.c[j];
-      if (GM == 2) u[j] = f4scale(d.neg_lr, grad_in[j]);
-      else u[j] = synth_u<GM, CNT>(d, c.v, c.p, blk);
-      a[j] = (c.flags & kFirst) ? u[j] : f4add(acc_in[j], u[j]);
-      if (c.flags & kStoreAcc) st4<CNT>(c.acc, q, a[j]);
-    }
-  }
-  // ---- 3. PS applies in commit order (momentum Z11) -----------------
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if (k < d.na) {
-      const float4 x = d.a[k].reg >= 0 ? pick<K>(a, d.a[k].reg) : src_in[k];
-      if (MOM) {
-        mm = f4add(f4scale(d.mu, mm), x);
-        wg = f4add(wg, mm);
-      } else {
-        wg = f4add(wg, x);
+    for (int j = 0; j < K; ++j) {
+      if (j < d.nc) {
+        if (d.c[j].flags & kLoadAcc) acc_in[x][j] = ld4<CNT>(d.c[j].acc, q);
+        if (GM == 2) grad_in[x][j] = ld4<CNT>(d.c[j].grad, q);
+      }
+      if (j < d.na && d.a[j].reg < 0) src_in[x][j] = ld4<CNT>(d.a[j].src, q);
+      if (j < d.ng) {
+        if (!d.g[j].pull) wl_in[x][j] = ld4<CNT>(d.g[j].wl, q);
+        else if (d.g[j].partial) part_in[x][j] = ld4<CNT>(d.g[j].partial, q);
       }
     }
+    wg[x] = make_float4(0.f, 0.f, 0.f, 0.f);
+    mm[x] = wg[x];
+    if (d.wg_load) wg[x] = ld4<CNT>(d.wg, q);
+    if (MOM && d.na > 0) mm[x] = ld4<CNT>(d.m, q);
   }
-  if (d.na > 0) {
-    st4<CNT>(d.wg, q, wg);
-    if (MOM) st4<CNT>(d.m, q, mm);
-  }
-  // ---- 4. w_local groups: pull base then due folds ---------
 #pragma unroll
-  for (int gi = 0; gi < K; ++gi) {
-    if (gi < d.ng) {
-      const DGroup& g = d.g[gi];
-      float4 w;
-      if (g.pull) {
-        w = wg;
-        if (g.partial_reg >= 0) w = f4add(wg, pick<K>(a, g.partial_reg));
-        else if (g.partial) w = f4add(wg, part_in[gi]);
-      } else {
-        w = wl_in[gi];
+  for (int x = 0; x < U; ++x) {
+    const int64_t q = q0 + x * qs;
+    const uint64_t blk = (uint64_t)(d.blk_base + q);
+    // ---- 2. completes: u_j, wave aggregate a_j ----------------------
+    float4 u[K], a[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (j < d.nc) {
+        const DComplete& c = d.c[j];
+        if (GM == 2) u[j] = f4scale(d.neg_lr, grad_in[x][j]);
+        else u[j] = synth_u<GM, CNT>(d, c.v, c.p, blk);
+        a[j] = (c.flags & kFirst) ? u[j] : f4add(acc_in[x][j], u[j]);
+        if (c.flags & kStoreAcc) st4<CNT>(c.acc, q, a[j]);
       }
-      for (int fi = g.f_begin; fi < g.f_end; ++fi) {
-        const DFold& f = d.f[fi];
-        float4 uf;
-        if (f.reg >= 0) uf = pick<K>(u, f.reg);
-        else if (GM == 2) uf = f4scale(d.neg_lr, ld4<CNT>(f.grad, q));
-        else uf = synth_u<GM, CNT>(d, f.v, f.p, blk);
-        w = f4add(w, uf);
+    }
+    // ---- 3. PS applies in commit order (momentum Z11) ---------------
+    float4 w_g = wg[x], m_g = mm[x];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (k < d.na) {
+        const float4 v = d.a[k].reg >= 0 ? pick<K>(a, d.a[k].reg) : src_in[x][k];
+        if (MOM) {
+          m_g = f4add(f4scale(d.mu, m_g), v);
+          w_g = f4add(w_g, m_g);
+        } else {
+          w_g = f4add(w_g, v);
+        }
       }
-      st4<CNT>(g.wl, q, w);
+    }
+    if (d.na > 0) {
+      st4<CNT>(d.wg, q, w_g);
+      if (MOM) st4<CNT>(d.m, q, m_g);
+    }
+    // ---- 4. w_local groups: pull base then due folds -------
+#pragma unroll
+    for (int gi = 0; gi < K; ++gi) {
+      if (gi < d.ng) {
+        const DGroup& g = d.g[gi];
+        float4 w;
+        if (g.pull) {
+          w = w_g;
+          if (g.partial_reg >= 0) w = f4add(w_g, pick<K>(a, g.partial_reg));
+          else if (g.partial) w = f4add(w_g, part_in[x][gi]);
+        } else {
+          w = wl_in[x][gi];
+        }
+        for (int fi = g.f_begin; fi < g.f_end; ++fi) {
+          const DFold& f = d.f[fi];
+          float4 uf;
+          if (f.reg >= 0) uf = pick<K>(u, f.reg);
+          else if (GM == 2) uf = f4scale(d.neg_lr, ld4<CNT>(f.grad, q));
+          else uf = synth_u<GM, CNT>(d, f.v, f.p, blk);
+          w = f4add(w, uf);
+        }
+        st4<CNT>(g.wl, q, w);
+      }
     }
   }
 }
 
-template <int GM, bool MOM, int K>
+template <int GM, bool MOM, int K, int U>
 __global__ void __launch_bounds__(256) tick_kernel(const __grid_constant__ TickDesc d) {
   const int64_t nfull = d.n >> 2;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t S = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (int64_t q = t0; q < nfull; q += stride) tick_chunk<GM, MOM, K, 4>(d, q);
+  const int64_t groups = nfull / (S * U);          // rounds where every thread has U chunks
+  int64_t q = t0;
+  for (int64_t r = 0; r < groups; ++r, q += S * U) tick_chunks<GM, MOM, K, U, 4>(d, q, S);
+  for (; q < nfull; q += S) tick_chunks<GM, MOM, K, 1, 4>(d, q, S);
   if (t0 == 0) {
     switch (d.n & 3) {
-      case 1: tick_chunk<GM, MOM, K, 1>(d, nfull); break;
-      case 2: tick_chunk<GM, MOM, K, 2>(d, nfull); break;
-      case 3: tick_chunk<GM, MOM, K, 3>(d, nfull); break;
+      case 1: tick_chunks<GM, MOM, K, 1, 1>(d, nfull, 0); break;
+      case 2: tick_chunks<GM, MOM, K, 1, 2>(d, nfull, 0); break;
+      case 3: tick_chunks<GM, MOM, K, 1, 3>(d, nfull, 0); break;
       default: break;
     }
   }
@@ -211,21 +226,21 @@ __global__ void init_kernel(float* out, int64_t n, int64_t param_begin, int w0_m
   }
 }
 
-template <int GM, bool MOM, int K>
+template <int GM, bool MOM, int K, int U>
 int launch_k(const TickDesc& d, cudaStream_t s) {
   static int grid_max = 0;
   if (grid_max == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tick_kernel<GM, MOM, K>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tick_kernel<GM, MOM, K, U>, 256, 0);
     grid_max = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int64_t chunks = (d.n + 3) >> 2;
   int64_t blocks = (chunks + 255) / 256;
   if (blocks > grid_max) blocks = grid_max;
   if (blocks < 1) blocks = 1;
-  tick_kernel<GM, MOM, K><<<(unsigned)blocks, 256, 0, s>>>(d);
+  tick_kernel<GM, MOM, K, U><<<(unsigned)blocks, 256, 0, s>>>(d);
   return (int)cudaGetLastError();
 }
 
@@ -234,10 +249,10 @@ int launch_gm(const TickDesc& d, cudaStream_t s) {
   int k = d.nc;
   if (d.na > k) k = d.na;
   if (d.ng > k) k = d.ng;
-  if (k <= 1) return launch_k<GM, MOM, 1>(d, s);
-  if (k <= 2) return launch_k<GM, MOM, 2>(d, s);
-  if (k <= 4) return launch_k<GM, MOM, 4>(d, s);
-  return launch_k<GM, MOM, 8>(d, s);
+  if (k <= 1) return launch_k<GM, MOM, 1, 4>(d, s);
+  if (k <= 2) return launch_k<GM, MOM, 2, 2>(d, s);
+  if (k <= 4) return launch_k<GM, MOM, 4, 1>(d, s);
+  return launch_k<GM, MOM, 8, 1>(d, s);
 }
 
 }  // namespace

@@ -72,6 +72,8 @@ EXPORTS = {
     "hp_profile_enable": (C.c_int, [C.c_void_p, C.c_int32]),
     "hp_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                   C.POINTER(C.c_int64)]),
+    "hp_profile_launches": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.POINTER(C.c_int64)]),
     "hp_s_global": (C.c_int64, [C.c_int32, C.c_int32]),
     "hp_version_floor": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
     "hp_last_error": (C.c_char_p, [C.c_void_p]),
@@ -107,6 +109,8 @@ def config_from(cfg, **overrides) -> hp_config:
     c.pull_policy, c.local_semantics = cfg.pull_policy, cfg.local_semantics
     for k, v in overrides.items():
         setattr(c, k, v)
+    if c.param_count < 0:
+        c.param_count = c.nparams - c.param_begin
     return c
 
 
@@ -228,6 +232,21 @@ class Context:
         ms, b, n = C.c_double(), C.c_double(), C.c_int64()
         self._chk(self.lib.hp_profile_read(self.h, C.byref(ms), C.byref(b), C.byref(n)))
         return ms.value, b.value, n.value
+
+
+def _profile_launches(self, max_records: int = 1 << 16):
+    ms = np.zeros(max_records, dtype=np.float32)
+    by = np.zeros(max_records, dtype=np.float64)
+    sh = np.zeros(max_records, dtype=np.int32)
+    n = C.c_int64()
+    self._chk(self.lib.hp_profile_launches(self.h, max_records, ms.ctypes.data_as(C.c_void_p),
+                                           by.ctypes.data_as(C.c_void_p),
+                                           sh.ctypes.data_as(C.c_void_p), C.byref(n)))
+    k = n.value
+    return ms[:k], by[:k], sh[:k]
+
+
+Context.profile_launches = _profile_launches
 
 
 def s_global(Nm: int, D: int) -> int:
