@@ -307,22 +307,12 @@ hp_status Engine::emit(TickDesc& d) {
   d.mu = cfg_.momentum;
   d.key0 = (uint32_t)(cfg_.seed & 0xffffffffu);
   d.key1 = (uint32_t)(cfg_.seed >> 32);
-  bool any_pull = false;
+  bool any_pull = false, apply_now = false;
   for (int g = 0; g < d.ng; ++g) any_pull |= d.g[g].pull != 0;
-  d.wg_load = (d.na > 0 || any_pull) ? 1 : 0;
-  int streams = 0;  // buffer passes
-  for (int j = 0; j < d.nc; ++j) {
-    streams += (d.c[j].flags & kLoadAcc) ? 1 : 0;
-    streams += (d.c[j].flags & kStoreAcc) ? 1 : 0;
-    streams += d.c[j].grad ? 1 : 0;
-  }
-  for (int k = 0; k < d.na; ++k) streams += d.a[k].reg < 0 ? 1 : 0;
-  streams += d.wg_load + (d.na > 0 ? 1 : 0);
-  if (m_ && d.na > 0) streams += 2;
-  for (int g = 0; g < d.ng; ++g) {
-    streams += 1 + (d.g[g].pull ? 0 : 1) + (d.g[g].partial ? 1 : 0);
-    for (int f = d.g[g].f_begin; f < d.g[g].f_end; ++f) streams += d.f[f].grad ? 1 : 0;
-  }
+  for (int j = 0; j < d.nc; ++j) apply_now |= (d.c[j].flags & kApplyNow) != 0;
+  d.wg_store = (d.na > 0 || apply_now) ? 1 : 0;
+  d.wg_load = (d.wg_store || any_pull) ? 1 : 0;
+  const int streams = tick_streams(d);
   const double bytes = 4.0 * (double)n_ * streams;
   if (d.nc == 0 && d.na == 0 && d.ng == 0) return HP_OK;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -353,46 +343,55 @@ hp_status Engine::emit(TickDesc& d) {
 hp_status Engine::flush() {
   if (sticky_) return sticky_;
   const bool strict = cfg_.local_semantics == HP_LOCAL_STRICT;
-  // 1. applies beyond kMaxA (oldest first) go out in apply-only launches
-  size_t a0 = 0;
-  while (ba_.size() - a0 > (size_t)kMaxA) {
-    TickDesc d;
-    memset(&d, 0, sizeof d);
-    for (int k = 0; k < kMaxA; ++k, ++a0) {
-      d.a[k].src = vw_[ba_[a0].v].acc[ba_[a0].slot];
-      d.a[k].reg = -1;
-    }
-    d.na = kMaxA;
-    applied_ += kMaxA;
-    if (hp_status st = emit(d)) return st;
-  }
   TickDesc d;
   memset(&d, 0, sizeof d);
-  // 2. completes
+  // 1. completes (phase B)
   d.nc = (int)bc_.size();
   for (int j = 0; j < d.nc; ++j) {
     const BComplete& b = bc_[j];
     DComplete& c = d.c[j];
     c.acc = vw_[b.v].acc[b.slot];
     c.grad = b.grad;
+    c.wl = nullptr;
     c.v = (uint32_t)b.v;
     c.p = (uint32_t)b.p;
     c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc;
   }
-  // 3. applies in commit order; a wave completed in this batch comes from its register
-  for (size_t k = a0; k < ba_.size(); ++k) {
-    DApply& a = d.a[d.na++];
-    a.reg = -1;
-    a.src = vw_[ba_[k].v].acc[ba_[k].slot];
+  // 2. applies in commit order. The longest suffix whose waves were completed
+  //    in this batch, in complete order, is applied straight from registers in
+  //    phase B (u~ never reaches HBM); the rest are read from their acc slots in
+  //    phase A, oldest first, overflow in apply-only launches before this one.
+  size_t reg_from = ba_.size();
+  int next_j = d.nc;
+  while (reg_from > 0) {
+    const BApply& a = ba_[reg_from - 1];
+    int jj = -1;
+    for (int j = 0; j < d.nc; ++j)
+      if (bc_[j].v == a.v && bc_[j].wave_end && wave_of(bc_[j].p, Nm_) == a.c) jj = j;
+    if (jj < 0 || jj >= next_j) break;
+    next_j = jj;
+    --reg_from;
+  }
+  for (size_t k = reg_from; k < ba_.size(); ++k) {
     for (int j = 0; j < d.nc; ++j) {
       if (bc_[j].v == ba_[k].v && bc_[j].wave_end && wave_of(bc_[j].p, Nm_) == ba_[k].c) {
-        a.reg = j;
-        d.c[j].flags &= ~kStoreAcc;   // applied here: u~ never needs to reach HBM
+        d.c[j].flags |= kApplyNow;
+        d.c[j].flags &= ~kStoreAcc;
       }
     }
-    applied_++;
   }
-  // 4. w_local groups: pulled VWs and VWs whose folds are due now
+  size_t a0 = 0;
+  while (reg_from - a0 > (size_t)kMaxA) {
+    TickDesc pre;
+    memset(&pre, 0, sizeof pre);
+    for (int k = 0; k < kMaxA; ++k, ++a0) pre.a[k].src = vw_[ba_[a0].v].acc[ba_[a0].slot];
+    pre.na = kMaxA;
+    if (hp_status st = emit(pre)) return st;
+  }
+  for (size_t k = a0; k < reg_from; ++k) d.a[d.na++].src = vw_[ba_[k].v].acc[ba_[k].slot];
+  applied_ += (int64_t)ba_.size();
+  // 3. w_local: pulled VWs and VWs whose folds are due now (phase D), or the
+  //    single due fold of this batch's own complete, folded inline (phase B)
   for (int v = 0; v < N_; ++v) {
     VW& s = vw_[v];
     const bool pulled = std::find(bpull_.begin(), bpull_.end(), v) != bpull_.end();
@@ -400,36 +399,34 @@ hp_status Engine::flush() {
     if (!pulled && (hold || s.pending_folds.empty())) continue;
     std::vector<int64_t> folds;
     if (!hold) folds.swap(s.pending_folds);
+    if (!pulled && folds.size() == 1) {
+      int jj = -1;
+      for (int j = 0; j < d.nc; ++j)
+        if (bc_[j].v == v && bc_[j].p == folds[0]) jj = j;
+      if (jj >= 0) {
+        d.c[jj].flags |= kFoldInline;
+        d.c[jj].wl = s.wl;
+        continue;
+      }
+    }
     size_t fi = 0;
     do {  // split a group whose folds overflow the descriptor
       if (d.ng == kMaxG || d.nf == kMaxF) {
         if (hp_status st = emit(d)) return st;
-        TickDesc nd;
-        memset(&nd, 0, sizeof nd);
-        d = nd;
+        memset(&d, 0, sizeof d);
       }
       DGroup& g = d.g[d.ng++];
       g.wl = s.wl;
       g.pull = (pulled && fi == 0) ? 1 : 0;
       g.partial = nullptr;
-      g.partial_reg = -1;
-      if (g.pull && !strict && s.acc_count > 0) {  // AT_LEAST: w_global + partial u~
-        const int64_t open = s.c_local;
-        g.partial = s.acc[open % R_];
-        for (int j = 0; j < d.nc; ++j)
-          if (bc_[j].v == v && wave_of(bc_[j].p, Nm_) == open) g.partial_reg = j;
-        if (g.partial_reg >= 0) g.partial = nullptr;
-      }
+      if (g.pull && !strict && s.acc_count > 0)   // AT_LEAST: w_global + partial u~
+        g.partial = s.acc[s.c_local % R_];        // stored in phase B if completed now
       g.f_begin = d.nf;
       for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
         DFold& f = d.f[d.nf++];
         f.v = (uint32_t)v;
         f.p = (uint32_t)folds[fi];
-        f.reg = -1;
-        f.grad = nullptr;
-        for (int j = 0; j < d.nc; ++j)
-          if (bc_[j].v == v && bc_[j].p == folds[fi]) f.reg = j;
-        if (f.reg < 0) f.grad = fold_grad(v, folds[fi]);
+        f.grad = fold_grad(v, folds[fi]);
       }
       g.f_end = d.nf;
     } while (fi < folds.size());

@@ -12,6 +12,7 @@
 // (P:839 w_local + u_p, P:929 w_global + u~) under reading Z10.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "tick_desc.h"
 
@@ -82,17 +83,8 @@ __device__ __forceinline__ void st4(float* base, int64_t q, float4 v) {
   if (CNT > 2) p[2] = v.z;
 }
 
-template <int K>
-__device__ __forceinline__ float4 pick(const float4 (&arr)[K], int r) {
-  float4 x = arr[0];
-#pragma unroll
-  for (int j = 1; j < K; ++j)
-    if (r == j) x = arr[j];
-  return x;
-}
-
 // u = fl(-lr * g) for the 4 params of global block blk.
-template <int GM, int CNT>
+template <int GM>
 __device__ __forceinline__ float4 synth_u(const TickDesc& d, uint32_t v, uint32_t p,
                                           uint64_t blk) {
   const uint4 x = philox4x32_10((uint32_t)blk, v, p, 0u, d.key0, d.key1);
@@ -100,109 +92,115 @@ __device__ __forceinline__ float4 synth_u(const TickDesc& d, uint32_t v, uint32_
                      __fmul_rn(d.neg_lr, grad_of<GM>(x.z)), __fmul_rn(d.neg_lr, grad_of<GM>(x.w)));
 }
 
-// U chunks (4 params each) of the tick program, chunk u at q0 + u*qs. Every
-// load of all U chunks is issued before any arithmetic or store, so a thread
-// keeps up to U*(2K+2) 16-byte requests in flight. K bounds nc, na and ng.
-template <int GM, bool MOM, int K, int U, int CNT>
-__device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64_t qs) {
-  float4 acc_in[U][K], grad_in[U][K], src_in[U][K], wl_in[U][K], part_in[U][K];
-  float4 wg[U], mm[U];
-  // ---- 1. loads ------------------------------------------------------------
-#pragma unroll
-  for (int x = 0; x < U; ++x) {
-    const int64_t q = q0 + x * qs;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      if (j < d.nc) {
-        if (d.c[j].flags & kLoadAcc) acc_in[x][j] = ld4<CNT>(d.c[j].acc, q);
-        if (GM == 2) grad_in[x][j] = ld4<CNT>(d.c[j].grad, q);
-      }
-      if (j < d.na && d.a[j].reg < 0) src_in[x][j] = ld4<CNT>(d.a[j].src, q);
-      if (j < d.ng) {
-        if (!d.g[j].pull) wl_in[x][j] = ld4<CNT>(d.g[j].wl, q);
-        else if (d.g[j].partial) part_in[x][j] = ld4<CNT>(d.g[j].partial, q);
-      }
-    }
-    wg[x] = make_float4(0.f, 0.f, 0.f, 0.f);
-    mm[x] = wg[x];
-    if (d.wg_load) wg[x] = ld4<CNT>(d.wg, q);
-    if (MOM && d.na > 0) mm[x] = ld4<CNT>(d.m, q);
-  }
-#pragma unroll
-  for (int x = 0; x < U; ++x) {
-    const int64_t q = q0 + x * qs;
-    const uint64_t blk = (uint64_t)(d.blk_base + q);
-    // ---- 2. completes: u_j, wave aggregate a_j ----------------------
-    float4 u[K], a[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      if (j < d.nc) {
-        const DComplete& c = d.c[j];
-        if (GM == 2) u[j] = f4scale(d.neg_lr, grad_in[x][j]);
-        else u[j] = synth_u<GM, CNT>(d, c.v, c.p, blk);
-        a[j] = (c.flags & kFirst) ? u[j] : f4add(acc_in[x][j], u[j]);
-        if (c.flags & kStoreAcc) st4<CNT>(c.acc, q, a[j]);
-      }
-    }
-    // ---- 3. PS applies in commit order (momentum Z11) ---------------
-    float4 w_g = wg[x], m_g = mm[x];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (k < d.na) {
-        const float4 v = d.a[k].reg >= 0 ? pick<K>(a, d.a[k].reg) : src_in[x][k];
-        if (MOM) {
-          m_g = f4add(f4scale(d.mu, m_g), v);
-          w_g = f4add(w_g, m_g);
-        } else {
-          w_g = f4add(w_g, v);
-        }
-      }
-    }
-    if (d.na > 0) {
-      st4<CNT>(d.wg, q, w_g);
-      if (MOM) st4<CNT>(d.m, q, m_g);
-    }
-    // ---- 4. w_local groups: pull base then due folds -------
-#pragma unroll
-    for (int gi = 0; gi < K; ++gi) {
-      if (gi < d.ng) {
-        const DGroup& g = d.g[gi];
-        float4 w;
-        if (g.pull) {
-          w = w_g;
-          if (g.partial_reg >= 0) w = f4add(w_g, pick<K>(a, g.partial_reg));
-          else if (g.partial) w = f4add(w_g, part_in[x][gi]);
-        } else {
-          w = wl_in[x][gi];
-        }
-        for (int fi = g.f_begin; fi < g.f_end; ++fi) {
-          const DFold& f = d.f[fi];
-          float4 uf;
-          if (f.reg >= 0) uf = pick<K>(u, f.reg);
-          else if (GM == 2) uf = f4scale(d.neg_lr, ld4<CNT>(f.grad, q));
-          else uf = synth_u<GM, CNT>(d, f.v, f.p, blk);
-          w = f4add(w, uf);
-        }
-        st4<CNT>(g.wl, q, w);
-      }
-    }
+template <bool MOM>
+__device__ __forceinline__ void apply(float4& wg, float4& m, float4 ut, float mu) {
+  if (MOM) {
+    m = f4add(f4scale(mu, m), ut);   // m = mu*m + u~   (Z11)
+    wg = f4add(wg, m);               // w_global += m
+  } else {
+    wg = f4add(wg, ut);              // w_global += u~
   }
 }
 
-template <int GM, bool MOM, int K, int U>
+// U chunks (4 params each), chunk x at q0 + x*qs, through phases A-D of
+// tick_desc.h. Inside each op the loads of all U chunks are issued together,
+// so a thread keeps U (or 2U-3U) 16-byte requests in flight per op while its
+// register footprint stays independent of the number of ops in the tick.
+template <int GM, bool MOM, int U, int CNT>
+__device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64_t qs) {
+  float4 wg[U], mm[U];
+#pragma unroll
+  for (int x = 0; x < U; ++x) {
+    wg[x] = make_float4(0.f, 0.f, 0.f, 0.f);
+    mm[x] = wg[x];
+  }
+  if (d.wg_load) {
+#pragma unroll
+    for (int x = 0; x < U; ++x) wg[x] = ld4<CNT>(d.wg, q0 + x * qs);
+  }
+  if (MOM && d.wg_store) {
+#pragma unroll
+    for (int x = 0; x < U; ++x) mm[x] = ld4<CNT>(d.m, q0 + x * qs);
+  }
+  // ---- A. memory-sourced applies, commit order ------------------------------
+  for (int k = 0; k < d.na; ++k) {
+    float4 s[U];
+#pragma unroll
+    for (int x = 0; x < U; ++x) s[x] = ld4<CNT>(d.a[k].src, q0 + x * qs);
+#pragma unroll
+    for (int x = 0; x < U; ++x) apply<MOM>(wg[x], mm[x], s[x], d.mu);
+  }
+  // ---- B. completes --------------------------------------------------------
+  for (int j = 0; j < d.nc; ++j) {
+    const DComplete& c = d.c[j];
+    const uint32_t fl = c.flags;
+    float4 ain[U], win[U], gin[U];
+#pragma unroll
+    for (int x = 0; x < U; ++x) {
+      const int64_t q = q0 + x * qs;
+      if (fl & kLoadAcc) ain[x] = ld4<CNT>(c.acc, q);
+      if (fl & kFoldInline) win[x] = ld4<CNT>(c.wl, q);
+      if (GM == 2) gin[x] = ld4<CNT>(c.grad, q);
+    }
+#pragma unroll
+    for (int x = 0; x < U; ++x) {
+      const int64_t q = q0 + x * qs;
+      const float4 u = (GM == 2) ? f4scale(d.neg_lr, gin[x])
+                                 : synth_u<GM>(d, c.v, c.p, (uint64_t)(d.blk_base + q));
+      const float4 a = (fl & kFirst) ? u : f4add(ain[x], u);   // wave aggregate
+      if (fl & kStoreAcc) st4<CNT>(c.acc, q, a);
+      if (fl & kApplyNow) apply<MOM>(wg[x], mm[x], a, d.mu);
+      if (fl & kFoldInline) st4<CNT>(c.wl, q, f4add(win[x], u));
+    }
+  }
+  // ---- C. store w_global / m ------------------------------------------------
+  if (d.wg_store) {
+#pragma unroll
+    for (int x = 0; x < U; ++x) {
+      st4<CNT>(d.wg, q0 + x * qs, wg[x]);
+      if (MOM) st4<CNT>(d.m, q0 + x * qs, mm[x]);
+    }
+  }
+  // ---- D. w_local groups: pull base then due folds ---------
+  for (int gi = 0; gi < d.ng; ++gi) {
+    const DGroup& g = d.g[gi];
+    float4 w[U];
+#pragma unroll
+    for (int x = 0; x < U; ++x) {
+      const int64_t q = q0 + x * qs;
+      if (!g.pull) w[x] = ld4<CNT>(g.wl, q);
+      else if (g.partial) w[x] = f4add(wg[x], ld4<CNT>(g.partial, q));
+      else w[x] = wg[x];
+    }
+    for (int fi = g.f_begin; fi < g.f_end; ++fi) {
+      const DFold& f = d.f[fi];
+#pragma unroll
+      for (int x = 0; x < U; ++x) {
+        const int64_t q = q0 + x * qs;
+        const float4 uf = (GM == 2) ? f4scale(d.neg_lr, ld4<CNT>(f.grad, q))
+                                    : synth_u<GM>(d, f.v, f.p, (uint64_t)(d.blk_base + q));
+        w[x] = f4add(w[x], uf);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < U; ++x) st4<CNT>(g.wl, q0 + x * qs, w[x]);
+  }
+}
+
+template <int GM, bool MOM, int U>
 __global__ void __launch_bounds__(256) tick_kernel(const __grid_constant__ TickDesc d) {
   const int64_t nfull = d.n >> 2;
   const int64_t S = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t groups = nfull / (S * U);          // rounds where every thread has U chunks
   int64_t q = t0;
-  for (int64_t r = 0; r < groups; ++r, q += S * U) tick_chunks<GM, MOM, K, U, 4>(d, q, S);
-  for (; q < nfull; q += S) tick_chunks<GM, MOM, K, 1, 4>(d, q, S);
+  for (int64_t r = 0; r < groups; ++r, q += S * U) tick_chunks<GM, MOM, U, 4>(d, q, S);
+  for (; q < nfull; q += S) tick_chunks<GM, MOM, 1, 4>(d, q, S);
   if (t0 == 0) {
     switch (d.n & 3) {
-      case 1: tick_chunks<GM, MOM, K, 1, 1>(d, nfull, 0); break;
-      case 2: tick_chunks<GM, MOM, K, 1, 2>(d, nfull, 0); break;
-      case 3: tick_chunks<GM, MOM, K, 1, 3>(d, nfull, 0); break;
+      case 1: tick_chunks<GM, MOM, 1, 1>(d, nfull, 0); break;
+      case 2: tick_chunks<GM, MOM, 1, 2>(d, nfull, 0); break;
+      case 3: tick_chunks<GM, MOM, 1, 3>(d, nfull, 0); break;
       default: break;
     }
   }
@@ -226,39 +224,44 @@ __global__ void init_kernel(float* out, int64_t n, int64_t param_begin, int w0_m
   }
 }
 
-template <int GM, bool MOM, int K, int U>
-int launch_k(const TickDesc& d, cudaStream_t s) {
+int g_u_override = -1;   // HP_TICK_U: tuning override of chunks per thread
+
+template <int GM, bool MOM, int U>
+int launch_u(const TickDesc& d, cudaStream_t s) {
   static int grid_max = 0;
   if (grid_max == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tick_kernel<GM, MOM, K, U>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tick_kernel<GM, MOM, U>, 256, 0);
     grid_max = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int64_t chunks = (d.n + 3) >> 2;
   int64_t blocks = (chunks + 255) / 256;
   if (blocks > grid_max) blocks = grid_max;
   if (blocks < 1) blocks = 1;
-  tick_kernel<GM, MOM, K, U><<<(unsigned)blocks, 256, 0, s>>>(d);
+  tick_kernel<GM, MOM, U><<<(unsigned)blocks, 256, 0, s>>>(d);
   return (int)cudaGetLastError();
 }
 
 template <int GM, bool MOM>
 int launch_gm(const TickDesc& d, cudaStream_t s) {
-  int k = d.nc;
-  if (d.na > k) k = d.na;
-  if (d.ng > k) k = d.ng;
-  if (k <= 1) return launch_k<GM, MOM, 1, 4>(d, s);
-  if (k <= 2) return launch_k<GM, MOM, 2, 2>(d, s);
-  if (k <= 4) return launch_k<GM, MOM, 4, 1>(d, s);
-  return launch_k<GM, MOM, 8, 1>(d, s);
+  // Thin ticks (few buffer passes) need more chunks in flight per thread.
+  int u = tick_streams(d) <= 3 ? 8 : 4;
+  if (g_u_override > 0) u = g_u_override;
+  if (u >= 8) return launch_u<GM, MOM, 8>(d, s);
+  if (u >= 4) return launch_u<GM, MOM, 4>(d, s);
+  return launch_u<GM, MOM, 2>(d, s);
 }
 
 }  // namespace
 
 int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  if (g_u_override == -1) {
+    const char* e = getenv("HP_TICK_U");
+    g_u_override = e ? atoi(e) : 0;
+  }
   if (d.n <= 0) return 0;
   switch (grad_mode) {
     case 0: return momentum ? launch_gm<0, true>(d, s) : launch_gm<0, false>(d, s);

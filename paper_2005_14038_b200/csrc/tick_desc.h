@@ -2,53 +2,59 @@
 //
 // Every WSP operation is element-wise in the parameter index (PAPER.md P:839
 // w_local += u_p, P:922 wave aggregate, P:929 w_global += u~, P:949 pull), so all
-// operations of one controller tick can run in ONE pass over the parameters with
-// every intermediate held in registers. The host engine builds a TickDesc per
-// tick in the paper's phase order (Z5):
-//   1. completes  u_j = fl(-lr*g(v_j,p_j));  a_j = first ? u_j : acc_j + u_j
-//   2. applies    in commit order: w_global += a (or m = mu*m + a; w += m)
-//   3. groups     per VW: w = pull ? w_global (+ partial u~) : w_local;
-//                 then the VW's due folds w += u_f in minibatch order; store w
+// operations of one controller tick run in ONE pass over the parameters. The
+// host engine builds a TickDesc per tick; the kernel executes, per param:
+//   A. memory applies  w_global += u~ (or m = mu*m + u~; w += m) for pushes whose
+//                      u~ is in an acc slot, in commit order (Z4, Z11)
+//   B. completes       u = fl(-lr*g(v,p)); a = first ? u : acc + u;
+//                      [store acc]; [apply a now: this tick's pushes, which come
+//                      last in commit order]; [inline fold w_local += u]
+//   C. store w_global (and m) if anything was applied
+//   D. w_local groups  w = pull ? w_global (+ partial u~, AT_LEAST) : w_local;
+//                      then the VW's due folds w += u in minibatch order; store
 // Passed by value as a __grid_constant__ kernel parameter (< 4 KB).
 #pragma once
 #include <stdint.h>
 
 namespace hp {
 
-constexpr int kMaxC = 8;    // completes per tick (at most one per VW)
-constexpr int kMaxA = 8;    // applies per launch
+constexpr int kMaxC = 8;    // completes per launch (at most one per VW per tick)
+constexpr int kMaxA = 16;   // memory-sourced applies per launch
 constexpr int kMaxG = 8;    // w_local groups per launch (one per VW)
-constexpr int kMaxF = 48;   // folds per launch
+constexpr int kMaxF = 40;   // folds per launch
 
-enum : uint32_t { kFirst = 1u, kStoreAcc = 2u, kLoadAcc = 4u };
+enum : uint32_t {
+  kFirst = 1u,       // first minibatch of its wave: a = u
+  kStoreAcc = 2u,    // write a back to the acc slot
+  kLoadAcc = 4u,     // read the acc slot (not first)
+  kApplyNow = 8u,    // w_global += a right after this complete (commit order)
+  kFoldInline = 16u  // w_local(v) += u right here (the VW's only due fold)
+};
 
 struct DComplete {
   float* acc;          // acc slot of the wave p belongs to
   const float* grad;   // EXTERNAL gradient (local shard) or nullptr
+  float* wl;           // w_local for kFoldInline, else nullptr
   uint32_t v, p;
-  uint32_t flags;      // kFirst | kStoreAcc
+  uint32_t flags;
   uint32_t pad;
 };
 
 struct DApply {
-  const float* src;    // acc slot in memory, used when reg < 0
-  int32_t reg;         // complete index whose register holds u~, or -1
-  int32_t pad;
+  const float* src;    // acc slot holding u~ of an earlier push
 };
 
 struct DFold {
-  const float* grad;   // EXTERNAL gradient or nullptr
+  const float* grad;   // EXTERNAL gradient or nullptr (synthetic: regenerate)
   uint32_t v, p;
-  int32_t reg;         // complete index whose register holds u_p, or -1
-  int32_t pad;
 };
 
 struct DGroup {
   float* wl;             // w_local of this VW (local shard)
-  const float* partial;  // AT_LEAST pull: open-wave acc in memory, or nullptr
+  const float* partial;  // AT_LEAST pull: open-wave acc slot, or nullptr
   int32_t pull;          // 1: base = w_global (+partial); 0: base = w_local
-  int32_t partial_reg;   // complete index holding the partial, or -1
   int32_t f_begin, f_end;
+  int32_t pad;
 };
 
 struct TickDesc {
@@ -61,7 +67,7 @@ struct TickDesc {
   uint32_t key0, key1;  // Philox key = seed
   int32_t nc, na, ng, nf;
   int32_t wg_load;      // w_global must be read (applies or pulls present)
-  int32_t pad;
+  int32_t wg_store;     // w_global (and m) must be written (applies present)
   DComplete c[kMaxC];
   DApply a[kMaxA];
   DGroup g[kMaxG];
@@ -69,6 +75,24 @@ struct TickDesc {
 };
 
 static_assert(sizeof(TickDesc) <= 4000, "TickDesc must fit a kernel parameter");
+
+// Buffer passes of one launch (each = 4 bytes per param): the algorithmic
+// bytes the fused tick must move, used for the roofline.
+inline int tick_streams(const TickDesc& d) {
+  int s = d.wg_load + (d.wg_store ? 1 : 0);
+  if (d.m && d.wg_store) s += 2;
+  s += d.na;
+  for (int j = 0; j < d.nc; ++j) {
+    const uint32_t f = d.c[j].flags;
+    s += ((f & kLoadAcc) ? 1 : 0) + ((f & kStoreAcc) ? 1 : 0) + (d.c[j].grad ? 1 : 0) +
+         ((f & kFoldInline) ? 2 : 0);
+  }
+  for (int g = 0; g < d.ng; ++g) {
+    s += 1 + (d.g[g].pull ? 0 : 1) + (d.g[g].partial ? 1 : 0);
+    for (int k = d.g[g].f_begin; k < d.g[g].f_end; ++k) s += d.f[k].grad ? 1 : 0;
+  }
+  return s;
+}
 
 // Launch the fused tick kernel (kernels.cu). grad_mode: HP_GRAD_*.
 // Returns a cudaError_t as int.

@@ -82,19 +82,28 @@ EXPORTS = {
 }
 
 
+def _bind(lib: C.CDLL) -> C.CDLL:
+    for name, (res, args) in EXPORTS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
 def load() -> C.CDLL:
     """Load libhetpipe.so (built by paper_2005_14038_b200.build); raise if absent."""
     global _lib
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2005_14038_b200.build`")
-        lib = C.CDLL(LIB_PATH)
-        for name, (res, args) in EXPORTS.items():
-            fn = getattr(lib, name)
-            fn.restype = res
-            fn.argtypes = args
-        _lib = lib
+        _lib = _bind(C.CDLL(LIB_PATH))
     return _lib
+
+
+def load_test_library(path: str) -> C.CDLL:
+    """Bind another build of the same ABI (tests/emu's host-emulated engine,
+    used only by CPU tests of the host logic). Never used by the product."""
+    return _bind(C.CDLL(path))
 
 
 def config_from(cfg, **overrides) -> hp_config:
@@ -117,8 +126,8 @@ def config_from(cfg, **overrides) -> hp_config:
 class Context:
     """One hp_ctx (one rank). Methods carry the C names without the prefix."""
 
-    def __init__(self, cfg: hp_config):
-        self.lib = load()
+    def __init__(self, cfg: hp_config, lib: Optional[C.CDLL] = None):
+        self.lib = lib if lib is not None else load()
         self.cfg = cfg
         h = C.c_void_p()
         st = self.lib.hp_init_ex(C.byref(h), C.byref(cfg))

@@ -1,0 +1,91 @@
+// TEST-ONLY host emulation of the tick descriptor semantics (tick_desc.h
+// phases A-D) and of the w0 initialisation, scalar and sequential. Lets CPU
+// tests check the engine's host logic against the oracle. Compiled with
+// -ffp-contract=off so every float op rounds once, as __fadd_rn/__fmul_rn do.
+#include <stdint.h>
+
+#include "../../paper_2005_14038_b200/csrc/tick_desc.h"
+
+namespace hp {
+namespace {
+
+void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = (uint32_t)p1;
+    c[2] = n2;
+    c[3] = (uint32_t)p0;
+  }
+}
+
+float draw_u(const TickDesc& d, int gm, uint32_t v, uint32_t p, int64_t i, const float* grad) {
+  if (gm == 2) return d.neg_lr * grad[i];
+  const int64_t gi = d.blk_base * 4 + i;
+  uint32_t c[4] = {(uint32_t)(gi >> 2), v, p, 0u};
+  philox(c, d.key0, d.key1);
+  const uint32_t x = c[gi & 3];
+  const float g = gm == 1 ? (float)((int)(x >> 28) - 8) : (float)(x >> 8) * 0x1p-24f - 0.5f;
+  return d.neg_lr * g;
+}
+
+void app(const TickDesc& d, bool mom, float& wg, float& m, float ut) {
+  if (mom) {
+    m = d.mu * m + ut;
+    wg = wg + m;
+  } else {
+    wg = wg + ut;
+  }
+}
+
+}  // namespace
+
+int launch_tick(const TickDesc& d, int gm, bool mom, void*) {
+  for (int64_t i = 0; i < d.n; ++i) {
+    float wg = d.wg_load ? d.wg[i] : 0.f;
+    float m = (mom && d.wg_store) ? d.m[i] : 0.f;
+    for (int k = 0; k < d.na; ++k) app(d, mom, wg, m, d.a[k].src[i]);
+    for (int j = 0; j < d.nc; ++j) {
+      const DComplete& c = d.c[j];
+      const float u = draw_u(d, gm, c.v, c.p, i, c.grad);
+      const float a = (c.flags & kFirst) ? u : c.acc[i] + u;
+      if (c.flags & kStoreAcc) c.acc[i] = a;
+      if (c.flags & kApplyNow) app(d, mom, wg, m, a);
+      if (c.flags & kFoldInline) c.wl[i] = c.wl[i] + u;
+    }
+    if (d.wg_store) {
+      d.wg[i] = wg;
+      if (mom) d.m[i] = m;
+    }
+    for (int g = 0; g < d.ng; ++g) {
+      const DGroup& G = d.g[g];
+      float w = !G.pull ? G.wl[i] : G.partial ? wg + G.partial[i] : wg;
+      for (int f = G.f_begin; f < G.f_end; ++f) w = w + draw_u(d, gm, d.f[f].v, d.f[f].p, i, d.f[f].grad);
+      G.wl[i] = w;
+    }
+  }
+  return 0;
+}
+
+int launch_init(float* out, int64_t n, int64_t begin, int w0_mode, int gm, uint32_t k0,
+                uint32_t k1, void*) {
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t gi = begin + i;
+    float w = 0.f;
+    if (w0_mode == 1) {
+      uint32_t c[4] = {(uint32_t)(gi >> 2), 0u, 0u, 1u};
+      philox(c, k0, k1);
+      const uint32_t x = c[gi & 3];
+      w = gm == 1 ? (float)(x >> 25) * 0x1p-6f - 1.0f : 2.0f * ((float)(x >> 8) * 0x1p-24f) - 1.0f;
+    }
+    out[i] = w;
+  }
+  return 0;
+}
+
+}  // namespace hp

@@ -1,0 +1,62 @@
+"""CPU tests of the engine's HOST logic (batching, deferred applies, fold
+elision, descriptor splitting): the real engine.cpp/capi.cpp linked against a
+scalar host emulation of the tick descriptor (tests/emu, test-only), checked
+against the oracle exactly like the GPU parity tests. The device kernels
+themselves are covered by tests/test_gpu_parity.py on a B200."""
+import random
+
+import numpy as np
+import pytest
+
+import test_gpu_parity as G
+from oracle import run_schedule
+from workloads import C1, C1_SKEW, C2, WSPConfig
+
+
+@pytest.fixture(scope="module")
+def hp():
+    from paper_2005_14038_b200 import hetpipe
+    from emu import build_emu
+    lib = hetpipe.load_test_library(build_emu.build())
+    return G._HP(hetpipe, lib)
+
+
+@pytest.mark.parametrize("cfg", [C1, C1_SKEW], ids=["C1", "C1-skew"])
+@pytest.mark.parametrize("apply_mode", [0, 1])
+def test_c1(hp, cfg, apply_mode):
+    G.test_c1_bsp_limit_bit_exact(hp, cfg, apply_mode)
+
+
+@pytest.mark.parametrize("seed", range(160))
+def test_random_configs(hp, seed):
+    G.test_random_configs_bit_exact(hp, seed)
+
+
+def test_per_tick_states(hp):
+    G.test_per_tick_states(hp)
+
+
+def test_external_gradients(hp):
+    G.test_external_gradients_match_synthetic(hp)
+
+
+def test_protocol_errors(hp):
+    G.test_event_api_protocol_errors(hp)
+
+
+def test_zero_and_tiny(hp):
+    G.test_zero_and_tiny_sizes(hp)
+
+
+@pytest.mark.parametrize("N,Nm,D,policy", [(8, 8, 0, 0), (8, 8, 4, 1), (8, 6, 1, 0), (5, 8, 32, 1)])
+def test_descriptor_overflow(hp, N, Nm, D, policy):
+    """Ticks with many VWs, long backlogs and many deferred applies force the
+    apply-only pre-launches and split w_local groups."""
+    tau = tuple(1 + (3 * v) % 5 for v in range(N))
+    cfg = WSPConfig("ovf", N, Nm, D, 133, 12, tau, pull_policy=policy,
+                    lat=tuple(t * Nm for t in tau))
+    o = run_schedule(cfg)
+    for apply_mode in (0, 1):
+        for slots in (2, 8):
+            trace, wg, wl, _, _ = G.run_device(hp, cfg, apply_mode, slots)
+            G.assert_same(o, trace, wg, wl)

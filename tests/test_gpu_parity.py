@@ -17,6 +17,21 @@ from workloads import (C1, C1_SKEW, C2, C3, C4, C5, GRAD_DYADIC, GRAD_EXTERNAL,
 pytestmark = pytest.mark.gpu
 
 
+class _HP:
+    """The binding plus the library build under test (real CUDA library here;
+    tests/test_engine_emu.py reuses these cases with the host emulation)."""
+
+    def __init__(self, hetpipe, lib=None):
+        self._m = hetpipe
+        self.lib = lib
+
+    def __getattr__(self, k):
+        return getattr(self._m, k)
+
+    def Context(self, cfg):
+        return self._m.Context(cfg, lib=self.lib)
+
+
 @pytest.fixture(scope="module")
 def hp():
     import torch
@@ -24,7 +39,7 @@ def hp():
         pytest.skip("needs a GPU")
     from paper_2005_14038_b200 import build, hetpipe
     build.build()
-    return hetpipe
+    return _HP(hetpipe)
 
 
 def run_device(hp, cfg, apply_mode=0, acc_slots=2, **over):
