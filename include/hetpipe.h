@@ -83,12 +83,14 @@ typedef struct {
   int32_t local_semantics; /* HP_LOCAL_* (Z3) */
   int32_t apply_mode;      /* HP_APPLY_* (Z4): defer applies to the observing pull */
   int32_t acc_slots;       /* acc ring depth R per VW, 2..8 (default 2) */
+  int32_t merge_ticks;     /* 1 (default): ops of consecutive ticks on disjoint VW
+                              state may share one launch; 0: one launch per tick */
   int32_t device;          /* CUDA device ordinal */
   void* stream;            /* cudaStream_t to run on; NULL = library-owned stream */
 } hp_config;
 
 /* Fill cfg with defaults (N=1, Nm=1, D=0, lr=0.01, FLOAT grads, PHILOX w0,
-   EAGER, STRICT, deferred applies, R=2, device 0, library stream). */
+   EAGER, STRICT, deferred applies, R=2, merged ticks, device 0, library stream). */
 void hp_config_default(hp_config* cfg);
 
 /* north_star entry point: hp_init(num_vw, Nm, D, nparams, lr) with the other
@@ -131,9 +133,13 @@ hp_status hp_clock(hp_ctx* ctx, int32_t vw, int64_t* c_local, int64_t* c_global)
    minibatches that completed while it waited (Z17). Never waits inside. */
 hp_status hp_pull(hp_ctx* ctx, int32_t vw);
 
-/* End of a tick: launch the fused kernel for the ops issued since the last tick
-   (one launch per tick, Z5 phase order) and emit the tick's START records. */
+/* End of a tick: emit the tick's START records (Z5 phase order). Its device ops
+   are launched now (merge_ticks = 0) or merged with the next ticks' ops on
+   disjoint VW state and launched at the latest by hp_flush / hp_sync /
+   hp_read_weights / the return of hp_schedule_advance. */
 hp_status hp_tick_end(hp_ctx* ctx);
+/* Launch every pending fused op batch (asynchronous; no stream sync). */
+hp_status hp_flush(hp_ctx* ctx);
 
 /* Stamp subsequent trace records with tick t (wait accounting uses it). */
 hp_status hp_set_tick(hp_ctx* ctx, int64_t t);

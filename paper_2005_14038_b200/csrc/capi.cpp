@@ -46,7 +46,7 @@ class Controller {
       if (events_.empty()) return e_->fail(HP_ERR_STATE, "deadlock: no pending completion");
       if (hp_status st = tick()) return st;
     }
-    return HP_OK;
+    return e_->flush_pending();   // everything committed so far is enqueued
   }
   void set_host_grads(const float* const* bufs, int n) { host_.assign(bufs, bufs + n); }
 
@@ -150,6 +150,7 @@ void hp_config_default(hp_config* c) {
   c->local_semantics = HP_LOCAL_STRICT;
   c->apply_mode = HP_APPLY_DEFERRED;
   c->acc_slots = 2;
+  c->merge_ticks = 1;
   c->device = 0;
   c->stream = nullptr;
 }
@@ -173,6 +174,7 @@ hp_status hp_init_ex(hp_ctx** out, const hp_config* cfg_in) {
   else if (cfg.pull_policy < 0 || cfg.pull_policy > 1) bad = "bad pull_policy";
   else if (cfg.local_semantics < 0 || cfg.local_semantics > 1) bad = "bad local_semantics";
   else if (cfg.apply_mode < 0 || cfg.apply_mode > 1) bad = "bad apply_mode";
+  else if (cfg.merge_ticks < 0 || cfg.merge_ticks > 1) bad = "bad merge_ticks";
   if (bad) {
     g_init_error = bad;
     return HP_ERR_INVALID;
@@ -244,6 +246,12 @@ hp_status hp_pull(hp_ctx* ctx, int32_t vw) {
 hp_status hp_tick_end(hp_ctx* ctx) {
   HP_ENTRY(ctx)
   return ctx->eng->tick_end(nullptr);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_flush(hp_ctx* ctx) {
+  HP_ENTRY(ctx)
+  return ctx->eng->flush_pending();
   HP_EXIT(ctx)
 }
 

@@ -292,7 +292,11 @@ hp_status Engine::tick_end(std::vector<std::pair<int, int64_t>>* ungated) {
   }
   ungated_.clear();
   ticks++;
-  return flush();
+  // Independent ops of consecutive ticks (disjoint VW state) may share a launch:
+  // the batch is flushed by the first op that would conflict (complete.. checks)
+  // or by the controller before it returns, so every buffer still passes through
+  // exactly the states of the tick model.
+  return cfg_.merge_ticks ? HP_OK : flush();
 }
 
 // ---------------------------------------------------------------------------
@@ -371,6 +375,17 @@ hp_status Engine::flush() {
     if (jj < 0 || jj >= next_j) break;
     next_j = jj;
     --reg_from;
+  }
+  // A memory-sourced apply must not read an acc slot this batch writes (phase A
+  // runs before phase B): then the completes go out in a launch of their own.
+  bool split = false;
+  for (size_t k = 0; k < reg_from; ++k)
+    for (int j = 0; j < d.nc; ++j)
+      split |= bc_[j].v == ba_[k].v && bc_[j].wave_end && wave_of(bc_[j].p, Nm_) == ba_[k].c;
+  if (split) {
+    if (hp_status st = emit(d)) return st;   // completes only: acc stored, no folds
+    d.nc = 0;
+    reg_from = ba_.size();
   }
   for (size_t k = reg_from; k < ba_.size(); ++k) {
     for (int j = 0; j < d.nc; ++j) {

@@ -51,6 +51,7 @@ class Engine {
   hp_status admit(int v, std::vector<int64_t>* started);
   hp_status tick_end(std::vector<std::pair<int, int64_t>>* ungated);
   hp_status flush_applies();
+  hp_status flush_pending() { return bc_.empty() && ba_.empty() && bpull_.empty() && !has_due_folds() ? HP_OK : flush(); }
   hp_status sync();
   hp_status read(int which, int64_t off, int64_t cnt, float* dst);
 
@@ -92,6 +93,11 @@ class Engine {
   void rec(char phase, int v, const char* kind, int64_t p, int64_t c);
   std::pair<bool, bool> gate_open(int v) const;
   const float* fold_grad(int v, int64_t p) const;
+  bool has_due_folds() const {
+    for (const auto& s : vw_)
+      if (!s.pending_folds.empty() && !(cfg_.local_semantics == HP_LOCAL_STRICT && s.at_gate)) return true;
+    return false;
+  }
 
   hp_config cfg_;
   int N_, Nm_, R_;

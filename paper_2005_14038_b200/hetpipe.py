@@ -30,7 +30,7 @@ class hp_config(C.Structure):
                 ("grad_mode", C.c_int32), ("w0_mode", C.c_int32),
                 ("pull_policy", C.c_int32), ("local_semantics", C.c_int32),
                 ("apply_mode", C.c_int32), ("acc_slots", C.c_int32),
-                ("device", C.c_int32), ("stream", C.c_void_p)]
+                ("merge_ticks", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p)]
 
 
 class hp_stats(C.Structure):
@@ -59,6 +59,7 @@ EXPORTS = {
     "hp_clock": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "hp_pull": (C.c_int, [C.c_void_p, C.c_int32]),
     "hp_tick_end": (C.c_int, [C.c_void_p]),
+    "hp_flush": (C.c_int, [C.c_void_p]),
     "hp_set_tick": (C.c_int, [C.c_void_p, C.c_int64]),
     "hp_schedule_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "hp_schedule_advance": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
@@ -174,6 +175,9 @@ class Context:
 
     def tick_end(self) -> int:
         return self._chk(self.lib.hp_tick_end(self.h))
+
+    def flush(self) -> int:
+        return self._chk(self.lib.hp_flush(self.h))
 
     def set_tick(self, t: int) -> int:
         return self._chk(self.lib.hp_set_tick(self.h, t))

@@ -40,6 +40,19 @@ def test_external_gradients(hp):
     G.test_external_gradients_match_synthetic(hp)
 
 
+@pytest.mark.parametrize("seed", range(40))
+def test_event_api_replay(hp, seed):
+    G.test_event_api_replay(hp, seed % 12) if seed < 12 else _replay_more(hp, seed)
+
+
+def _replay_more(hp, seed):
+    cfg = G._rand_cfg(900 + seed)
+    o, trace, wg, wl = G.replay_events(hp, cfg, shuffle_seed=seed, merge=seed % 2)
+    assert np.array_equal(wg, o.wg)
+    for v in range(cfg.num_vw):
+        assert np.array_equal(wl[v], o.wl[v])
+
+
 def test_protocol_errors(hp):
     G.test_event_api_protocol_errors(hp)
 
@@ -58,5 +71,18 @@ def test_descriptor_overflow(hp, N, Nm, D, policy):
     o = run_schedule(cfg)
     for apply_mode in (0, 1):
         for slots in (2, 8):
-            trace, wg, wl, _, _ = G.run_device(hp, cfg, apply_mode, slots)
-            G.assert_same(o, trace, wg, wl)
+            for merge in (0, 1):
+                trace, wg, wl, _, _ = G.run_device(hp, cfg, apply_mode, slots, merge_ticks=merge)
+                G.assert_same(o, trace, wg, wl)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_same_tick_pushes_out_of_complete_order(hp, seed):
+    """C1 (equal speeds, N_m=1): both VWs push in every tick; shuffled complete
+    order makes commit order differ from complete order, which must split the
+    launch so no apply reads an acc slot before this tick writes it."""
+    for cfg in (C1, C1.replace(momentum=0.5, grad_mode=0, lr=0.01, w0_mode=1)):
+        o, trace, wg, wl = G.replay_events(hp, cfg, shuffle_seed=seed, merge=seed % 2)
+        assert np.array_equal(wg, o.wg)
+        for v in range(cfg.num_vw):
+            assert np.array_equal(wl[v], o.wl[v])

@@ -98,7 +98,8 @@ def test_random_configs_bit_exact(hp, seed):
     o = run_schedule(cfg)
     rng = random.Random(1000 + seed)
     trace, wg, wl, m, _ = run_device(hp, cfg, apply_mode=rng.randint(0, 1),
-                                     acc_slots=rng.choice([2, 3, 8]))
+                                     acc_slots=rng.choice([2, 3, 8]),
+                                     merge_ticks=rng.randint(0, 1))
     assert_same(o, trace, wg, wl)
     if cfg.momentum:
         assert np.array_equal(m, o.m)
@@ -156,6 +157,57 @@ def test_external_gradients_match_synthetic(hp):
     for v in range(cfg.num_vw):
         assert np.array_equal(ctx.read_weights(v), o.wl[v])
     ctx.close()
+
+
+def replay_events(hp, cfg, shuffle_seed=None, merge=1):
+    """Drive the event-granular ABI (hp_set_tick, hp_accumulate_minibatch,
+    hp_push_wave, hp_pull, hp_tick_end) through the oracle's own event order;
+    optionally shuffle the COMPLETE order inside each tick (phase order and
+    commit order are what the protocol fixes, not the VW order of completes)."""
+    o = run_schedule(cfg)
+    ctx = hp.Context(hp.config_from(cfg, merge_ticks=merge))
+    rng = random.Random(shuffle_seed)
+    by_tick = {}
+    for ln in o.trace:
+        f = ln.split()
+        by_tick.setdefault(int(f[0]), []).append((f[1], int(f[2]), f[3], int(f[4]), int(f[5])))
+    for t in sorted(by_tick):
+        if t == 0 and all(k == "START" for _, _, k, _, _ in by_tick[t]):
+            continue
+        ctx.set_tick(t)
+        ev = by_tick[t]
+        comps = [(v, p) for ph, v, k, p, c in ev if k == "COMPLETE"]
+        if shuffle_seed is not None:
+            rng.shuffle(comps)
+        for v, p in comps:
+            ctx.accumulate_minibatch(v, p)
+        for ph, v, k, p, c in ev:
+            if k == "PUSH":
+                ctx.push_wave(v, c)
+        for v in range(cfg.num_vw):
+            try:
+                ctx.pull(v)
+            except hp.HetPipeError as e:
+                assert e.status == hp.HP_ERR_PROTOCOL      # not waiting at its gate
+        ctx.tick_end()
+    ctx.flush()
+    with tempfile.NamedTemporaryFile(suffix=".trace") as f:
+        trace = ctx.trace_lines(f.name)
+    wg = ctx.read_weights(-1)
+    wl = [ctx.read_weights(v) for v in range(cfg.num_vw)]
+    ctx.close()
+    return o, trace, wg, wl
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_event_api_replay(hp, seed):
+    cfg = _rand_cfg(500 + seed).replace(local_semantics=LOCAL_STRICT, momentum=0.0)
+    o, trace, wg, wl = replay_events(hp, cfg, merge=seed % 2)
+    assert_same(o, trace, wg, wl)
+    o, trace, wg, wl = replay_events(hp, cfg, shuffle_seed=seed, merge=seed % 2)
+    assert np.array_equal(wg, o.wg)
+    for v in range(cfg.num_vw):
+        assert np.array_equal(wl[v], o.wl[v])
 
 
 def test_event_api_protocol_errors(hp):
