@@ -182,6 +182,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-params", type=int, default=1 << 18)
+    ap.add_argument("--merge-ticks", type=int, default=1)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -214,7 +215,7 @@ def main():
     torch.cuda.set_stream(stream)              # and the timing events below record on it
     ctx = hetpipe.Context(hetpipe.config_from(
         run_cfg, param_begin=lo, param_count=hi - lo, device=local,
-        stream=stream.cuda_stream))
+        stream=stream.cuda_stream, merge_ticks=args.merge_ticks))
     ctx.trace_enable(False)
     ctx.schedule_begin(run_cfg.tau, run_cfg.latency())
     sampler = ClockSampler(local)
@@ -238,7 +239,8 @@ def main():
     l_ms, l_bytes, l_shape = ctx.profile_launches()
     mix = {}
     for t_ms, by, sh in zip(l_ms, l_bytes, l_shape):
-        key = f"c{sh & 255}a{(sh >> 8) & 255}g{(sh >> 16) & 255}f{(sh >> 24) & 255}"
+        key = (f"c{sh & 15}i{(sh >> 4) & 15}a{(sh >> 8) & 255}g{(sh >> 16) & 255}"
+               f"f{(sh >> 24) & 255}")
         e = mix.setdefault(key, [0, 0.0, 0.0])
         e[0] += 1
         e[1] += float(t_ms)

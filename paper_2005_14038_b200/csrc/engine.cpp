@@ -337,7 +337,9 @@ hp_status Engine::emit(TickDesc& d) {
     prof_bytes_ += bytes;
     prof_launches_++;
     prof_launch_bytes_.push_back(bytes);
-    prof_launch_shape_.push_back(d.nc | (d.na << 8) | (d.ng << 16) | (d.nf << 24));
+    int inl = 0;
+    for (int j = 0; j < d.nc; ++j) inl += (d.c[j].flags & kFoldInline) ? 1 : 0;
+    prof_launch_shape_.push_back(d.nc | (inl << 4) | (d.na << 8) | (d.ng << 16) | (d.nf << 24));
   }
   launches_++;
   alg_bytes_ += bytes;
