@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-from workloads import CONFIGS, GRAD_EXTERNAL, even_shards  # noqa: E402
+from workloads import CONFIGS, GRAD_EXTERNAL  # noqa: E402
 
 METRIC = "synced params/sec"
 UNIT = "params/s"
@@ -193,7 +193,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2005_14038_b200 import hetpipe
+    from paper_2005_14038_b200 import dist as hdist
 
     ws, rank, local = _dist()
     if ws != args.gpus and "WORLD_SIZE" in os.environ:
@@ -206,16 +206,14 @@ def main():
         if ws > 1:
             dist.barrier()
 
-    b = even_shards(cfg.nparams, ws)
-    lo, hi = b[rank], b[rank + 1]
+    lo, hi = hdist.shard_bounds(cfg.nparams, ws, rank)
     N = cfg.num_vw
     waves = args.warmup + args.steps + 2
     run_cfg = cfg.replace(waves=waves)
     stream = torch.cuda.Stream(local)          # a real stream: the library launches on it
     torch.cuda.set_stream(stream)              # and the timing events below record on it
-    ctx = hetpipe.Context(hetpipe.config_from(
-        run_cfg, param_begin=lo, param_count=hi - lo, device=local,
-        stream=stream.cuda_stream, merge_ticks=args.merge_ticks))
+    ctx = hdist.rank_context(run_cfg, rank, ws, device=local, stream=stream.cuda_stream,
+                             merge_ticks=args.merge_ticks)
     ctx.trace_enable(False)
     ctx.schedule_begin(run_cfg.tau, run_cfg.latency())
     sampler = ClockSampler(local)
@@ -271,9 +269,8 @@ def main():
         for h in host:
             h.numpy()[:] = (rng.random(nloc, dtype=np.float32) - np.float32(0.5))
         out = torch.empty(nloc, dtype=torch.float32, pin_memory=True)
-        ectx = hetpipe.Context(hetpipe.config_from(
-            ecfg, param_begin=lo, param_count=nloc, device=local, grad_mode=GRAD_EXTERNAL,
-            stream=stream.cuda_stream))
+        ectx = hdist.rank_context(ecfg, rank, ws, device=local, stream=stream.cuda_stream,
+                                  grad_mode=GRAD_EXTERNAL)
         ectx.trace_enable(False)
         ectx.schedule_set_host_grads([h.numpy() for h in host])
         ectx.schedule_begin(ecfg.tau, ecfg.latency())

@@ -246,10 +246,11 @@ int launch_u(const TickDesc& d, cudaStream_t s) {
 
 template <int GM, bool MOM>
 int launch_gm(const TickDesc& d, cudaStream_t s) {
-  // Thin ticks (few buffer passes) need more chunks in flight per thread.
-  int u = tick_streams(d) <= 3 ? 8 : 4;
+  // Measured on B200 (profiles/): complete-only launches run best with 4 chunks
+  // per thread; launches with pull groups (more ops per chunk, more Philox
+  // folds) with 2, which keeps 3 CTAs/SM resident.
+  int u = d.ng > 0 ? 2 : 4;
   if (g_u_override > 0) u = g_u_override;
-  if (u >= 8) return launch_u<GM, MOM, 8>(d, s);
   if (u >= 4) return launch_u<GM, MOM, 4>(d, s);
   return launch_u<GM, MOM, 2>(d, s);
 }
