@@ -183,6 +183,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-params", type=int, default=1 << 18)
     ap.add_argument("--merge-ticks", type=int, default=1)
+    ap.add_argument("--span", type=int, default=0,
+                    help="N>1: GPUs per VW of the distributed placement (k<N exchanges over "
+                         "NVLink); 0 = ED-local shards (no exchange)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -212,8 +215,13 @@ def main():
     run_cfg = cfg.replace(waves=waves)
     stream = torch.cuda.Stream(local)          # a real stream: the library launches on it
     torch.cuda.set_stream(stream)              # and the timing events below record on it
-    ctx = hdist.rank_context(run_cfg, rank, ws, device=local, stream=stream.cuda_stream,
-                             merge_ticks=args.merge_ticks)
+    placed = ws > 1 and args.span > 0
+    if placed:
+        ctx = hdist.placed_context(run_cfg, rank, ws, args.span, device=local,
+                                   stream=stream.cuda_stream, merge_ticks=args.merge_ticks)
+    else:
+        ctx = hdist.rank_context(run_cfg, rank, ws, device=local, stream=stream.cuda_stream,
+                                 merge_ticks=args.merge_ticks)
     ctx.trace_enable(False)
     ctx.schedule_begin(run_cfg.tau, run_cfg.latency())
     sampler = ClockSampler(local)
@@ -253,6 +261,10 @@ def main():
     ms_max = float(t.item())
     value = commits * cfg.nparams / (ms_max / 1e3)
     launches = st1.launches - st0.launches
+    nvl = torch.tensor([st1.nvl_bytes - st0.nvl_bytes], dtype=torch.float64, device=f"cuda:{local}")
+    if ws > 1:
+        dist.all_reduce(nvl, op=dist.ReduceOp.MAX)
+    nvl_bytes_max = float(nvl.item())
     sync_waits = [int(x) for x in st1.wait_ticks[:N]]
     ctx.close()
     del ctx
@@ -260,7 +272,7 @@ def main():
 
     # ---------------- e2e: host gradients in, w_global out, through the C-ABI
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not placed:
         e_steps = max(1, args.e2e_steps)
         ecfg = cfg.replace(waves=3 + e_steps + 1)
         nloc = hi - lo
@@ -313,7 +325,8 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "num_vw": N, "Nm": cfg.Nm, "D": cfg.D,
                    "nparams": cfg.nparams, "tau": list(cfg.tau), "placement":
-                   "ED-local shards" if ws > 1 else "single GPU",
+                   (f"distributed, {args.span} GPU(s) per VW, PS sharded over {ws}" if placed
+                    else "ED-local shards" if ws > 1 else "single GPU"),
                    "grad": "Philox FLOAT in-kernel", "pull": "EAGER", "local": "STRICT",
                    "l2": "inputs larger than L2 (>= 13 x 230 MiB buffers per GPU)"},
         "images_per_sec_equiv": commits * 32 * cfg.Nm / (ms_max / 1e3),
@@ -322,6 +335,9 @@ def main():
                      "peak_kind": peak_kind, "kernel": "hp::tick_kernel (all launches)",
                      "kernel_ms": kern_ms, "launches": kern_launches,
                      "alg_bytes_per_launch": kern_bytes / max(kern_launches, 1)},
+        "nvlink": {"bytes_per_step_max_rank": nvl_bytes_max / args.steps,
+                   "GBps_over_step": nvl_bytes_max / (ms_max / 1e3) / 1e9,
+                   "peak_GBps": 770.0, "peak_kind": "guide-measured peer copy per direction"},
         "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
         "launch_mix": launch_mix,
         "gpu_launches": launches,

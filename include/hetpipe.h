@@ -85,6 +85,12 @@ typedef struct {
   int32_t acc_slots;       /* acc ring depth R per VW, 2..8 (default 2) */
   int32_t merge_ticks;     /* 1 (default): ops of consecutive ticks on disjoint VW
                               state may share one launch; 0: one launch per tick */
+  int32_t world;           /* G ranks (one process per GPU); 1 = single context */
+  int32_t rank;            /* this rank, 0..G-1 */
+  int32_t vw_span;         /* k GPUs per VW (1..G): VW v's stage j (even split of P
+                              over k) lives on GPU (v*k+j) mod G; PS shard q (even
+                              split over G) on GPU q. k = G is ED-local (P:104-106,
+                              no exchange); k < G exchanges over NVLink. */
   int32_t device;          /* CUDA device ordinal */
   void* stream;            /* cudaStream_t to run on; NULL = library-owned stream */
 } hp_config;
@@ -92,6 +98,19 @@ typedef struct {
 /* Fill cfg with defaults (N=1, Nm=1, D=0, lr=0.01, FLOAT grads, PHILOX w0,
    EAGER, STRICT, deferred applies, R=2, merged ticks, device 0, library stream). */
 void hp_config_default(hp_config* cfg);
+
+/* Distributed placements (world > 1), set up collectively on every rank:
+   rank 0 calls hp_comm_unique_id and broadcasts the 128 bytes; every rank
+   calls hp_init_ex, hp_ipc_handle (64 bytes, all-gathered by the caller), then
+   hp_connect(handles = world*64 bytes in rank order, comm_id). After that the
+   ranks must issue the same protocol calls in the same order (the replicated
+   controller does); pushes are applied by each PS shard owner reading the
+   pushed u~ slices from the GPU that holds them, and pulls read w_global
+   shards from their owners -- NVLink loads inside the tick kernels, ordered by
+   a stream-ordered barrier (a 4-byte NCCL all-reduce). */
+hp_status hp_comm_unique_id(void* out128);
+hp_status hp_ipc_handle(hp_ctx* ctx, void* out64);
+hp_status hp_connect(hp_ctx* ctx, const void* handles, const void* comm_id);
 
 /* north_star entry point: hp_init(num_vw, Nm, D, nparams, lr) with the other
    fields at their defaults. Allocates ~ (N*(1+R) + 1 (+1 momentum)) * 4 * P
@@ -162,8 +181,9 @@ hp_status hp_schedule_set_host_grads(hp_ctx* ctx, const float* const* host_bufs,
 hp_status hp_sync(hp_ctx* ctx);
 
 /* Copy count fp32 of a buffer, from local offset `offset`, to host memory.
-   which = -1: w_global (pending applies are flushed first); -2: momentum m;
-   0..N-1: w_local(which) as its next START will read it (while that VW waits at
+   which = -1: w_global (pending applies are flushed first); -2: momentum m
+   (this rank's PS shard when world > 1); 0..N-1: this rank's stage of
+   w_local(which) as its next START will read it (while that VW waits at
    its gate, STRICT folds deferred to admission are not yet in it). Blocking. */
 hp_status hp_read_weights(hp_ctx* ctx, int32_t which, int64_t offset, int64_t count,
                           float* host_dst);
@@ -181,6 +201,7 @@ typedef struct {
   double alg_bytes;         /* algorithmic HBM bytes of all launches */
   int64_t wait_ticks[8];    /* per VW simulated wait */
   int64_t pulls[8];         /* per VW pulls */
+  double nvl_bytes;         /* bytes this rank's kernels read from peer GPUs */
 } hp_stats;
 hp_status hp_get_stats(hp_ctx* ctx, hp_stats* out);
 

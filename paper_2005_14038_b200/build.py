@@ -11,8 +11,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhetpipe.so")
-SOURCES = ["kernels.cu", "engine.cpp", "capi.cpp"]
-HEADERS = ["tick_desc.h", "engine.h", os.path.join("..", "..", "include", "hetpipe.h")]
+SOURCES = ["kernels.cu", "engine.cpp", "capi.cpp", "comm_nccl.cpp"]
+HEADERS = ["tick_desc.h", "engine.h", "comm.h", os.path.join("..", "..", "include", "hetpipe.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc, *NVCC_FLAGS, "-shared", "-o", LIB + ".tmp",
-           *[os.path.join(CSRC, s) for s in SOURCES]]
+           *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -151,6 +151,9 @@ void hp_config_default(hp_config* c) {
   c->apply_mode = HP_APPLY_DEFERRED;
   c->acc_slots = 2;
   c->merge_ticks = 1;
+  c->world = 1;
+  c->rank = 0;
+  c->vw_span = 1;
   c->device = 0;
   c->stream = nullptr;
 }
@@ -175,6 +178,11 @@ hp_status hp_init_ex(hp_ctx** out, const hp_config* cfg_in) {
   else if (cfg.local_semantics < 0 || cfg.local_semantics > 1) bad = "bad local_semantics";
   else if (cfg.apply_mode < 0 || cfg.apply_mode > 1) bad = "bad apply_mode";
   else if (cfg.merge_ticks < 0 || cfg.merge_ticks > 1) bad = "bad merge_ticks";
+  else if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world) bad = "bad world/rank";
+  else if (cfg.world > 1 && (cfg.vw_span < 1 || cfg.vw_span > cfg.world)) bad = "vw_span must be 1..world";
+  else if (cfg.world > 1 && (cfg.param_begin != 0 || cfg.param_count != cfg.nparams))
+    bad = "world > 1 places the whole model: param_begin 0, param_count -1";
+  else if (cfg.world > 1 && cfg.grad_mode == HP_GRAD_EXTERNAL) bad = "EXTERNAL gradients need world 1";
   if (bad) {
     g_init_error = bad;
     return HP_ERR_INVALID;
@@ -252,6 +260,30 @@ hp_status hp_tick_end(hp_ctx* ctx) {
 hp_status hp_flush(hp_ctx* ctx) {
   HP_ENTRY(ctx)
   return ctx->eng->flush_pending();
+  HP_EXIT(ctx)
+}
+
+hp_status hp_comm_unique_id(void* out) {
+  if (!out) return HP_ERR_INVALID;
+  std::string err;
+  if (hp::comm_unique_id(out, &err)) {
+    g_init_error = err;
+    return HP_ERR_COMM;
+  }
+  return HP_OK;
+}
+
+hp_status hp_ipc_handle(hp_ctx* ctx, void* out) {
+  HP_ENTRY(ctx)
+  if (!out) return ctx->eng->fail(HP_ERR_INVALID, "out is NULL");
+  return ctx->eng->ipc_handle(out);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_connect(hp_ctx* ctx, const void* handles, const void* comm_id) {
+  HP_ENTRY(ctx)
+  if (!handles || !comm_id) return ctx->eng->fail(HP_ERR_INVALID, "NULL handles or id");
+  return ctx->eng->connect(handles, comm_id);
   HP_EXIT(ctx)
 }
 

@@ -1,0 +1,121 @@
+// comm_nccl.cpp -- Comm over NCCL (dlopen'd; the process's own libnccl.so.2,
+// e.g. the one torch loaded, is reused). Only a 4-byte all-reduce is issued:
+// it completes on a rank only after every rank's stream reached it, which is
+// the device-side barrier the distributed flush needs.
+#include <dlfcn.h>
+
+#include <cstring>
+#include <string>
+
+#include "comm.h"
+
+namespace hp {
+namespace {
+
+typedef int ncclResult_t;
+typedef struct ncclComm* ncclComm_t;
+struct ncclUniqueId {
+  char internal[kCommIdBytes];
+};
+enum { ncclInt32 = 2, ncclSum = 0 };
+
+struct Api {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Api* api(std::string* err) {
+  static Api a;
+  static bool tried = false;
+  if (tried) {
+    if (!a.h && err) *err = "libnccl.so.2 not loadable";
+    return a.h ? &a : nullptr;
+  }
+  tried = true;
+  const char* names[] = {
+      "libnccl.so.2",
+      "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
+      "/usr/lib/x86_64-linux-gnu/libnccl.so.2"};
+  for (const char* n : names) {
+    a.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (a.h) break;
+  }
+  if (!a.h) {
+    if (err) *err = "libnccl.so.2 not loadable";
+    return nullptr;
+  }
+  a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(a.h, "ncclGetUniqueId");
+  a.CommInitRank = (decltype(a.CommInitRank))dlsym(a.h, "ncclCommInitRank");
+  a.AllReduce = (decltype(a.AllReduce))dlsym(a.h, "ncclAllReduce");
+  a.CommDestroy = (decltype(a.CommDestroy))dlsym(a.h, "ncclCommDestroy");
+  a.GetErrorString = (decltype(a.GetErrorString))dlsym(a.h, "ncclGetErrorString");
+  if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.CommDestroy) {
+    a.h = nullptr;
+    if (err) *err = "libnccl.so.2 lacks required symbols";
+    return nullptr;
+  }
+  return &a;
+}
+
+class NcclComm : public Comm {
+ public:
+  NcclComm(Api* a, ncclComm_t c, int* scratch) : a_(a), c_(c), scratch_(scratch) {}
+  ~NcclComm() override {
+    if (c_) a_->CommDestroy(c_);
+    if (scratch_) cudaFree(scratch_);
+  }
+  int barrier(cudaStream_t s) override {
+    ncclResult_t r = a_->AllReduce(scratch_, scratch_ + 1, 1, ncclInt32, ncclSum, c_, s);
+    if (r != 0) err_ = a_->GetErrorString ? a_->GetErrorString(r) : "ncclAllReduce failed";
+    return r;
+  }
+  std::string error() const override { return err_; }
+
+ private:
+  Api* a_;
+  ncclComm_t c_;
+  int* scratch_;
+  std::string err_;
+};
+
+}  // namespace
+
+int comm_unique_id(void* out, std::string* err) {
+  Api* a = api(err);
+  if (!a) return -1;
+  ncclUniqueId id;
+  ncclResult_t r = a->GetUniqueId(&id);
+  if (r != 0) {
+    if (err) *err = "ncclGetUniqueId failed";
+    return r;
+  }
+  memcpy(out, id.internal, kCommIdBytes);
+  return 0;
+}
+
+Comm* comm_create(const void* id, int world, int rank, std::string* err) {
+  Api* a = api(err);
+  if (!a) return nullptr;
+  ncclUniqueId uid;
+  memcpy(uid.internal, id, kCommIdBytes);
+  ncclComm_t c = nullptr;
+  ncclResult_t r = a->CommInitRank(&c, world, uid, rank);
+  if (r != 0) {
+    if (err) *err = std::string("ncclCommInitRank: ") + (a->GetErrorString ? a->GetErrorString(r) : "");
+    return nullptr;
+  }
+  int* scratch = nullptr;
+  if (cudaMalloc(&scratch, 2 * sizeof(int)) != cudaSuccess) {
+    a->CommDestroy(c);
+    if (err) *err = "barrier scratch allocation failed";
+    return nullptr;
+  }
+  cudaMemset(scratch, 0, 2 * sizeof(int));
+  return new NcclComm(a, c, scratch);
+}
+
+}  // namespace hp

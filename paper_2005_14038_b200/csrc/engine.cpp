@@ -21,9 +21,66 @@ Engine::Engine(const hp_config& cfg) : cfg_(cfg) {
   begin_ = cfg.param_begin;
   n_ = cfg.param_count;
   vw_.resize(N_);
+  G_ = cfg.world;
+  rank_ = cfg.rank;
+  span_ = cfg.vw_span;
+  dist_ = G_ > 1;
+}
+
+namespace {
+// even contiguous split of [0, P) into n parts, inner boundaries multiples of 32
+// floats, the last part takes the remainder (reading Z12)
+std::vector<int64_t> even_bounds(int64_t P, int n) {
+  const int64_t per = (P / n) / 32 * 32;
+  std::vector<int64_t> b(n + 1);
+  for (int i = 0; i < n; ++i) b[i] = per * i;
+  b[n] = P;
+  return b;
+}
+size_t align256(int64_t nfloat) { return ((size_t)std::max<int64_t>(nfloat, 1) * 4 + 255) / 256 * 256; }
+}  // namespace
+
+// Placement (world G, span k): PS shard q = even_bounds(P, G)[q..q+1] on GPU q;
+// VW v's stage j = even_bounds(P, k)[j..j+1] on GPU (v*k + j) mod G. k = G is the
+// paper's ED-local placement (stage q = shard q); k = 1 a full
+// replica per VW (one VW per GPU as in C5, or several).
+RankLayout Engine::layout_of(int q) const {
+  RankLayout L;
+  L.s0 = shard_b_[q];
+  L.s1 = shard_b_[q + 1];
+  L.a.assign(N_, 0);
+  L.len.assign(N_, 0);
+  L.has.assign(N_, 0);
+  L.wl_off.assign(N_, 0);
+  L.acc_off.assign(N_, std::vector<size_t>(R_, 0));
+  size_t off = 0;
+  L.wg_off = off;
+  off += align256(L.s1 - L.s0);
+  if (cfg_.momentum != 0.f) {
+    L.m_off = off;
+    off += align256(L.s1 - L.s0);
+  }
+  for (int v = 0; v < N_; ++v) {
+    for (int j = 0; j < span_; ++j) {
+      if ((v * span_ + j) % G_ != q) continue;
+      L.a[v] = stage_b_[j];
+      L.len[v] = stage_b_[j + 1] - stage_b_[j];
+      L.has[v] = 1;
+      L.wl_off[v] = off;
+      off += align256(L.len[v]);
+      for (int r = 0; r < R_; ++r) {
+        L.acc_off[v][r] = off;
+        off += align256(L.len[v]);
+      }
+    }
+  }
+  L.bytes = off;
+  return L;
 }
 
 Engine::~Engine() {
+  delete comm_;
+  for (void* p : opened_) cudaIpcCloseMemHandle(p);
   for (auto e : ev_) cudaEventDestroy(e);
   if (arena_) cudaFree(arena_);
   for (auto& v : vw_)
@@ -52,29 +109,49 @@ hp_status Engine::init() {
     if (int e = cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking)) return check_cuda(e, "stream");
     own_stream_ = true;
   }
-  // arena: w_global, [m], per VW w_local + R acc slots; each 256-byte aligned
-  const size_t stride = ((size_t)std::max<int64_t>(n_, 1) * 4 + 255) / 256 * 256;
-  const size_t nbuf = 1 + (cfg_.momentum != 0.f ? 1 : 0) + (size_t)N_ * (1 + R_);
-  if (cudaMalloc(&arena_, stride * nbuf) != cudaSuccess) {
+  // arena: w_global, [m], per VW w_local + R acc slots; each 256-byte aligned.
+  // Single-rank contexts own [param_begin, +param_count) of every buffer; with
+  // world > 1 the placement layout decides (layout_of).
+  if (dist_) {
+    shard_b_ = even_bounds(cfg_.nparams, G_);
+    stage_b_ = even_bounds(cfg_.nparams, span_);
+  } else {
+    shard_b_ = {begin_, begin_ + n_};
+    stage_b_ = {begin_, begin_ + n_};
+    G_ = 1;
+    span_ = 1;
+    rank_ = 0;
+  }
+  for (int q = 0; q < G_; ++q) lay_.push_back(layout_of(q));
+  const RankLayout& L = lay_[rank_];
+  if (cudaMalloc(&arena_, L.bytes) != cudaSuccess) {
     cudaGetLastError();
     arena_ = nullptr;
     return fail(HP_ERR_OOM, "device arena allocation failed");
   }
   char* base = (char*)arena_;
-  size_t k = 0;
-  wg_ = (float*)(base + stride * k++);
-  if (cfg_.momentum != 0.f) m_ = (float*)(base + stride * k++);
-  for (auto& v : vw_) {
-    v.wl = (float*)(base + stride * k++);
-    for (int r = 0; r < R_; ++r) v.acc.push_back((float*)(base + stride * k++));
-    v.grad_of_slot.assign(Nm_, nullptr);
+  begin_ = L.s0;
+  n_ = L.s1 - L.s0;
+  wg_ = (float*)(base + L.wg_off);
+  if (cfg_.momentum != 0.f) m_ = (float*)(base + L.m_off);
+  for (int v = 0; v < N_; ++v) {
+    VW& s = vw_[v];
+    s.a0 = L.a[v];
+    s.len = L.len[v];
+    s.grad_of_slot.assign(Nm_, nullptr);
+    s.here = L.has[v] != 0;
+    if (!s.here) continue;
+    s.wl = (float*)(base + L.wl_off[v]);
+    for (int r = 0; r < R_; ++r) s.acc.push_back((float*)(base + L.acc_off[v][r]));
   }
+  peer_.assign(G_, nullptr);
+  peer_[rank_] = base;
   const uint32_t k0 = (uint32_t)(cfg_.seed & 0xffffffffu), k1 = (uint32_t)(cfg_.seed >> 32);
   hp_status st = check_cuda(
       launch_init(wg_, n_, begin_, cfg_.w0_mode, cfg_.grad_mode, k0, k1, stream_), "init");
   for (auto& v : vw_)
-    if (st == HP_OK)
-      st = check_cuda(launch_init(v.wl, n_, begin_, cfg_.w0_mode, cfg_.grad_mode, k0, k1, stream_),
+    if (st == HP_OK && v.here)
+      st = check_cuda(launch_init(v.wl, v.len, v.a0, cfg_.w0_mode, cfg_.grad_mode, k0, k1, stream_),
                       "init");
   if (st == HP_OK && m_) st = check_cuda(cudaMemsetAsync(m_, 0, (size_t)n_ * 4, stream_), "memset");
   if (st != HP_OK) return st;
@@ -123,6 +200,7 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
                            bool* wave_end_out) {
   if (sticky_) return sticky_;
   if (v < 0 || v >= N_) return fail(HP_ERR_INVALID, "vw out of range");
+  if (dist_ && !comm_) return fail(HP_ERR_STATE, "distributed context not connected (hp_connect)");
   VW& s = vw_[v];
   if (p != s.completed + 1 || p > s.started || p > last_p_)
     return fail(HP_ERR_PROTOCOL, "COMPLETE out of order or minibatch not started");
@@ -153,12 +231,12 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
       s.grad_ring.assign(Nm_, nullptr);
     }
     float*& dst = s.grad_ring[(p - 1) % Nm_];
-    if (!dst && cudaMalloc(&dst, (size_t)std::max<int64_t>(n_, 1) * 4) != cudaSuccess) {
+    if (!dst && cudaMalloc(&dst, (size_t)std::max<int64_t>(s.len, 1) * 4) != cudaSuccess) {
       cudaGetLastError();
       dst = nullptr;
       return fail(HP_ERR_OOM, "gradient staging allocation failed");
     }
-    if (hp_status st = check_cuda(cudaMemcpyAsync(dst, grad_host, (size_t)n_ * 4,
+    if (hp_status st = check_cuda(cudaMemcpyAsync(dst, grad_host, (size_t)s.len * 4,
                                                   cudaMemcpyHostToDevice, stream_), "H2D grad"))
       return st;
     g = dst;
@@ -301,10 +379,11 @@ hp_status Engine::tick_end(std::vector<std::pair<int, int64_t>>* ungated) {
 
 // ---------------------------------------------------------------------------
 // Batch -> TickDesc(s). Algorithmic bytes are counted from the descriptor: each
-// buffer read or written once per launch = 4 bytes per param.
-hp_status Engine::emit(TickDesc& d) {
-  d.n = n_;
-  d.blk_base = begin_ >> 2;
+// buffer read or written once per launch = 4 bytes per param of the launch's
+// range [begin, begin+n); reads through peer segments are also NVLink bytes.
+hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n) {
+  d.n = n;
+  d.blk_base = begin >> 2;
   d.wg = wg_;
   d.m = m_;
   d.neg_lr = -cfg_.lr;
@@ -312,13 +391,30 @@ hp_status Engine::emit(TickDesc& d) {
   d.key0 = (uint32_t)(cfg_.seed & 0xffffffffu);
   d.key1 = (uint32_t)(cfg_.seed >> 32);
   bool any_pull = false, apply_now = false;
-  for (int g = 0; g < d.ng; ++g) any_pull |= d.g[g].pull != 0;
+  for (int g = 0; g < d.ng; ++g) any_pull |= d.g[g].pull == 1;
   for (int j = 0; j < d.nc; ++j) apply_now |= (d.c[j].flags & kApplyNow) != 0;
   d.wg_store = (d.na > 0 || apply_now) ? 1 : 0;
   d.wg_load = (d.wg_store || any_pull) ? 1 : 0;
-  const int streams = tick_streams(d);
-  const double bytes = 4.0 * (double)n_ * streams;
   if (d.nc == 0 && d.na == 0 && d.ng == 0) return HP_OK;
+  const int streams = tick_streams(d);
+  const double bytes = 4.0 * (double)n * streams;
+  // remote (NVLink) reads: segments whose pointer is outside this rank's arena
+  double remote = 0;
+  const char* lo = (const char*)arena_;
+  const char* hi = lo + lay_[rank_].bytes;
+  for (int k = 0; k < d.na; ++k)
+    for (int t = d.a[k].seg_begin; t < d.a[k].seg_end; ++t) {
+      const int64_t b = t == d.a[k].seg_begin ? 0 : d.s[t - 1].end;
+      const char* p = (const char*)(d.s[t].ptr + b);
+      if (p < lo || p >= hi) remote += 4.0 * (double)(d.s[t].end - b);
+    }
+  for (int g = 0; g < d.ng; ++g)
+    if (d.g[g].pull == 2)
+      for (int t = d.g[g].seg_begin; t < d.g[g].seg_end; ++t) {
+        const int64_t b = t == d.g[g].seg_begin ? 0 : d.s[t - 1].end;
+        const char* p = (const char*)(d.s[t].ptr + b);
+        if (p < lo || p >= hi) remote += 4.0 * (double)(d.s[t].end - b);
+      }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (prof_on_) {
     while (ev_.size() < ev_used_ + 2) {
@@ -343,11 +439,54 @@ hp_status Engine::emit(TickDesc& d) {
   }
   launches_++;
   alg_bytes_ += bytes;
+  nvl_bytes_ += remote;
   return check_cuda(err, "tick kernel");
+}
+
+// Append the segments of a source covering global range [a, a+len): the acc
+// slot `slot` of VW v (acc_of_vw) or w_global, wherever (which GPU) each part
+// lives. Pointers are pre-offset so the launch's local index addresses them.
+// Returns the number of segments added, or -1 if the table is full.
+int Engine::add_segs(TickDesc& d, int64_t a, int64_t len, bool acc_of_vw, int v, int slot) {
+  const int first = d.ns;
+  for (int q = 0; q < G_; ++q) {
+    const RankLayout& L = lay_[q];
+    int64_t lo, hi;
+    size_t off;
+    if (acc_of_vw) {
+      if (!L.has[v]) continue;
+      lo = L.a[v];
+      hi = L.a[v] + L.len[v];
+      off = L.acc_off[v][slot];
+    } else {
+      lo = L.s0;
+      hi = L.s1;
+      off = L.wg_off;
+    }
+    const int64_t x0 = std::max(lo, a), x1 = std::min(hi, a + len);
+    if (x0 >= x1) continue;
+    if (d.ns == kMaxS) {
+      d.ns = first;
+      return -1;
+    }
+    // element i of the launch (global a + i) lives at buffer index a + i - lo
+    const float* base = (const float*)(peer_[q] + off);
+    d.s[d.ns].ptr = (const float*)((uintptr_t)base + (uintptr_t)((a - lo) * 4));
+    d.s[d.ns].end = x1 - a;
+    d.ns++;
+  }
+  // segments must come in increasing order of range (ranks hold increasing
+  // ranges for w_global; a VW's stages are increasing in j but not in rank)
+  std::sort(d.s + first, d.s + d.ns, [](const DSeg& x, const DSeg& y) { return x.end < y.end; });
+  return d.ns - first;
 }
 
 hp_status Engine::flush() {
   if (sticky_) return sticky_;
+  return dist_ ? flush_dist() : flush_local();
+}
+
+hp_status Engine::flush_local() {
   const bool strict = cfg_.local_semantics == HP_LOCAL_STRICT;
   TickDesc d;
   memset(&d, 0, sizeof d);
@@ -385,7 +524,7 @@ hp_status Engine::flush() {
     for (int j = 0; j < d.nc; ++j)
       split |= bc_[j].v == ba_[k].v && bc_[j].wave_end && wave_of(bc_[j].p, Nm_) == ba_[k].c;
   if (split) {
-    if (hp_status st = emit(d)) return st;   // completes only: acc stored, no folds
+    if (hp_status st = emit(d, begin_, n_)) return st;   // completes only: acc stored
     d.nc = 0;
     reg_from = ba_.size();
   }
@@ -401,11 +540,20 @@ hp_status Engine::flush() {
   while (reg_from - a0 > (size_t)kMaxA) {
     TickDesc pre;
     memset(&pre, 0, sizeof pre);
-    for (int k = 0; k < kMaxA; ++k, ++a0) pre.a[k].src = vw_[ba_[a0].v].acc[ba_[a0].slot];
+    for (int k = 0; k < kMaxA; ++k, ++a0) {
+      pre.a[k].seg_begin = pre.ns;
+      add_segs(pre, begin_, n_, true, ba_[a0].v, ba_[a0].slot);
+      pre.a[k].seg_end = pre.ns;
+    }
     pre.na = kMaxA;
-    if (hp_status st = emit(pre)) return st;
+    if (hp_status st = emit(pre, begin_, n_)) return st;
   }
-  for (size_t k = a0; k < reg_from; ++k) d.a[d.na++].src = vw_[ba_[k].v].acc[ba_[k].slot];
+  for (size_t k = a0; k < reg_from; ++k) {
+    DApply& a = d.a[d.na++];
+    a.seg_begin = d.ns;
+    add_segs(d, begin_, n_, true, ba_[k].v, ba_[k].slot);
+    a.seg_end = d.ns;
+  }
   applied_ += (int64_t)ba_.size();
   // 3. w_local: pulled VWs and VWs whose folds are due now (phase D), or the
   //    single due fold of this batch's own complete, folded inline (phase B)
@@ -429,7 +577,7 @@ hp_status Engine::flush() {
     size_t fi = 0;
     do {  // split a group whose folds overflow the descriptor
       if (d.ng == kMaxG || d.nf == kMaxF) {
-        if (hp_status st = emit(d)) return st;
+        if (hp_status st = emit(d, begin_, n_)) return st;
         memset(&d, 0, sizeof d);
       }
       DGroup& g = d.g[d.ng++];
@@ -452,7 +600,190 @@ hp_status Engine::flush() {
   ba_.clear();
   bpull_.clear();
   phase_ = kNone;
-  return emit(d);
+  return emit(d, begin_, n_);
+}
+
+// Distributed flush (world > 1). Replicated on every rank with identical
+// decisions, so every rank issues the same barriers:
+//   1. local launches, one per distinct local stage range: this rank's part of
+//      the batch's completes (acc always stored: peers read it), inline folds
+//      and fold-only groups;
+//   2. if the batch applies pushes: BARRIER (peer accs complete; earlier pulls
+//      of w_global done everywhere) -> apply launch(es) over this rank's PS
+//      shard, reading every pushed u~ slice from the GPU that holds it (NVLink
+//      loads inside the kernel, commit order) -> BARRIER (w_global final; acc
+//      slots free for reuse);
+//   3. pull launches: w_local(v) of each local stage <- w_global read from the
+//      shard owners (NVLink loads), then the VW's due folds.
+hp_status Engine::flush_dist() {
+  const bool strict = cfg_.local_semantics == HP_LOCAL_STRICT;
+  // ---- 1. local work, grouped by stage range -----------------------------
+  std::vector<std::pair<int64_t, int64_t>> ranges;
+  for (int v = 0; v < N_; ++v)
+    if (vw_[v].here && std::find(ranges.begin(), ranges.end(), std::make_pair(vw_[v].a0, vw_[v].len)) == ranges.end())
+      ranges.push_back({vw_[v].a0, vw_[v].len});
+  std::vector<std::vector<int64_t>> pull_folds(N_);
+  std::vector<bool> pulled(N_, false);
+  for (int v : bpull_) pulled[v] = true;
+  for (auto& rg : ranges) {
+    TickDesc d;
+    memset(&d, 0, sizeof d);
+    for (const BComplete& b : bc_) {
+      const VW& s = vw_[b.v];
+      if (!s.here || s.a0 != rg.first || s.len != rg.second) continue;
+      DComplete& c = d.c[d.nc++];
+      c.acc = s.acc[b.slot];
+      c.grad = nullptr;
+      c.wl = nullptr;
+      c.v = (uint32_t)b.v;
+      c.p = (uint32_t)b.p;
+      c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc;
+    }
+    for (int v = 0; v < N_; ++v) {
+      VW& s = vw_[v];
+      if (!s.here || s.a0 != rg.first || s.len != rg.second || pulled[v]) continue;
+      const bool hold = strict && s.at_gate;
+      if (hold || s.pending_folds.empty()) continue;
+      std::vector<int64_t> folds;
+      folds.swap(s.pending_folds);
+      if (folds.size() == 1) {
+        int jj = -1;
+        for (int j = 0; j < d.nc; ++j)
+          if ((int)d.c[j].v == v && (int64_t)d.c[j].p == folds[0]) jj = j;
+        if (jj >= 0) {
+          d.c[jj].flags |= kFoldInline;
+          d.c[jj].wl = s.wl;
+          continue;
+        }
+      }
+      size_t fi = 0;
+      do {
+        if (d.ng == kMaxG || d.nf == kMaxF) {
+          if (hp_status st = emit(d, rg.first, rg.second)) return st;
+          memset(&d, 0, sizeof d);
+        }
+        DGroup& g = d.g[d.ng++];
+        g.wl = s.wl;
+        g.pull = 0;
+        g.f_begin = d.nf;
+        for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
+          DFold& f = d.f[d.nf++];
+          f.v = (uint32_t)v;
+          f.p = (uint32_t)folds[fi];
+          f.grad = nullptr;
+        }
+        g.f_end = d.nf;
+      } while (fi < folds.size());
+    }
+    if (hp_status st = emit(d, rg.first, rg.second)) return st;
+  }
+  // folds of VWs without a stage here are someone else's device work
+  for (int v = 0; v < N_; ++v)
+    if (!vw_[v].here && !pulled[v] && !(strict && vw_[v].at_gate)) vw_[v].pending_folds.clear();
+  // ---- 2. applies on this rank's PS shard -------------------------------
+  if (!ba_.empty()) {
+    if (int e = comm_->barrier(stream_)) return fail(HP_ERR_COMM, comm_->error());
+    size_t k = 0;
+    while (k < ba_.size()) {
+      TickDesc d;
+      memset(&d, 0, sizeof d);
+      while (k < ba_.size() && d.na < kMaxA) {
+        const int b = d.ns;
+        if (add_segs(d, begin_, n_, true, ba_[k].v, ba_[k].slot) < 0) break;
+        d.a[d.na].seg_begin = b;
+        d.a[d.na].seg_end = d.ns;
+        d.na++;
+        ++k;
+      }
+      if (hp_status st = emit(d, begin_, n_)) return st;
+    }
+    applied_ += (int64_t)ba_.size();
+    if (int e = comm_->barrier(stream_)) return fail(HP_ERR_COMM, comm_->error());
+  }
+  // ---- 3. pulls -----------------------------------------------------------
+  for (auto& rg : ranges) {
+    TickDesc d;
+    memset(&d, 0, sizeof d);
+    for (int v : bpull_) {
+      VW& s = vw_[v];
+      if (!s.here || s.a0 != rg.first || s.len != rg.second) continue;
+      std::vector<int64_t> folds;
+      folds.swap(s.pending_folds);
+      size_t fi = 0;
+      bool first_part = true;
+      do {
+        if (d.ng == kMaxG || d.nf == kMaxF || d.ns + G_ > kMaxS) {
+          if (hp_status st = emit(d, rg.first, rg.second)) return st;
+          memset(&d, 0, sizeof d);
+        }
+        DGroup& g = d.g[d.ng++];
+        g.wl = s.wl;
+        g.partial = nullptr;
+        if (first_part) {
+          g.pull = 2;
+          g.seg_begin = d.ns;
+          add_segs(d, s.a0, s.len, false, 0, 0);
+          g.seg_end = d.ns;
+          if (!strict && s.acc_count > 0) g.partial = s.acc[s.c_local % R_];
+        } else {
+          g.pull = 0;
+        }
+        first_part = false;
+        g.f_begin = d.nf;
+        for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
+          DFold& f = d.f[d.nf++];
+          f.v = (uint32_t)v;
+          f.p = (uint32_t)folds[fi];
+          f.grad = nullptr;
+        }
+        g.f_end = d.nf;
+      } while (fi < folds.size());
+    }
+    if (hp_status st = emit(d, rg.first, rg.second)) return st;
+  }
+  for (int v : bpull_)
+    if (!vw_[v].here) vw_[v].pending_folds.clear();
+  bc_.clear();
+  ba_.clear();
+  bpull_.clear();
+  phase_ = kNone;
+  return HP_OK;
+}
+
+hp_status Engine::ipc_handle(void* out) {
+  if (sticky_) return sticky_;
+  cudaIpcMemHandle_t h;
+  if (int e = cudaIpcGetMemHandle(&h, arena_)) return check_cuda(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == kIpcBytes, "IPC handle size");
+  memcpy(out, &h, kIpcBytes);
+  return HP_OK;
+}
+
+hp_status Engine::connect(const void* handles, const void* comm_id) {
+  if (sticky_) return sticky_;
+  if (!dist_) return fail(HP_ERR_STATE, "hp_connect needs world > 1");
+  if (comm_) return fail(HP_ERR_STATE, "already connected");
+  for (int q = 0; q < G_; ++q) {
+    if (q == rank_) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char*)handles + (size_t)q * kIpcBytes, kIpcBytes);
+    void* p = nullptr;
+    if (int e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess))
+      return check_cuda(e, "cudaIpcOpenMemHandle");
+    opened_.push_back(p);
+    peer_[q] = (char*)p;
+  }
+  std::string err;
+  comm_ = comm_create(comm_id, G_, rank_, &err);
+  if (!comm_) return fail(HP_ERR_COMM, err);
+  // everyone's init writes are complete before anyone reads a peer
+  if (int e = comm_->barrier(stream_)) return fail(HP_ERR_COMM, comm_->error());
+  return check_cuda(cudaStreamSynchronize(stream_), "connect sync");
+}
+
+int64_t Engine::local_len(int which) const {
+  if (which == -1 || which == -2) return n_;
+  return vw_[which].here ? vw_[which].len : 0;
 }
 
 hp_status Engine::flush_applies() {
@@ -474,8 +805,9 @@ hp_status Engine::sync() {
 hp_status Engine::read(int which, int64_t off, int64_t cnt, float* dst) {
   if (sticky_) return sticky_;
   if (which < -2 || which >= N_) return fail(HP_ERR_INVALID, "bad buffer id");
-  if (off < 0 || cnt < 0 || off + cnt > n_ || (cnt && !dst)) return fail(HP_ERR_INVALID, "bad range");
   if (which == -2 && !m_) return fail(HP_ERR_INVALID, "no momentum buffer");
+  const int64_t len = local_len(which);
+  if (off < 0 || cnt < 0 || off + cnt > len || (cnt && !dst)) return fail(HP_ERR_INVALID, "bad range");
   if (hp_status st = sync()) return st;
   const float* src = which == -1 ? wg_ : which == -2 ? m_ : vw_[which].wl;
   if (int e = cudaMemcpy(dst, src + off, (size_t)cnt * 4, cudaMemcpyDeviceToHost))
@@ -494,6 +826,7 @@ void Engine::stats(hp_stats* out) const {
     out->wait_ticks[v] = vw_[v].wait;
     out->pulls[v] = vw_[v].pulls;
   }
+  out->nvl_bytes = nvl_bytes_;
 }
 
 hp_status Engine::profile_enable(bool on) {

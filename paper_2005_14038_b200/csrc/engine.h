@@ -19,9 +19,21 @@
 #include <vector>
 
 #include "../../include/hetpipe.h"
+#include "comm.h"
 #include "tick_desc.h"
 
 namespace hp {
+
+// Where a rank's buffers live in its arena (same function on every rank, so
+// any rank can address any peer's buffers through the peer's arena base).
+struct RankLayout {
+  int64_t s0 = 0, s1 = 0;             // PS shard [s0, s1) (global params)
+  size_t wg_off = 0, m_off = 0, bytes = 0;
+  std::vector<int64_t> a, len;        // per VW: local stage [a, a+len)
+  std::vector<char> has;              // per VW: a stage lives on this rank
+  std::vector<size_t> wl_off;
+  std::vector<std::vector<size_t>> acc_off;
+};
 
 struct VW {
   int64_t started = 0, completed = 0, c_local = 0;
@@ -32,6 +44,8 @@ struct VW {
   int64_t acc_count = 0;         // completions in the open wave
   std::vector<int64_t> backlog;  // completions while waiting at the gate (Z17)
   std::vector<int64_t> pending_folds;  // u_p not yet folded into w_local on device
+  int64_t a0 = 0, len = 0;       // this rank's stage of the VW (global range)
+  bool here = false;             // the VW has a stage (possibly empty) on this rank
   float* wl = nullptr;
   std::vector<float*> acc;       // ring of R slots; wave c -> slot c % R
   std::vector<const float*> grad_of_slot;  // EXTERNAL: grad of minibatch p in slot (p-1)%Nm
@@ -51,6 +65,11 @@ class Engine {
   hp_status admit(int v, std::vector<int64_t>* started);
   hp_status tick_end(std::vector<std::pair<int, int64_t>>* ungated);
   hp_status flush_applies();
+  hp_status ipc_handle(void* out);
+  hp_status connect(const void* handles, const void* comm_id);
+  bool distributed() const { return dist_; }
+  int64_t local_len(int which) const;
+  double nvl_bytes() const { return nvl_bytes_; }
   hp_status flush_pending() { return bc_.empty() && ba_.empty() && bpull_.empty() && !has_due_folds() ? HP_OK : flush(); }
   hp_status sync();
   hp_status read(int which, int64_t off, int64_t cnt, float* dst);
@@ -88,7 +107,11 @@ class Engine {
   enum Phase { kNone = 0, kPhComplete = 1, kPhPush = 2, kPhPull = 3 };
 
   hp_status flush();
-  hp_status emit(TickDesc& d);
+  hp_status flush_local();
+  hp_status flush_dist();
+  hp_status emit(TickDesc& d, int64_t begin, int64_t n);
+  RankLayout layout_of(int q) const;
+  int add_segs(TickDesc& d, int64_t a, int64_t len, bool acc_of_vw, int v, int slot);
   hp_status check_cuda(int err, const char* what);
   void rec(char phase, int v, const char* kind, int64_t p, int64_t c);
   std::pair<bool, bool> gate_open(int v) const;
@@ -100,6 +123,15 @@ class Engine {
   }
 
   hp_config cfg_;
+  bool dist_ = false;                 // world > 1: placement with peer exchange
+  int G_ = 1, rank_ = 0, span_ = 1;
+  std::vector<int64_t> shard_b_;      // PS shard boundaries over G
+  std::vector<int64_t> stage_b_;      // VW stage boundaries over span
+  std::vector<RankLayout> lay_;
+  std::vector<char*> peer_;           // arena base of every rank (own = arena_)
+  std::vector<void*> opened_;         // IPC mappings to close
+  Comm* comm_ = nullptr;
+  double nvl_bytes_ = 0;
   int N_, Nm_, R_;
   int64_t W_, last_p_, n_, begin_;
   cudaStream_t stream_ = nullptr;

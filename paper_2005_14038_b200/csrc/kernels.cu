@@ -92,6 +92,14 @@ __device__ __forceinline__ float4 synth_u(const TickDesc& d, uint32_t v, uint32_
                      __fmul_rn(d.neg_lr, grad_of<GM>(x.z)), __fmul_rn(d.neg_lr, grad_of<GM>(x.w)));
 }
 
+// Source of chunk q among segments [b, e): first with 4q < end (ends are
+// multiples of 32 params, so a chunk never straddles two segments).
+__device__ __forceinline__ const float* seg_ptr(const TickDesc& d, int b, int e, int64_t q) {
+  int s = b;
+  while (s + 1 < e && 4 * q >= d.s[s].end) ++s;
+  return d.s[s].ptr;
+}
+
 template <bool MOM>
 __device__ __forceinline__ void apply(float4& wg, float4& m, float4 ut, float mu) {
   if (MOM) {
@@ -126,7 +134,7 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
   for (int k = 0; k < d.na; ++k) {
     float4 s[U];
 #pragma unroll
-    for (int x = 0; x < U; ++x) s[x] = ld4<CNT>(d.a[k].src, q0 + x * qs);
+    for (int x = 0; x < U; ++x) s[x] = ld4<CNT>(seg_ptr(d, d.a[k].seg_begin, d.a[k].seg_end, q0 + x * qs), q0 + x * qs);
 #pragma unroll
     for (int x = 0; x < U; ++x) apply<MOM>(wg[x], mm[x], s[x], d.mu);
   }
@@ -168,9 +176,10 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
 #pragma unroll
     for (int x = 0; x < U; ++x) {
       const int64_t q = q0 + x * qs;
-      if (!g.pull) w[x] = ld4<CNT>(g.wl, q);
-      else if (g.partial) w[x] = f4add(wg[x], ld4<CNT>(g.partial, q));
+      if (g.pull == 0) w[x] = ld4<CNT>(g.wl, q);
+      else if (g.pull == 2) w[x] = ld4<CNT>(seg_ptr(d, g.seg_begin, g.seg_end, q), q);
       else w[x] = wg[x];
+      if (g.pull && g.partial) w[x] = f4add(w[x], ld4<CNT>(g.partial, q));
     }
     for (int fi = g.f_begin; fi < g.f_end; ++fi) {
       const DFold& f = d.f[fi];

@@ -22,6 +22,7 @@ constexpr int kMaxC = 8;    // completes per launch (at most one per VW per tick
 constexpr int kMaxA = 16;   // memory-sourced applies per launch
 constexpr int kMaxG = 8;    // w_local groups per launch (one per VW)
 constexpr int kMaxF = 40;   // folds per launch
+constexpr int kMaxS = 32;   // source segments per launch
 
 enum : uint32_t {
   kFirst = 1u,       // first minibatch of its wave: a = u
@@ -40,8 +41,16 @@ struct DComplete {
   uint32_t pad;
 };
 
+// A source array split into segments by local index: element i of the launch
+// reads seg.ptr[i] for the first segment with i < seg.end (ptr pre-offset so the
+// launch's local index addresses it; may point into a peer GPU's memory).
+struct DSeg {
+  const float* ptr;
+  int64_t end;
+};
+
 struct DApply {
-  const float* src;    // acc slot holding u~ of an earlier push
+  int32_t seg_begin, seg_end;   // acc slice(s) holding u~ of an earlier push
 };
 
 struct DFold {
@@ -52,8 +61,10 @@ struct DFold {
 struct DGroup {
   float* wl;             // w_local of this VW (local shard)
   const float* partial;  // AT_LEAST pull: open-wave acc slot, or nullptr
-  int32_t pull;          // 1: base = w_global (+partial); 0: base = w_local
+  int32_t pull;          // 0: base = w_local; 1: base = this launch's w_global
+                         // (+partial); 2: base = w_global read through segments
   int32_t f_begin, f_end;
+  int32_t seg_begin, seg_end;
   int32_t pad;
 };
 
@@ -72,9 +83,12 @@ struct TickDesc {
   DApply a[kMaxA];
   DGroup g[kMaxG];
   DFold f[kMaxF];
+  DSeg s[kMaxS];
+  int32_t ns;
+  int32_t pad2;
 };
 
-static_assert(sizeof(TickDesc) <= 4000, "TickDesc must fit a kernel parameter");
+static_assert(sizeof(TickDesc) <= 4096, "TickDesc must fit a kernel parameter");
 
 // Buffer passes of one launch (each = 4 bytes per param): the algorithmic
 // bytes the fused tick must move, used for the roofline.
@@ -88,7 +102,7 @@ inline int tick_streams(const TickDesc& d) {
          ((f & kFoldInline) ? 2 : 0);
   }
   for (int g = 0; g < d.ng; ++g) {
-    s += 1 + (d.g[g].pull ? 0 : 1) + (d.g[g].partial ? 1 : 0);
+    s += 1 + (d.g[g].pull == 1 ? 0 : 1) + (d.g[g].partial ? 1 : 0);
     for (int k = d.g[g].f_begin; k < d.g[g].f_end; ++k) s += d.f[k].grad ? 1 : 0;
   }
   return s;

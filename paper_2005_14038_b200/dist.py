@@ -26,3 +26,22 @@ def rank_context(cfg, rank: int, world: int, device: int = 0, stream: int = 0,
     c = hetpipe.config_from(cfg, param_begin=lo, param_count=hi - lo, device=device,
                             stream=stream or None, **overrides)
     return hetpipe.Context(c, lib=lib)
+
+
+def placed_context(cfg, rank: int, world: int, span: int, device: int = 0, stream: int = 0,
+                   pg=None, **overrides) -> hetpipe.Context:
+    """Collective: context for `rank` of a distributed placement (world G, VW
+    span k; include/hetpipe.h hp_config.vw_span). Rank 0 draws the barrier
+    communicator id; IPC handles of every rank's arena are all-gathered with
+    torch.distributed (process group `pg`, default group), then hp_connect maps
+    the peers. After this every rank must drive the same protocol calls."""
+    import torch.distributed as dist
+    c = hetpipe.config_from(cfg, world=world, rank=rank, vw_span=span, device=device,
+                            stream=stream or None, **overrides)
+    ctx = hetpipe.Context(c)
+    ids = [hetpipe.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0, group=pg)
+    handles = [None] * world
+    dist.all_gather_object(handles, ctx.ipc_handle(), group=pg)
+    ctx.connect(handles, ids[0])
+    return ctx

@@ -30,14 +30,15 @@ class hp_config(C.Structure):
                 ("grad_mode", C.c_int32), ("w0_mode", C.c_int32),
                 ("pull_policy", C.c_int32), ("local_semantics", C.c_int32),
                 ("apply_mode", C.c_int32), ("acc_slots", C.c_int32),
-                ("merge_ticks", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p)]
+                ("merge_ticks", C.c_int32), ("world", C.c_int32), ("rank", C.c_int32),
+                ("vw_span", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p)]
 
 
 class hp_stats(C.Structure):
     _fields_ = [("commits", C.c_int64), ("applied", C.c_int64),
                 ("launches", C.c_int64), ("ticks", C.c_int64),
                 ("alg_bytes", C.c_double), ("wait_ticks", C.c_int64 * 8),
-                ("pulls", C.c_int64 * 8)]
+                ("pulls", C.c_int64 * 8), ("nvl_bytes", C.c_double)]
 
 
 class HetPipeError(RuntimeError):
@@ -61,6 +62,9 @@ EXPORTS = {
     "hp_tick_end": (C.c_int, [C.c_void_p]),
     "hp_flush": (C.c_int, [C.c_void_p]),
     "hp_set_tick": (C.c_int, [C.c_void_p, C.c_int64]),
+    "hp_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "hp_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "hp_connect": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "hp_schedule_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "hp_schedule_advance": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
     "hp_run_schedule": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -179,6 +183,16 @@ class Context:
     def flush(self) -> int:
         return self._chk(self.lib.hp_flush(self.h))
 
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        self._chk(self.lib.hp_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def connect(self, handles: Sequence[bytes], comm_id: bytes) -> None:
+        hb = C.create_string_buffer(b"".join(handles), 64 * len(handles))
+        cb = C.create_string_buffer(comm_id, 128)
+        self._chk(self.lib.hp_connect(self.h, hb, cb))
+
     def set_tick(self, t: int) -> int:
         return self._chk(self.lib.hp_set_tick(self.h, t))
 
@@ -209,13 +223,28 @@ class Context:
         self._chk(self.lib.hp_schedule_set_host_grads(self.h, arr, len(bufs)))
 
     # -- data -----------------------------------------------------------------
+    def local_len(self, which: int) -> int:
+        """Length of buffer `which` on this rank (placement-aware)."""
+        from workloads import even_shards
+        c = self.cfg
+        if c.world <= 1:
+            return c.param_count
+        if which < 0:
+            b = even_shards(c.nparams, c.world)
+            return b[c.rank + 1] - b[c.rank]
+        for j in range(c.vw_span):
+            if (which * c.vw_span + j) % c.world == c.rank:
+                b = even_shards(c.nparams, c.vw_span)
+                return b[j + 1] - b[j]
+        return 0
+
     def sync(self) -> None:
         self._chk(self.lib.hp_sync(self.h))
 
     def read_weights(self, which: int, offset: int = 0, count: Optional[int] = None,
                      out: Optional[np.ndarray] = None) -> np.ndarray:
         if count is None:
-            count = self.cfg.param_count - offset
+            count = self.local_len(which) - offset
         if out is None:
             out = np.empty(count, dtype=np.float32)
         self._chk(self.lib.hp_read_weights(self.h, which, offset, count,
@@ -260,6 +289,15 @@ def _profile_launches(self, max_records: int = 1 << 16):
 
 
 Context.profile_launches = _profile_launches
+
+
+def comm_unique_id(lib: Optional[C.CDLL] = None) -> bytes:
+    lib = lib if lib is not None else load()
+    buf = C.create_string_buffer(128)
+    st = lib.hp_comm_unique_id(buf)
+    if st != HP_OK:
+        raise HetPipeError(st, lib.hp_last_error(None).decode())
+    return buf.raw
 
 
 def s_global(Nm: int, D: int) -> int:

@@ -14,6 +14,10 @@ typedef struct CUevent_st* cudaEvent_t;
 enum cudaMemcpyKind { cudaMemcpyHostToHost, cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost,
                       cudaMemcpyDeviceToDevice, cudaMemcpyDefault };
 #define cudaStreamNonBlocking 1
+#define cudaIpcMemLazyEnablePeerAccess 1
+typedef struct {
+  char reserved[64];
+} cudaIpcMemHandle_t;
 
 inline cudaError_t cudaSetDevice(int) { return cudaSuccess; }
 inline cudaError_t cudaGetLastError() { return cudaSuccess; }
@@ -57,5 +61,21 @@ inline cudaError_t cudaEventDestroy(cudaEvent_t) { return cudaSuccess; }
 inline cudaError_t cudaEventRecord(cudaEvent_t, cudaStream_t) { return cudaSuccess; }
 inline cudaError_t cudaEventElapsedTime(float* ms, cudaEvent_t, cudaEvent_t) {
   *ms = 0.f;
+  return cudaSuccess;
+}
+
+// "IPC" inside one process: the handle carries the pointer itself.
+inline cudaError_t cudaIpcGetMemHandle(cudaIpcMemHandle_t* h, void* p) {
+  memset(h, 0, sizeof *h);
+  memcpy(h->reserved, &p, sizeof p);
+  return cudaSuccess;
+}
+inline cudaError_t cudaIpcOpenMemHandle(void** p, cudaIpcMemHandle_t h, unsigned) {
+  memcpy(p, h.reserved, sizeof *p);
+  return cudaSuccess;
+}
+inline cudaError_t cudaIpcCloseMemHandle(void*) { return cudaSuccess; }
+inline cudaError_t cudaMemset(void* p, int v, size_t n) {
+  memset(p, v, n);
   return cudaSuccess;
 }

@@ -34,6 +34,12 @@ float draw_u(const TickDesc& d, int gm, uint32_t v, uint32_t p, int64_t i, const
   return d.neg_lr * g;
 }
 
+const float* seg(const TickDesc& d, int b, int e, int64_t i) {
+  int s = b;
+  while (s + 1 < e && i >= d.s[s].end) ++s;
+  return d.s[s].ptr;
+}
+
 void app(const TickDesc& d, bool mom, float& wg, float& m, float ut) {
   if (mom) {
     m = d.mu * m + ut;
@@ -49,7 +55,7 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*) {
   for (int64_t i = 0; i < d.n; ++i) {
     float wg = d.wg_load ? d.wg[i] : 0.f;
     float m = (mom && d.wg_store) ? d.m[i] : 0.f;
-    for (int k = 0; k < d.na; ++k) app(d, mom, wg, m, d.a[k].src[i]);
+    for (int k = 0; k < d.na; ++k) app(d, mom, wg, m, seg(d, d.a[k].seg_begin, d.a[k].seg_end, i)[i]);
     for (int j = 0; j < d.nc; ++j) {
       const DComplete& c = d.c[j];
       const float u = draw_u(d, gm, c.v, c.p, i, c.grad);
@@ -64,7 +70,8 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*) {
     }
     for (int g = 0; g < d.ng; ++g) {
       const DGroup& G = d.g[g];
-      float w = !G.pull ? G.wl[i] : G.partial ? wg + G.partial[i] : wg;
+      float w = G.pull == 0 ? G.wl[i] : G.pull == 2 ? seg(d, G.seg_begin, G.seg_end, i)[i] : wg;
+      if (G.pull && G.partial) w = w + G.partial[i];
       for (int f = G.f_begin; f < G.f_end; ++f) w = w + draw_u(d, gm, d.f[f].v, d.f[f].p, i, d.f[f].grad);
       G.wl[i] = w;
     }

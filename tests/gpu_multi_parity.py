@@ -1,0 +1,111 @@
+"""Multi-GPU parity of the distributed placements (run under torchrun, one
+rank per GPU; invoked by tests/test_gpu_multi.py). Every rank drives the real
+library; rank 0 gathers the shards/stages and compares them with the oracle:
+bit-exact arrays (the applies run in commit order) and identical traces.
+Prints 'MULTI-GPU PARITY OK' on success, exits 1 otherwise."""
+import os
+import sys
+import tempfile
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import run_schedule  # noqa: E402
+from paper_2005_14038_b200 import dist as hdist  # noqa: E402
+from workloads import C3, C4, C5, WSPConfig, sample_indices, even_shards  # noqa: E402
+
+
+def run(cfg, G, k, rank, local, sampled):
+    stream = torch.cuda.Stream(local)
+    ctx = hdist.placed_context(cfg, rank, G, k, device=local, stream=stream.cuda_stream)
+    ctx.run_schedule(cfg.tau, cfg.latency())
+    with tempfile.NamedTemporaryFile(suffix=".trace") as f:
+        tr = ctx.trace_lines(f.name)
+    wg = ctx.read_weights(-1)
+    m = ctx.read_weights(-2) if cfg.momentum else None
+    wl = {}
+    for v in range(cfg.num_vw):
+        if any((v * k + j) % G == rank for j in range(k)):
+            wl[v] = ctx.read_weights(v)
+    nvl = ctx.stats().nvl_bytes
+    ctx.close()
+    if sampled is not None:      # ship only sampled entries (full arrays are GBs)
+        sb = even_shards(cfg.nparams, G)
+        lo = sb[rank]
+        wg = {int(i): float(wg[i - lo]) for i in sampled if sb[rank] <= i < sb[rank + 1]}
+        m = None if m is None else {int(i): float(m[i - lo]) for i in sampled if sb[rank] <= i < sb[rank + 1]}
+        st = even_shards(cfg.nparams, k)
+        wl2 = {}
+        for v, arr in wl.items():
+            j = [j for j in range(k) if (v * k + j) % G == rank][0]
+            wl2[v] = {int(i): float(arr[i - st[j]]) for i in sampled if st[j] <= i < st[j + 1]}
+        wl = wl2
+    objs = [None] * G
+    dist.all_gather_object(objs, (tr, wg, m, wl, nvl))
+    return objs
+
+
+def check(cfg, G, k, objs, sampled):
+    o = run_schedule(cfg, idx=None if sampled is None else np.array(sampled))
+    for r in range(G):
+        assert objs[r][0] == o.trace, f"trace of rank {r}"
+    if sampled is None:
+        assert np.array_equal(np.concatenate([objs[r][1] for r in range(G)]), o.wg)
+        if cfg.momentum:
+            assert np.array_equal(np.concatenate([objs[r][2] for r in range(G)]), o.m)
+        for v in range(cfg.num_vw):
+            parts = [objs[(v * k + j) % G][3][v] for j in range(k)]
+            assert np.array_equal(np.concatenate(parts), o.wl[v]), f"w_local({v})"
+    else:
+        pos = {int(i): n for n, i in enumerate(sampled)}
+        wg = {}
+        for r in range(G):
+            wg.update(objs[r][1])
+        assert all(np.float32(wg[i]) == o.wg[pos[i]] for i in sampled)
+        for v in range(cfg.num_vw):
+            wl = {}
+            for j in range(k):
+                wl.update(objs[(v * k + j) % G][3][v])
+            assert all(np.float32(wl[i]) == o.wl[v][pos[i]] for i in sampled), f"w_local({v})"
+    nvl = sum(objs[r][4] for r in range(G))
+    assert (nvl == 0) == (k == G), nvl
+
+
+def main():
+    rank, G, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")          # object exchange only; data moves over NVLink
+    cases = [
+        (C3.replace(nparams=40_000, waves=8), 1, None),
+        (C3.replace(nparams=40_003, waves=8, momentum=0.9), max(1, G // 2), None),
+        (WSPConfig("lazy", 3, 3, 1, 12_345, 7, (3, 5, 4), pull_policy=1, local_semantics=1), 1, None),
+        (C4.replace(nparams=50_000, waves=4), G, None),
+        (C5.replace(waves=2, D=4, num_vw=G, tau=C5.tau[:G]) if G <= 8 else None, 1, "sample"),
+        (C3.replace(waves=3), max(1, G // 4), "sample"),
+    ]
+    ok = True
+    for cfg, k, mode in cases:
+        if cfg is None:
+            continue
+        sampled = sample_indices(cfg.nparams, 104729, even_shards(cfg.nparams, G)) if mode else None
+        objs = run(cfg, G, k, rank, local, sampled)
+        if rank == 0:
+            try:
+                check(cfg, G, k, objs, sampled)
+                print(f"ok {cfg.name} N={cfg.num_vw} P={cfg.nparams} G={G} k={k}", flush=True)
+            except AssertionError as e:
+                ok = False
+                print(f"FAIL {cfg.name} G={G} k={k}: {e}", flush=True)
+        dist.barrier()
+    if rank == 0:
+        print("MULTI-GPU PARITY OK" if ok else "MULTI-GPU PARITY FAILED", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
