@@ -244,9 +244,13 @@ def main():
     kern_ms, kern_bytes, kern_launches = ctx.profile_read()
     l_ms, l_bytes, l_shape = ctx.profile_launches()
     mix = {}
+    sync_us = []
     for t_ms, by, sh in zip(l_ms, l_bytes, l_shape):
+        sh = int(sh) & 0xFFFFFFFF
         key = (f"c{sh & 15}i{(sh >> 4) & 15}a{(sh >> 8) & 255}g{(sh >> 16) & 255}"
-               f"f{(sh >> 24) & 255}")
+               f"f{(sh >> 24) & 127}")
+        if sh >> 31 or (sh >> 8) & 255:
+            sync_us.append(1e3 * float(t_ms))
         e = mix.setdefault(key, [0, 0.0, 0.0])
         e[0] += 1
         e[1] += float(t_ms)
@@ -338,6 +342,11 @@ def main():
         "nvlink": {"bytes_per_step_max_rank": nvl_bytes_max / args.steps,
                    "GBps_over_step": nvl_bytes_max / (ms_max / 1e3) / 1e9,
                    "peak_GBps": 770.0, "peak_kind": "guide-measured peer copy per direction"},
+        "wave_sync_latency_us": (
+            {"p50": float(np.percentile(sync_us, 50)), "p99": float(np.percentile(sync_us, 99)),
+             "n": len(sync_us),
+             "def": "device time of each launch that applies pushed waves or pulls "
+                    "(push -> apply -> pull of a round, fused)"} if sync_us else None),
         "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
         "launch_mix": launch_mix,
         "gpu_launches": launches,

@@ -211,9 +211,9 @@ hp_status hp_profile_enable(hp_ctx* ctx, int32_t enable);
 hp_status hp_profile_read(hp_ctx* ctx, double* kernel_ms, double* alg_bytes,
                           int64_t* launches);
 /* Per-launch detail of the same window, up to max records: duration (ms),
-   algorithmic bytes, and shape = nc | ni<<4 | na<<8 | ng<<16 | nf<<24
-   (completes, inline folds, memory applies, w_local groups, group folds of the
-   fused launch). *n = records written. */
+   algorithmic bytes, and shape = nc | ni<<4 | na<<8 | ng<<16 | nf<<24 | pull<<31
+   (completes, inline folds, memory applies, w_local groups, group folds, and
+   whether a pull is in the fused launch). *n = records written. */
 hp_status hp_profile_launches(hp_ctx* ctx, int64_t max, float* ms, double* alg_bytes,
                               int32_t* shape, int64_t* n);
 

@@ -435,7 +435,10 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n) {
     prof_launch_bytes_.push_back(bytes);
     int inl = 0;
     for (int j = 0; j < d.nc; ++j) inl += (d.c[j].flags & kFoldInline) ? 1 : 0;
-    prof_launch_shape_.push_back(d.nc | (inl << 4) | (d.na << 8) | (d.ng << 16) | (d.nf << 24));
+    int pulls = 0;
+    for (int g = 0; g < d.ng; ++g) pulls |= d.g[g].pull != 0;
+    prof_launch_shape_.push_back(d.nc | (inl << 4) | (d.na << 8) | (d.ng << 16) | (d.nf << 24) |
+                                 (int)((unsigned)pulls << 31));
   }
   launches_++;
   alg_bytes_ += bytes;
