@@ -80,6 +80,8 @@ RankLayout Engine::layout_of(int q) const {
 
 Engine::~Engine() {
   delete comm_;
+  for (auto e : evpool_) cudaEventDestroy(e);
+  if (xs_) cudaStreamDestroy(xs_);
   for (void* p : opened_) cudaIpcCloseMemHandle(p);
   for (auto e : ev_) cudaEventDestroy(e);
   if (arena_) cudaFree(arena_);
@@ -381,7 +383,8 @@ hp_status Engine::tick_end(std::vector<std::pair<int, int64_t>>* ungated) {
 // Batch -> TickDesc(s). Algorithmic bytes are counted from the descriptor: each
 // buffer read or written once per launch = 4 bytes per param of the launch's
 // range [begin, begin+n); reads through peer segments are also NVLink bytes.
-hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n) {
+hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st) {
+  if (!st) st = stream_;
   d.n = n;
   d.blk_base = begin >> 2;
   d.wg = wg_;
@@ -425,11 +428,11 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n) {
     e0 = ev_[ev_used_];
     e1 = ev_[ev_used_ + 1];
     ev_used_ += 2;
-    cudaEventRecord(e0, stream_);
+    cudaEventRecord(e0, st);
   }
-  int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, stream_);
+  int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, st);
   if (prof_on_) {
-    cudaEventRecord(e1, stream_);
+    cudaEventRecord(e1, st);
     prof_bytes_ += bytes;
     prof_launches_++;
     prof_launch_bytes_.push_back(bytes);
@@ -628,9 +631,18 @@ hp_status Engine::flush_dist() {
   std::vector<std::vector<int64_t>> pull_folds(N_);
   std::vector<bool> pulled(N_, false);
   for (int v : bpull_) pulled[v] = true;
+  auto wait_x = [&](int v) {  // compute stream waits for v's last exchange op
+    if (xdep_[v]) {
+      cudaStreamWaitEvent(stream_, xdep_[v], 0);
+      xdep_[v] = nullptr;
+    }
+  };
   for (auto& rg : ranges) {
     TickDesc d;
     memset(&d, 0, sizeof d);
+    for (const BComplete& b : bc_) {
+      if (vw_[b.v].here && vw_[b.v].a0 == rg.first && vw_[b.v].len == rg.second) wait_x(b.v);
+    }
     for (const BComplete& b : bc_) {
       const VW& s = vw_[b.v];
       if (!s.here || s.a0 != rg.first || s.len != rg.second) continue;
@@ -649,6 +661,7 @@ hp_status Engine::flush_dist() {
       if (hold || s.pending_folds.empty()) continue;
       std::vector<int64_t> folds;
       folds.swap(s.pending_folds);
+      wait_x(v);
       if (folds.size() == 1) {
         int jj = -1;
         for (int j = 0; j < d.nc; ++j)
@@ -684,8 +697,16 @@ hp_status Engine::flush_dist() {
   for (int v = 0; v < N_; ++v)
     if (!vw_[v].here && !pulled[v] && !(strict && vw_[v].at_gate)) vw_[v].pending_folds.clear();
   // ---- 2. applies on this rank's PS shard -------------------------------
+  // the exchange stream starts after every local launch issued so far (the
+  // pushed u~ and the pulled VWs' w_local are complete on this rank)
+  if (!ba_.empty() || !bpull_.empty()) {
+    cudaEvent_t e = pool_event();
+    cudaEventRecord(e, stream_);
+    cudaStreamWaitEvent(xs_, e, 0);
+    x_pending_ = true;
+  }
   if (!ba_.empty()) {
-    if (int e = comm_->barrier(stream_)) return fail(HP_ERR_COMM, comm_->error());
+    if (int e = comm_->barrier(xs_)) return fail(HP_ERR_COMM, comm_->error());
     size_t k = 0;
     while (k < ba_.size()) {
       TickDesc d;
@@ -698,10 +719,14 @@ hp_status Engine::flush_dist() {
         d.na++;
         ++k;
       }
-      if (hp_status st = emit(d, begin_, n_)) return st;
+      if (hp_status st = emit(d, begin_, n_, xs_)) return st;
     }
     applied_ += (int64_t)ba_.size();
-    if (int e = comm_->barrier(stream_)) return fail(HP_ERR_COMM, comm_->error());
+    if (int e = comm_->barrier(xs_)) return fail(HP_ERR_COMM, comm_->error());
+    cudaEvent_t e = pool_event();       // acc slots read by the applies are free
+    cudaEventRecord(e, xs_);
+    for (const BApply& a : ba_)
+      if (vw_[a.v].here) xdep_[a.v] = e;
   }
   // ---- 3. pulls -----------------------------------------------------------
   for (auto& rg : ranges) {
@@ -716,7 +741,7 @@ hp_status Engine::flush_dist() {
       bool first_part = true;
       do {
         if (d.ng == kMaxG || d.nf == kMaxF || d.ns + G_ > kMaxS) {
-          if (hp_status st = emit(d, rg.first, rg.second)) return st;
+          if (hp_status st = emit(d, rg.first, rg.second, xs_)) return st;
           memset(&d, 0, sizeof d);
         }
         DGroup& g = d.g[d.ng++];
@@ -742,7 +767,13 @@ hp_status Engine::flush_dist() {
         g.f_end = d.nf;
       } while (fi < folds.size());
     }
-    if (hp_status st = emit(d, rg.first, rg.second)) return st;
+    if (hp_status st = emit(d, rg.first, rg.second, xs_)) return st;
+  }
+  if (!bpull_.empty()) {
+    cudaEvent_t e = pool_event();       // w_local of the pulled VWs is written
+    cudaEventRecord(e, xs_);
+    for (int v : bpull_)
+      if (vw_[v].here) xdep_[v] = e;
   }
   for (int v : bpull_)
     if (!vw_[v].here) vw_[v].pending_folds.clear();
@@ -751,6 +782,30 @@ hp_status Engine::flush_dist() {
   bpull_.clear();
   phase_ = kNone;
   return HP_OK;
+}
+
+cudaEvent_t Engine::pool_event() {
+  // events are reused round-robin; an event is only waited on shortly after it
+  // is recorded, long before the pool wraps
+  if (evpool_.size() < 256) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    evpool_.push_back(e);
+    return e;
+  }
+  cudaEvent_t e = evpool_[evnext_];
+  evnext_ = (evnext_ + 1) % evpool_.size();
+  return e;
+}
+
+hp_status Engine::join_exchange() {
+  if (!x_pending_) return HP_OK;
+  cudaEvent_t e = pool_event();
+  cudaEventRecord(e, xs_);
+  cudaStreamWaitEvent(stream_, e, 0);
+  std::fill(xdep_.begin(), xdep_.end(), nullptr);
+  x_pending_ = false;
+  return check_cuda(cudaGetLastError(), "join");
 }
 
 hp_status Engine::ipc_handle(void* out) {
@@ -779,6 +834,8 @@ hp_status Engine::connect(const void* handles, const void* comm_id) {
   std::string err;
   comm_ = comm_create(comm_id, G_, rank_, &err);
   if (!comm_) return fail(HP_ERR_COMM, err);
+  if (int e = cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking)) return check_cuda(e, "stream");
+  xdep_.assign(N_, nullptr);
   // everyone's init writes are complete before anyone reads a peer
   if (int e = comm_->barrier(stream_)) return fail(HP_ERR_COMM, comm_->error());
   return check_cuda(cudaStreamSynchronize(stream_), "connect sync");
@@ -802,6 +859,7 @@ hp_status Engine::sync() {
   for (auto& vp : ungated_) rec('S', vp.first, "START", vp.second, wave_of(vp.second, Nm_));
   ungated_.clear();
   if (hp_status st = flush_applies()) return st;
+  if (hp_status st = join_exchange()) return st;
   return check_cuda(cudaStreamSynchronize(stream_), "sync");
 }
 
@@ -846,6 +904,7 @@ hp_status Engine::profile_enable(bool on) {
 hp_status Engine::profile_launches(int64_t max, float* ms, double* bytes, int32_t* shape,
                                    int64_t* n) {
   if (sticky_) return sticky_;
+  if (hp_status st = join_exchange()) return st;
   if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "profile sync")) return st;
   const int64_t cnt = std::min<int64_t>(max, (int64_t)prof_launch_bytes_.size());
   for (int64_t i = 0; i < cnt; ++i) {
@@ -861,6 +920,7 @@ hp_status Engine::profile_launches(int64_t max, float* ms, double* bytes, int32_
 
 hp_status Engine::profile_read(double* ms, double* bytes, int64_t* launches) {
   if (sticky_) return sticky_;
+  if (hp_status st = join_exchange()) return st;
   if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "profile sync")) return st;
   double tot = 0;
   for (size_t i = 0; i + 1 < ev_used_; i += 2) {

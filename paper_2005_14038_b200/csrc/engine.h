@@ -70,7 +70,11 @@ class Engine {
   bool distributed() const { return dist_; }
   int64_t local_len(int which) const;
   double nvl_bytes() const { return nvl_bytes_; }
-  hp_status flush_pending() { return bc_.empty() && ba_.empty() && bpull_.empty() && !has_due_folds() ? HP_OK : flush(); }
+  hp_status flush_pending() {
+    if (!(bc_.empty() && ba_.empty() && bpull_.empty() && !has_due_folds()))
+      if (hp_status st = flush()) return st;
+    return join_exchange();
+  }
   hp_status sync();
   hp_status read(int which, int64_t off, int64_t cnt, float* dst);
 
@@ -109,7 +113,9 @@ class Engine {
   hp_status flush();
   hp_status flush_local();
   hp_status flush_dist();
-  hp_status emit(TickDesc& d, int64_t begin, int64_t n);
+  hp_status emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st = nullptr);
+  cudaEvent_t pool_event();
+  hp_status join_exchange();          // compute stream waits for the exchange stream
   RankLayout layout_of(int q) const;
   int add_segs(TickDesc& d, int64_t a, int64_t len, bool acc_of_vw, int v, int slot);
   hp_status check_cuda(int err, const char* what);
@@ -131,6 +137,14 @@ class Engine {
   std::vector<char*> peer_;           // arena base of every rank (own = arena_)
   std::vector<void*> opened_;         // IPC mappings to close
   Comm* comm_ = nullptr;
+  // a9 overlap (world > 1): barrier/apply/pull launches run on an exchange
+  // stream; a compute-stream launch waits only for the exchange events of the
+  // VWs whose buffers it touches.
+  cudaStream_t xs_ = nullptr;
+  std::vector<cudaEvent_t> xdep_;     // per VW: exchange op that last touched it
+  std::vector<cudaEvent_t> evpool_;
+  size_t evnext_ = 0;
+  bool x_pending_ = false;            // exchange work not yet joined
   double nvl_bytes_ = 0;
   int N_, Nm_, R_;
   int64_t W_, last_p_, n_, begin_;

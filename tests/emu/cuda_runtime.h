@@ -58,6 +58,9 @@ inline cudaError_t cudaEventCreate(cudaEvent_t* e) {
   return cudaSuccess;
 }
 inline cudaError_t cudaEventDestroy(cudaEvent_t) { return cudaSuccess; }
+#define cudaEventDisableTiming 2
+inline cudaError_t cudaEventCreateWithFlags(cudaEvent_t* e, unsigned) { return cudaEventCreate(e); }
+inline cudaError_t cudaStreamWaitEvent(cudaStream_t, cudaEvent_t, unsigned) { return cudaSuccess; }
 inline cudaError_t cudaEventRecord(cudaEvent_t, cudaStream_t) { return cudaSuccess; }
 inline cudaError_t cudaEventElapsedTime(float* ms, cudaEvent_t, cudaEvent_t) {
   *ms = 0.f;
