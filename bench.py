@@ -203,7 +203,11 @@ def main():
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
     torch.cuda.set_device(local)
     if ws > 1:
-        os.environ.setdefault("NCCL_DEBUG", "WARN")     # keep stdout to the one JSON line
+        # libraries print to fd 1 (NCCL's version banner): send C-level stdout to
+        # stderr and keep the real stdout for the one JSON line
+        real_out = os.dup(1)
+        os.dup2(2, 1)
+        sys.stdout = os.fdopen(real_out, "w")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():

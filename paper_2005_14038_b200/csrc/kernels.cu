@@ -198,6 +198,10 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
 
 template <int GM, bool MOM, int U>
 __global__ void __launch_bounds__(256) tick_kernel(const __grid_constant__ TickDesc d) {
+  // Programmatic dependent launch: this grid may start while the previous tick
+  // kernel drains; it touches no global memory before the previous grid has
+  // completed and flushed its writes.
+  cudaGridDependencySynchronize();
   const int64_t nfull = d.n >> 2;
   const int64_t S = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -234,6 +238,7 @@ __global__ void init_kernel(float* out, int64_t n, int64_t param_begin, int w0_m
 }
 
 int g_u_override = -1;   // HP_TICK_U: tuning override of chunks per thread
+int g_pdl = 1;           // HP_PDL=0 disables programmatic dependent launch
 
 template <int GM, bool MOM, int U>
 int launch_u(const TickDesc& d, cudaStream_t s) {
@@ -249,8 +254,17 @@ int launch_u(const TickDesc& d, cudaStream_t s) {
   int64_t blocks = (chunks + 255) / 256;
   if (blocks > grid_max) blocks = grid_max;
   if (blocks < 1) blocks = 1;
-  tick_kernel<GM, MOM, U><<<(unsigned)blocks, 256, 0, s>>>(d);
-  return (int)cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, tick_kernel<GM, MOM, U>, d);
 }
 
 template <int GM, bool MOM>
@@ -271,6 +285,8 @@ int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream) {
   if (g_u_override == -1) {
     const char* e = getenv("HP_TICK_U");
     g_u_override = e ? atoi(e) : 0;
+    const char* p = getenv("HP_PDL");
+    g_pdl = p ? atoi(p) : 1;
   }
   if (d.n <= 0) return 0;
   switch (grad_mode) {
