@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace hp {
@@ -82,6 +83,8 @@ Engine::~Engine() {
   delete comm_;
   for (auto e : evpool_) cudaEventDestroy(e);
   if (xs_) cudaStreamDestroy(xs_);
+  for (auto v : vs_)
+    if (v) cudaStreamDestroy(v);
   for (void* p : opened_) cudaIpcCloseMemHandle(p);
   for (auto e : ev_) cudaEventDestroy(e);
   if (arena_) cudaFree(arena_);
@@ -383,7 +386,7 @@ hp_status Engine::tick_end(std::vector<std::pair<int, int64_t>>* ungated) {
 // Batch -> TickDesc(s). Algorithmic bytes are counted from the descriptor: each
 // buffer read or written once per launch = 4 bytes per param of the launch's
 // range [begin, begin+n); reads through peer segments are also NVLink bytes.
-hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st) {
+hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, int max_blocks) {
   if (!st) st = stream_;
   d.n = n;
   d.blk_base = begin >> 2;
@@ -430,7 +433,7 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st) {
     ev_used_ += 2;
     cudaEventRecord(e0, st);
   }
-  int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, st);
+  int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, st, max_blocks);
   if (prof_on_) {
     cudaEventRecord(e1, st);
     prof_bytes_ += bytes;
@@ -610,42 +613,36 @@ hp_status Engine::flush_local() {
 }
 
 // Distributed flush (world > 1). Replicated on every rank with identical
-// decisions, so every rank issues the same barriers:
-//   1. local launches, one per distinct local stage range: this rank's part of
-//      the batch's completes (acc always stored: peers read it), inline folds
-//      and fold-only groups;
-//   2. if the batch applies pushes: BARRIER (peer accs complete; earlier pulls
-//      of w_global done everywhere) -> apply launch(es) over this rank's PS
-//      shard, reading every pushed u~ slice from the GPU that holds it (NVLink
-//      loads inside the kernel, commit order) -> BARRIER (w_global final; acc
-//      slots free for reuse);
-//   3. pull launches: w_local(v) of each local stage <- w_global read from the
+// decisions, so every rank issues the same barriers. Streams (row a9,
+// overlap): each local VW's accumulation runs on its own stream; barriers,
+// applies and pulls run on the exchange stream xs_, which waits only for the
+// accumulation launches whose results it reads, and a VW's stream waits only
+// for the exchange ops that touched that VW's buffers.
+//   1. per local VW: its complete (acc always stored: peers read it) with an
+//      inline fold, or its fold-only group, on the VW's stream;
+//   2. if the batch applies pushes: xs_ waits for the pushing VWs' streams ->
+//      BARRIER (every rank's pushed u~ complete; earlier pulls of w_global done
+//      everywhere) -> apply launch(es) over this rank's PS shard reading every
+//      pushed u~ slice from the GPU that holds it (NVLink loads inside the
+//      kernel, commit order) -> BARRIER (w_global final; acc slots reusable);
+//   3. pulls on xs_: w_local(v) of each local stage <- w_global read from the
 //      shard owners (NVLink loads), then the VW's due folds.
 hp_status Engine::flush_dist() {
   const bool strict = cfg_.local_semantics == HP_LOCAL_STRICT;
-  // ---- 1. local work, grouped by stage range -----------------------------
-  std::vector<std::pair<int64_t, int64_t>> ranges;
-  for (int v = 0; v < N_; ++v)
-    if (vw_[v].here && std::find(ranges.begin(), ranges.end(), std::make_pair(vw_[v].a0, vw_[v].len)) == ranges.end())
-      ranges.push_back({vw_[v].a0, vw_[v].len});
-  std::vector<std::vector<int64_t>> pull_folds(N_);
+  fork_streams();
   std::vector<bool> pulled(N_, false);
   for (int v : bpull_) pulled[v] = true;
-  auto wait_x = [&](int v) {  // compute stream waits for v's last exchange op
-    if (xdep_[v]) {
-      cudaStreamWaitEvent(stream_, xdep_[v], 0);
-      xdep_[v] = nullptr;
+  // ---- 1. accumulation, one launch per local VW on its own stream ----------
+  for (int v = 0; v < N_; ++v) {
+    VW& s = vw_[v];
+    if (!s.here) {
+      if (!pulled[v] && !(strict && s.at_gate)) s.pending_folds.clear();  // peers' work
+      continue;
     }
-  };
-  for (auto& rg : ranges) {
     TickDesc d;
     memset(&d, 0, sizeof d);
     for (const BComplete& b : bc_) {
-      if (vw_[b.v].here && vw_[b.v].a0 == rg.first && vw_[b.v].len == rg.second) wait_x(b.v);
-    }
-    for (const BComplete& b : bc_) {
-      const VW& s = vw_[b.v];
-      if (!s.here || s.a0 != rg.first || s.len != rg.second) continue;
+      if (b.v != v) continue;
       DComplete& c = d.c[d.nc++];
       c.acc = s.acc[b.slot];
       c.grad = nullptr;
@@ -654,58 +651,48 @@ hp_status Engine::flush_dist() {
       c.p = (uint32_t)b.p;
       c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc;
     }
-    for (int v = 0; v < N_; ++v) {
-      VW& s = vw_[v];
-      if (!s.here || s.a0 != rg.first || s.len != rg.second || pulled[v]) continue;
-      const bool hold = strict && s.at_gate;
-      if (hold || s.pending_folds.empty()) continue;
-      std::vector<int64_t> folds;
-      folds.swap(s.pending_folds);
-      wait_x(v);
-      if (folds.size() == 1) {
-        int jj = -1;
-        for (int j = 0; j < d.nc; ++j)
-          if ((int)d.c[j].v == v && (int64_t)d.c[j].p == folds[0]) jj = j;
-        if (jj >= 0) {
-          d.c[jj].flags |= kFoldInline;
-          d.c[jj].wl = s.wl;
-          continue;
-        }
-      }
-      size_t fi = 0;
-      do {
-        if (d.ng == kMaxG || d.nf == kMaxF) {
-          if (hp_status st = emit(d, rg.first, rg.second)) return st;
-          memset(&d, 0, sizeof d);
-        }
-        DGroup& g = d.g[d.ng++];
-        g.wl = s.wl;
-        g.pull = 0;
-        g.f_begin = d.nf;
-        for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
-          DFold& f = d.f[d.nf++];
-          f.v = (uint32_t)v;
-          f.p = (uint32_t)folds[fi];
-          f.grad = nullptr;
-        }
-        g.f_end = d.nf;
-      } while (fi < folds.size());
+    const bool hold = strict && s.at_gate;
+    std::vector<int64_t> folds;
+    if (!pulled[v] && !hold) folds.swap(s.pending_folds);
+    if (d.nc == 0 && folds.empty()) continue;
+    if (xdep_[v]) {
+      cudaStreamWaitEvent(vs_[v], xdep_[v], 0);
+      xdep_[v] = nullptr;
     }
-    if (hp_status st = emit(d, rg.first, rg.second)) return st;
+    if (folds.size() == 1 && d.nc == 1 && (int64_t)d.c[0].p == folds[0]) {
+      d.c[0].flags |= kFoldInline;
+      d.c[0].wl = s.wl;
+      folds.clear();
+    }
+    size_t fi = 0;
+    while (fi < folds.size()) {
+      if (d.ng == kMaxG || d.nf == kMaxF) {
+        if (hp_status st = emit(d, s.a0, s.len, vs_[v])) return st;
+        memset(&d, 0, sizeof d);
+      }
+      DGroup& g = d.g[d.ng++];
+      g.wl = s.wl;
+      g.pull = 0;
+      g.f_begin = d.nf;
+      for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
+        DFold& f = d.f[d.nf++];
+        f.v = (uint32_t)v;
+        f.p = (uint32_t)folds[fi];
+        f.grad = nullptr;
+      }
+      g.f_end = d.nf;
+    }
+    if (hp_status st = emit(d, s.a0, s.len, vs_[v])) return st;
+    lastc_[v] = pool_event();
+    cudaEventRecord(lastc_[v], vs_[v]);
   }
-  // folds of VWs without a stage here are someone else's device work
-  for (int v = 0; v < N_; ++v)
-    if (!vw_[v].here && !pulled[v] && !(strict && vw_[v].at_gate)) vw_[v].pending_folds.clear();
-  // ---- 2. applies on this rank's PS shard -------------------------------
-  // the exchange stream starts after every local launch issued so far (the
-  // pushed u~ and the pulled VWs' w_local are complete on this rank)
-  if (!ba_.empty() || !bpull_.empty()) {
-    cudaEvent_t e = pool_event();
-    cudaEventRecord(e, stream_);
-    cudaStreamWaitEvent(xs_, e, 0);
-    x_pending_ = true;
-  }
+  // ---- 2. exchange stream: wait only for the producers it reads ------------
+  auto xs_wait = [&](int v) {
+    if (vw_[v].here && lastc_[v]) cudaStreamWaitEvent(xs_, lastc_[v], 0);
+  };
   if (!ba_.empty()) {
+    for (const BApply& a : ba_) xs_wait(a.v);
+    for (int v : bpull_) xs_wait(v);
     if (int e = comm_->barrier(xs_)) return fail(HP_ERR_COMM, comm_->error());
     size_t k = 0;
     while (k < ba_.size()) {
@@ -719,7 +706,7 @@ hp_status Engine::flush_dist() {
         d.na++;
         ++k;
       }
-      if (hp_status st = emit(d, begin_, n_, xs_)) return st;
+      if (hp_status st = emit(d, begin_, n_, xs_, xblocks_)) return st;
     }
     applied_ += (int64_t)ba_.size();
     if (int e = comm_->barrier(xs_)) return fail(HP_ERR_COMM, comm_->error());
@@ -727,61 +714,69 @@ hp_status Engine::flush_dist() {
     cudaEventRecord(e, xs_);
     for (const BApply& a : ba_)
       if (vw_[a.v].here) xdep_[a.v] = e;
+  } else {
+    for (int v : bpull_) xs_wait(v);
   }
-  // ---- 3. pulls -----------------------------------------------------------
-  for (auto& rg : ranges) {
+  // ---- 3. pulls --------------------------------------------------------------
+  for (int v : bpull_) {
+    VW& s = vw_[v];
+    if (!s.here) {
+      s.pending_folds.clear();
+      continue;
+    }
+    std::vector<int64_t> folds;
+    folds.swap(s.pending_folds);
     TickDesc d;
     memset(&d, 0, sizeof d);
-    for (int v : bpull_) {
-      VW& s = vw_[v];
-      if (!s.here || s.a0 != rg.first || s.len != rg.second) continue;
-      std::vector<int64_t> folds;
-      folds.swap(s.pending_folds);
-      size_t fi = 0;
-      bool first_part = true;
-      do {
-        if (d.ng == kMaxG || d.nf == kMaxF || d.ns + G_ > kMaxS) {
-          if (hp_status st = emit(d, rg.first, rg.second, xs_)) return st;
-          memset(&d, 0, sizeof d);
-        }
-        DGroup& g = d.g[d.ng++];
-        g.wl = s.wl;
-        g.partial = nullptr;
-        if (first_part) {
-          g.pull = 2;
-          g.seg_begin = d.ns;
-          add_segs(d, s.a0, s.len, false, 0, 0);
-          g.seg_end = d.ns;
-          if (!strict && s.acc_count > 0) g.partial = s.acc[s.c_local % R_];
-        } else {
-          g.pull = 0;
-        }
-        first_part = false;
-        g.f_begin = d.nf;
-        for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
-          DFold& f = d.f[d.nf++];
-          f.v = (uint32_t)v;
-          f.p = (uint32_t)folds[fi];
-          f.grad = nullptr;
-        }
-        g.f_end = d.nf;
-      } while (fi < folds.size());
-    }
-    if (hp_status st = emit(d, rg.first, rg.second, xs_)) return st;
-  }
-  if (!bpull_.empty()) {
-    cudaEvent_t e = pool_event();       // w_local of the pulled VWs is written
+    size_t fi = 0;
+    bool first_part = true;
+    do {
+      if (d.ng == kMaxG || d.nf == kMaxF || d.ns + G_ > kMaxS) {
+        if (hp_status st = emit(d, s.a0, s.len, xs_, xblocks_)) return st;
+        memset(&d, 0, sizeof d);
+      }
+      DGroup& g = d.g[d.ng++];
+      g.wl = s.wl;
+      g.partial = nullptr;
+      if (first_part) {
+        g.pull = 2;
+        g.seg_begin = d.ns;
+        add_segs(d, s.a0, s.len, false, 0, 0);
+        g.seg_end = d.ns;
+        if (!strict && s.acc_count > 0) g.partial = s.acc[s.c_local % R_];
+      } else {
+        g.pull = 0;
+      }
+      first_part = false;
+      g.f_begin = d.nf;
+      for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
+        DFold& f = d.f[d.nf++];
+        f.v = (uint32_t)v;
+        f.p = (uint32_t)folds[fi];
+        f.grad = nullptr;
+      }
+      g.f_end = d.nf;
+    } while (fi < folds.size());
+    if (hp_status st = emit(d, s.a0, s.len, xs_, xblocks_)) return st;
+    cudaEvent_t e = pool_event();       // w_local of v is written
     cudaEventRecord(e, xs_);
-    for (int v : bpull_)
-      if (vw_[v].here) xdep_[v] = e;
+    xdep_[v] = e;
   }
-  for (int v : bpull_)
-    if (!vw_[v].here) vw_[v].pending_folds.clear();
   bc_.clear();
   ba_.clear();
   bpull_.clear();
   phase_ = kNone;
   return HP_OK;
+}
+
+void Engine::fork_streams() {
+  if (forked_) return;
+  cudaEvent_t e = pool_event();
+  cudaEventRecord(e, stream_);
+  cudaStreamWaitEvent(xs_, e, 0);
+  for (int v = 0; v < N_; ++v)
+    if (vs_[v]) cudaStreamWaitEvent(vs_[v], e, 0);
+  forked_ = true;
 }
 
 cudaEvent_t Engine::pool_event() {
@@ -798,13 +793,22 @@ cudaEvent_t Engine::pool_event() {
   return e;
 }
 
+// The context stream waits for every side stream (all work issued so far is
+// ordered before anything later on the context stream, e.g. a timing event).
 hp_status Engine::join_exchange() {
-  if (!x_pending_) return HP_OK;
+  if (!dist_ || !forked_) return HP_OK;
   cudaEvent_t e = pool_event();
   cudaEventRecord(e, xs_);
   cudaStreamWaitEvent(stream_, e, 0);
+  for (int v = 0; v < N_; ++v) {
+    if (!vs_[v]) continue;
+    cudaEvent_t ev = pool_event();
+    cudaEventRecord(ev, vs_[v]);
+    cudaStreamWaitEvent(stream_, ev, 0);
+  }
   std::fill(xdep_.begin(), xdep_.end(), nullptr);
-  x_pending_ = false;
+  std::fill(lastc_.begin(), lastc_.end(), nullptr);
+  forked_ = false;
   return check_cuda(cudaGetLastError(), "join");
 }
 
@@ -836,6 +840,12 @@ hp_status Engine::connect(const void* handles, const void* comm_id) {
   if (!comm_) return fail(HP_ERR_COMM, err);
   if (int e = cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking)) return check_cuda(e, "stream");
   xdep_.assign(N_, nullptr);
+  lastc_.assign(N_, nullptr);
+  vs_.assign(N_, nullptr);
+  for (int v = 0; v < N_; ++v)
+    if (vw_[v].here)
+      if (int e = cudaStreamCreateWithFlags(&vs_[v], cudaStreamNonBlocking)) return check_cuda(e, "stream");
+  if (const char* xb = getenv("HP_XBLOCKS")) xblocks_ = atoi(xb);
   // everyone's init writes are complete before anyone reads a peer
   if (int e = comm_->barrier(stream_)) return fail(HP_ERR_COMM, comm_->error());
   return check_cuda(cudaStreamSynchronize(stream_), "connect sync");

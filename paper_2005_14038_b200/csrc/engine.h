@@ -113,7 +113,9 @@ class Engine {
   hp_status flush();
   hp_status flush_local();
   hp_status flush_dist();
-  hp_status emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st = nullptr);
+  hp_status emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st = nullptr,
+                 int max_blocks = 0);
+  void fork_streams();
   cudaEvent_t pool_event();
   hp_status join_exchange();          // compute stream waits for the exchange stream
   RankLayout layout_of(int q) const;
@@ -142,9 +144,12 @@ class Engine {
   // VWs whose buffers it touches.
   cudaStream_t xs_ = nullptr;
   std::vector<cudaEvent_t> xdep_;     // per VW: exchange op that last touched it
+  std::vector<cudaEvent_t> lastc_;    // per VW: its last accumulation launch
+  std::vector<cudaStream_t> vs_;      // per local VW: accumulation stream
+  bool forked_ = false;               // side streams ordered after the context stream
+  int xblocks_ = 0;                   // grid bound of exchange launches (HP_XBLOCKS)
   std::vector<cudaEvent_t> evpool_;
   size_t evnext_ = 0;
-  bool x_pending_ = false;            // exchange work not yet joined
   double nvl_bytes_ = 0;
   int N_, Nm_, R_;
   int64_t W_, last_p_, n_, begin_;

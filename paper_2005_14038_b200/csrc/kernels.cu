@@ -239,9 +239,10 @@ __global__ void init_kernel(float* out, int64_t n, int64_t param_begin, int w0_m
 
 int g_u_override = -1;   // HP_TICK_U: tuning override of chunks per thread
 int g_pdl = 1;           // HP_PDL=0 disables programmatic dependent launch
+int g_grid = 0;          // HP_GRID=1: one round of U chunks per thread (non-persistent)
 
 template <int GM, bool MOM, int U>
-int launch_u(const TickDesc& d, cudaStream_t s) {
+int launch_u(const TickDesc& d, cudaStream_t s, int max_blocks) {
   static int grid_max = 0;
   if (grid_max == 0) {
     int dev = 0, sms = 0, per_sm = 0;
@@ -251,8 +252,10 @@ int launch_u(const TickDesc& d, cudaStream_t s) {
     grid_max = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int64_t chunks = (d.n + 3) >> 2;
-  int64_t blocks = (chunks + 255) / 256;
-  if (blocks > grid_max) blocks = grid_max;
+  int64_t blocks = g_grid == 1 ? (chunks + 256 * U - 1) / (256 * U) : (chunks + 255) / 256;
+  if (g_grid != 1 && blocks > grid_max) blocks = grid_max;
+  if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
+  if (blocks > 0x7fffffff) blocks = 0x7fffffff;
   if (blocks < 1) blocks = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)blocks);
@@ -268,31 +271,33 @@ int launch_u(const TickDesc& d, cudaStream_t s) {
 }
 
 template <int GM, bool MOM>
-int launch_gm(const TickDesc& d, cudaStream_t s) {
+int launch_gm(const TickDesc& d, cudaStream_t s, int mb) {
   // Measured on B200 (profiles/): complete-only launches run best with 4 chunks
   // per thread; launches with pull groups (more ops per chunk, more Philox
   // folds) with 2, which keeps 3 CTAs/SM resident.
   int u = d.ng > 0 ? 2 : 4;
   if (g_u_override > 0) u = g_u_override;
-  if (u >= 4) return launch_u<GM, MOM, 4>(d, s);
-  return launch_u<GM, MOM, 2>(d, s);
+  if (u >= 4) return launch_u<GM, MOM, 4>(d, s, mb);
+  return launch_u<GM, MOM, 2>(d, s, mb);
 }
 
 }  // namespace
 
-int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream) {
+int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream, int mb) {
   cudaStream_t s = (cudaStream_t)stream;
   if (g_u_override == -1) {
     const char* e = getenv("HP_TICK_U");
     g_u_override = e ? atoi(e) : 0;
     const char* p = getenv("HP_PDL");
     g_pdl = p ? atoi(p) : 1;
+    const char* g = getenv("HP_GRID");
+    g_grid = g ? atoi(g) : 0;
   }
   if (d.n <= 0) return 0;
   switch (grad_mode) {
-    case 0: return momentum ? launch_gm<0, true>(d, s) : launch_gm<0, false>(d, s);
-    case 1: return momentum ? launch_gm<1, true>(d, s) : launch_gm<1, false>(d, s);
-    default: return momentum ? launch_gm<2, true>(d, s) : launch_gm<2, false>(d, s);
+    case 0: return momentum ? launch_gm<0, true>(d, s, mb) : launch_gm<0, false>(d, s, mb);
+    case 1: return momentum ? launch_gm<1, true>(d, s, mb) : launch_gm<1, false>(d, s, mb);
+    default: return momentum ? launch_gm<2, true>(d, s, mb) : launch_gm<2, false>(d, s, mb);
   }
 }
 

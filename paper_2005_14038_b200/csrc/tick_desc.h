@@ -110,7 +110,10 @@ inline int tick_streams(const TickDesc& d) {
 
 // Launch the fused tick kernel (kernels.cu). grad_mode: HP_GRAD_*.
 // Returns a cudaError_t as int.
-int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream);
+// max_blocks > 0 bounds the grid (exchange launches that share the GPU with
+// accumulation launches on other streams); 0 = default grid.
+int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream,
+                int max_blocks = 0);
 // out[i] = w0(param_begin + i) over the shard (kernels.cu, reading Z8).
 int launch_init(float* out, int64_t n, int64_t param_begin, int w0_mode, int grad_mode,
                 uint32_t key0, uint32_t key1, void* stream);

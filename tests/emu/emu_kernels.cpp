@@ -51,7 +51,7 @@ void app(const TickDesc& d, bool mom, float& wg, float& m, float ut) {
 
 }  // namespace
 
-int launch_tick(const TickDesc& d, int gm, bool mom, void*) {
+int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
   for (int64_t i = 0; i < d.n; ++i) {
     float wg = d.wg_load ? d.wg[i] : 0.f;
     float m = (mom && d.wg_store) ? d.m[i] : 0.f;
