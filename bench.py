@@ -183,6 +183,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-params", type=int, default=1 << 18)
     ap.add_argument("--merge-ticks", type=int, default=1)
+    ap.add_argument("--apply-mode", type=int, default=0,
+                    help="0: defer PS applies to the observing pull; 1: apply on arrival")
     ap.add_argument("--span", type=int, default=0,
                     help="N>1: GPUs per VW of the distributed placement (k<N exchanges over "
                          "NVLink); 0 = ED-local shards (no exchange)")
@@ -223,10 +225,11 @@ def main():
     placed = ws > 1 and args.span > 0
     if placed:
         ctx = hdist.placed_context(run_cfg, rank, ws, args.span, device=local,
-                                   stream=stream.cuda_stream, merge_ticks=args.merge_ticks)
+                                   stream=stream.cuda_stream, merge_ticks=args.merge_ticks,
+                                   apply_mode=args.apply_mode)
     else:
         ctx = hdist.rank_context(run_cfg, rank, ws, device=local, stream=stream.cuda_stream,
-                                 merge_ticks=args.merge_ticks)
+                                 merge_ticks=args.merge_ticks, apply_mode=args.apply_mode)
     ctx.trace_enable(False)
     ctx.schedule_begin(run_cfg.tau, run_cfg.latency())
     sampler = ClockSampler(local)
@@ -337,6 +340,7 @@ def main():
                    (f"distributed, {args.span} GPU(s) per VW, PS sharded over {ws}" if placed
                     else "ED-local shards" if ws > 1 else "single GPU"),
                    "grad": "Philox FLOAT in-kernel", "pull": "EAGER", "local": "STRICT",
+                   "apply": "on arrival" if args.apply_mode else "deferred to the observing pull",
                    "l2": "inputs larger than L2 (>= 13 x 230 MiB buffers per GPU)"},
         "images_per_sec_equiv": commits * 32 * cfg.Nm / (ms_max / 1e3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

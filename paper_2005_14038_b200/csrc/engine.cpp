@@ -414,6 +414,11 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
       const char* p = (const char*)(d.s[t].ptr + b);
       if (p < lo || p >= hi) remote += 4.0 * (double)(d.s[t].end - b);
     }
+  for (int t = d.wgs_begin; t < d.wgs_end && d.wg_load; ++t) {
+    const int64_t b = t == d.wgs_begin ? 0 : d.s[t - 1].end;
+    const char* p = (const char*)(d.s[t].ptr + b);
+    if (p < lo || p >= hi) remote += 4.0 * (double)(d.s[t].end - b);
+  }
   for (int g = 0; g < d.ng; ++g)
     if (d.g[g].pull == 2)
       for (int t = d.g[g].seg_begin; t < d.g[g].seg_end; ++t) {
@@ -717,50 +722,63 @@ hp_status Engine::flush_dist() {
   } else {
     for (int v : bpull_) xs_wait(v);
   }
-  // ---- 3. pulls --------------------------------------------------------------
+  // ---- 3. pulls: per local stage range one launch reads w_global from the
+  //      shard owners once (into registers) and writes every pulled w_local of
+  //      that range, each followed by its own due folds ----------------------
+  std::vector<std::pair<int64_t, int64_t>> pranges;
   for (int v : bpull_) {
     VW& s = vw_[v];
     if (!s.here) {
       s.pending_folds.clear();
       continue;
     }
-    std::vector<int64_t> folds;
-    folds.swap(s.pending_folds);
+    if (std::find(pranges.begin(), pranges.end(), std::make_pair(s.a0, s.len)) == pranges.end())
+      pranges.push_back({s.a0, s.len});
+  }
+  for (auto& rg : pranges) {
     TickDesc d;
-    memset(&d, 0, sizeof d);
-    size_t fi = 0;
-    bool first_part = true;
-    do {
-      if (d.ng == kMaxG || d.nf == kMaxF || d.ns + G_ > kMaxS) {
-        if (hp_status st = emit(d, s.a0, s.len, xs_, xblocks_)) return st;
-        memset(&d, 0, sizeof d);
-      }
-      DGroup& g = d.g[d.ng++];
-      g.wl = s.wl;
-      g.partial = nullptr;
-      if (first_part) {
-        g.pull = 2;
-        g.seg_begin = d.ns;
-        add_segs(d, s.a0, s.len, false, 0, 0);
-        g.seg_end = d.ns;
-        if (!strict && s.acc_count > 0) g.partial = s.acc[s.c_local % R_];
-      } else {
-        g.pull = 0;
-      }
-      first_part = false;
-      g.f_begin = d.nf;
-      for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
-        DFold& f = d.f[d.nf++];
-        f.v = (uint32_t)v;
-        f.p = (uint32_t)folds[fi];
-        f.grad = nullptr;
-      }
-      g.f_end = d.nf;
-    } while (fi < folds.size());
-    if (hp_status st = emit(d, s.a0, s.len, xs_, xblocks_)) return st;
-    cudaEvent_t e = pool_event();       // w_local of v is written
+    auto fresh = [&]() {
+      memset(&d, 0, sizeof d);
+      d.wgs_begin = d.ns;
+      add_segs(d, rg.first, rg.second, false, 0, 0);
+      d.wgs_end = d.ns;
+    };
+    fresh();
+    for (int v : bpull_) {
+      VW& s = vw_[v];
+      if (!s.here || s.a0 != rg.first || s.len != rg.second) continue;
+      std::vector<int64_t> folds;
+      folds.swap(s.pending_folds);
+      size_t fi = 0;
+      bool first_part = true;
+      do {
+        if (d.ng == kMaxG || d.nf == kMaxF) {
+          if (hp_status st = emit(d, rg.first, rg.second, xs_, xblocks_)) return st;
+          fresh();
+        }
+        DGroup& g = d.g[d.ng++];
+        g.wl = s.wl;
+        g.partial = nullptr;
+        g.pull = first_part ? 1 : 0;     // 1: base = the w_global registers
+        if (first_part && !strict && s.acc_count > 0) g.partial = s.acc[s.c_local % R_];
+        first_part = false;
+        g.f_begin = d.nf;
+        for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
+          DFold& f = d.f[d.nf++];
+          f.v = (uint32_t)v;
+          f.p = (uint32_t)folds[fi];
+          f.grad = nullptr;
+        }
+        g.f_end = d.nf;
+      } while (fi < folds.size());
+    }
+    if (hp_status st = emit(d, rg.first, rg.second, xs_, xblocks_)) return st;
+  }
+  if (!bpull_.empty()) {
+    cudaEvent_t e = pool_event();       // w_local of the pulled VWs is written
     cudaEventRecord(e, xs_);
-    xdep_[v] = e;
+    for (int v : bpull_)
+      if (vw_[v].here) xdep_[v] = e;
   }
   bc_.clear();
   ba_.clear();

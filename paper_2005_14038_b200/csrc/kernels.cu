@@ -124,7 +124,10 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
   }
   if (d.wg_load) {
 #pragma unroll
-    for (int x = 0; x < U; ++x) wg[x] = ld4<CNT>(d.wg, q0 + x * qs);
+    for (int x = 0; x < U; ++x) {
+      const int64_t q = q0 + x * qs;
+      wg[x] = ld4<CNT>(d.wgs_end > d.wgs_begin ? seg_ptr(d, d.wgs_begin, d.wgs_end, q) : d.wg, q);
+    }
   }
   if (MOM && d.wg_store) {
 #pragma unroll

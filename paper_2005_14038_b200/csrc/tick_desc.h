@@ -85,6 +85,8 @@ struct TickDesc {
   DFold f[kMaxF];
   DSeg s[kMaxS];
   int32_t ns;
+  int32_t wgs_begin, wgs_end;   // if non-empty: w_global registers are loaded from
+                                // these segments (remote shards) instead of wg
   int32_t pad2;
 };
 

@@ -53,7 +53,7 @@ void app(const TickDesc& d, bool mom, float& wg, float& m, float ut) {
 
 int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
   for (int64_t i = 0; i < d.n; ++i) {
-    float wg = d.wg_load ? d.wg[i] : 0.f;
+    float wg = !d.wg_load ? 0.f : d.wgs_end > d.wgs_begin ? seg(d, d.wgs_begin, d.wgs_end, i)[i] : d.wg[i];
     float m = (mom && d.wg_store) ? d.m[i] : 0.f;
     for (int k = 0; k < d.na; ++k) app(d, mom, wg, m, seg(d, d.a[k].seg_begin, d.a[k].seg_end, i)[i]);
     for (int j = 0; j < d.nc; ++j) {
