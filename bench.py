@@ -108,10 +108,25 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_baseline(cfg, params=1 << 21, rounds=4):
-    """The oracle as it stands (numpy, one thread) on a bounded sample of the
-    same workload: the first `params` params of the C2 schedule for `rounds`
-    rounds. Returns synced params/s of the sample."""
+def _oracle_chunk(job):
+    """One worker of the all-cores oracle timing: the oracle as it stands on the
+    param range [lo, hi) of the schedule (every op is element-wise in the param
+    index, SURVEY.md 8(c) "sampled parity", so ranges are independent)."""
+    import numpy as np
+    from oracle import run_schedule
+    cfg, lo, hi = job
+    t0 = time.time()
+    o = run_schedule(cfg, idx=np.arange(lo, hi))
+    return t0, time.time(), len(o.commit) if hasattr(o, "commit") else None
+
+
+def cpu_baseline(cfg, params=1 << 21, rounds=4, per_core=1 << 20, max_cores=64):
+    """The oracle as it stands (numpy) on a bounded sample of the same workload:
+    (1) one thread over the first `params` params of the schedule for `rounds`
+    rounds; (2) every host core, each process running the oracle on its own
+    `per_core`-param range of the same schedule. Returns synced params/s."""
+    import multiprocessing as mp
+
     import numpy as np
     from oracle import run_schedule
     c = cfg.replace(waves=rounds)
@@ -121,10 +136,22 @@ def cpu_baseline(cfg, params=1 << 21, rounds=4):
                  on_tick=lambda t, sm: marks.append((time.perf_counter(), len(sm.commit))))
     dt = time.perf_counter() - t0
     commits = marks[-1][1]
-    return {"value": commits * min(params, c.nparams) / dt, "unit": UNIT, "cores": 1,
-            "kind": "oracle",
-            "sample": f"{cfg.name} schedule on params [0,{min(params, c.nparams)}) for "
-                      f"{rounds} rounds ({commits} pushes), numpy single thread, {dt:.1f} s"}
+    one = commits * min(params, c.nparams) / dt
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    cores = max(1, min(cores, max_cores, c.nparams // per_core or 1))
+    jobs = [(c, k * per_core, min((k + 1) * per_core, c.nparams)) for k in range(cores)]
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_oracle_chunk, jobs)
+    span = max(r[1] for r in res) - min(r[0] for r in res)
+    allc = commits * sum(hi - lo for _, lo, hi in jobs) / span
+    return {"value": allc, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "value_1core": one,
+            "sample": f"{cfg.name} schedule, {rounds} rounds ({commits} pushes): all-cores = "
+                      f"{cores} processes x {per_core} params each ({span:.1f} s wall); "
+                      f"1 core = params [0,{min(params, c.nparams)}) ({dt:.1f} s), numpy"}
 
 
 def run_reference(args, cfg):
@@ -250,7 +277,24 @@ def main():
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
     kern_ms, kern_bytes, kern_launches = ctx.profile_read()
-    l_ms, l_bytes, l_shape = ctx.profile_launches()
+    l_ms, l_bytes, l_shape, l_sync, l_t0 = ctx.profile_launches()
+    # device time during which at least one tick kernel runs (union of the
+    # launch intervals: the distributed placements launch on several streams)
+    busy_ms, cur_a, cur_b = 0.0, None, None
+    for a, d in sorted(zip((float(x) for x in l_t0), (float(x) for x in l_ms))):
+        if cur_b is None or a > cur_b:
+            if cur_b is not None:
+                busy_ms += cur_b - cur_a
+            cur_a, cur_b = a, a + d
+        else:
+            cur_b = max(cur_b, a + d)
+    if cur_b is not None:
+        busy_ms += cur_b - cur_a
+    # sync-only time: each launch's device time attributed to synchronisation
+    # in proportion to its sync share of the algorithmic bytes (the push/apply/
+    # pull ops are fused with accumulation, so they have no launch of their own)
+    sync_ms = float(sum(float(t) * float(sy) / float(by)
+                        for t, by, sy in zip(l_ms, l_bytes, l_sync) if by > 0))
     mix = {}
     sync_us = []
     for t_ms, by, sh in zip(l_ms, l_bytes, l_shape):
@@ -267,10 +311,11 @@ def main():
                   for k, (n, t, b) in sorted(mix.items(), key=lambda kv: -kv[1][1])}
     st1 = ctx.stats()
     commits = st1.commits - st0.commits
-    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([ms, sync_ms], dtype=torch.float64, device=f"cuda:{local}")
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = float(t[0].item())
+    sync_ms_max = float(t[1].item())
     value = commits * cfg.nparams / (ms_max / 1e3)
     launches = st1.launches - st0.launches
     nvl = torch.tensor([st1.nvl_bytes - st0.nvl_bytes], dtype=torch.float64, device=f"cuda:{local}")
@@ -330,7 +375,9 @@ def main():
         return 0
 
     peak, peak_kind = _peaks()
-    achieved = kern_bytes / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else 0.0
+    # algorithmic bytes over the time some tick kernel is running (= the sum of
+    # launch durations on one stream; the union of intervals across streams)
+    achieved = kern_bytes / (busy_ms / 1e3) / 1e9 if busy_ms > 0 else 0.0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -343,10 +390,16 @@ def main():
                    "apply": "on arrival" if args.apply_mode else "deferred to the observing pull",
                    "l2": "inputs larger than L2 (>= 13 x 230 MiB buffers per GPU)"},
         "images_per_sec_equiv": commits * 32 * cfg.Nm / (ms_max / 1e3),
+        "sync_only": ({"value": commits * cfg.nparams / (sync_ms_max / 1e3), "unit": UNIT,
+                       "ms_per_step": sync_ms_max / args.steps,
+                       "def": "push+apply+pull only: each launch's device time attributed to "
+                              "synchronisation by its share of algorithmic bytes (w_global/m, "
+                              "u~ reads, pull writes); max over ranks"}
+                      if sync_ms_max > 0 else None),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _ncu_traffic(cfg.name),
                      "peak_kind": peak_kind, "kernel": "hp::tick_kernel (all launches)",
-                     "kernel_ms": kern_ms, "launches": kern_launches,
+                     "kernel_ms": kern_ms, "busy_ms": busy_ms, "launches": kern_launches,
                      "alg_bytes_per_launch": kern_bytes / max(kern_launches, 1)},
         "nvlink": {"bytes_per_step_max_rank": nvl_bytes_max / args.steps,
                    "GBps_over_step": nvl_bytes_max / (ms_max / 1e3) / 1e9,
@@ -356,7 +409,7 @@ def main():
              "n": len(sync_us),
              "def": "device time of each launch that applies pushed waves or pulls "
                     "(push -> apply -> pull of a round, fused)"} if sync_us else None),
-        "kernel_share_of_step": kern_ms / ms if ms > 0 else None,
+        "kernel_share_of_step": busy_ms / ms if ms > 0 else None,
         "launch_mix": launch_mix,
         "gpu_launches": launches,
         "clocks": clocks,

@@ -213,9 +213,15 @@ hp_status hp_profile_read(hp_ctx* ctx, double* kernel_ms, double* alg_bytes,
 /* Per-launch detail of the same window, up to max records: duration (ms),
    algorithmic bytes, and shape = nc | ni<<4 | na<<8 | ng<<16 | nf<<24 | pull<<31
    (completes, inline folds, memory applies, w_local groups, group folds, and
-   whether a pull is in the fused launch). *n = records written. */
+   whether a pull is in the fused launch), and sync_bytes = the part of
+   alg_bytes that is synchronisation (w_global/m traffic, u~ reads of the
+   applies, pull writes of w_local; the rest is wave accumulation and folds).
+   start_ms = the launch's start relative to the first profiled launch (launches
+   of the distributed placements run on several streams and overlap).
+   Any output pointer may be NULL. *n = records written. */
 hp_status hp_profile_launches(hp_ctx* ctx, int64_t max, float* ms, double* alg_bytes,
-                              int32_t* shape, int64_t* n);
+                              int32_t* shape, double* sync_bytes, float* start_ms,
+                              int64_t* n);
 
 /* Closed forms of section 5 (no context needed). */
 int64_t hp_s_global(int32_t Nm, int32_t D);                  /* (D+1)*Nm + Nm - 2 */

@@ -384,9 +384,10 @@ hp_status hp_profile_read(hp_ctx* ctx, double* kernel_ms, double* alg_bytes, int
 }
 
 hp_status hp_profile_launches(hp_ctx* ctx, int64_t max, float* ms, double* alg_bytes,
-                              int32_t* shape, int64_t* n) {
+                              int32_t* shape, double* sync_bytes, float* start_ms,
+                              int64_t* n) {
   HP_ENTRY(ctx)
-  return ctx->eng->profile_launches(max, ms, alg_bytes, shape, n);
+  return ctx->eng->profile_launches(max, ms, alg_bytes, shape, sync_bytes, start_ms, n);
   HP_EXIT(ctx)
 }
 

@@ -444,6 +444,7 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
     prof_bytes_ += bytes;
     prof_launches_++;
     prof_launch_bytes_.push_back(bytes);
+    prof_launch_sync_.push_back(4.0 * (double)n * tick_sync_streams(d));
     int inl = 0;
     for (int j = 0; j < d.nc; ++j) inl += (d.c[j].flags & kFoldInline) ? 1 : 0;
     int pulls = 0;
@@ -925,12 +926,13 @@ hp_status Engine::profile_enable(bool on) {
   prof_bytes_ = 0;
   prof_launches_ = 0;
   prof_launch_bytes_.clear();
+  prof_launch_sync_.clear();
   prof_launch_shape_.clear();
   return HP_OK;
 }
 
 hp_status Engine::profile_launches(int64_t max, float* ms, double* bytes, int32_t* shape,
-                                   int64_t* n) {
+                                   double* sync_bytes, float* start_ms, int64_t* n) {
   if (sticky_) return sticky_;
   if (hp_status st = join_exchange()) return st;
   if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "profile sync")) return st;
@@ -941,6 +943,12 @@ hp_status Engine::profile_launches(int64_t max, float* ms, double* bytes, int32_
     if (ms) ms[i] = t;
     if (bytes) bytes[i] = prof_launch_bytes_[i];
     if (shape) shape[i] = prof_launch_shape_[i];
+    if (sync_bytes) sync_bytes[i] = prof_launch_sync_[i];
+    if (start_ms) {   // launch start relative to the first profiled launch (any stream)
+      float t0 = 0;
+      if (int e = cudaEventElapsedTime(&t0, ev_[0], ev_[2 * i])) return check_cuda(e, "elapsed");
+      start_ms[i] = t0;
+    }
   }
   if (n) *n = cnt;
   return HP_OK;

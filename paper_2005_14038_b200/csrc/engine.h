@@ -92,7 +92,8 @@ class Engine {
   void stats(hp_stats* out) const;
   hp_status profile_enable(bool on);
   hp_status profile_read(double* ms, double* bytes, int64_t* launches);
-  hp_status profile_launches(int64_t max, float* ms, double* bytes, int32_t* shape, int64_t* n);
+  hp_status profile_launches(int64_t max, float* ms, double* bytes, int32_t* shape,
+                             double* sync_bytes, float* start_ms, int64_t* n);
   int64_t ticks = 0;
 
  private:
@@ -178,6 +179,7 @@ class Engine {
   size_t ev_used_ = 0;
   double prof_bytes_ = 0;
   std::vector<double> prof_launch_bytes_;
+  std::vector<double> prof_launch_sync_;
   std::vector<int32_t> prof_launch_shape_;
   int64_t prof_launches_ = 0;
 

@@ -110,6 +110,18 @@ inline int tick_streams(const TickDesc& d) {
   return s;
 }
 
+// The synchronisation share of tick_streams(): w_global load/store, momentum,
+// memory-sourced applies (the u~ reads of a4/a5) and the pull writes of w_local
+// (a7, plus the AT_LEAST partial). The rest is accumulation (a2/a3).
+inline int tick_sync_streams(const TickDesc& d) {
+  int s = d.wg_load + (d.wg_store ? 1 : 0);
+  if (d.m && d.wg_store) s += 2;
+  s += d.na;
+  for (int g = 0; g < d.ng; ++g)
+    if (d.g[g].pull) s += 1 + (d.g[g].pull == 2 ? 1 : 0) + (d.g[g].partial ? 1 : 0);
+  return s;
+}
+
 // Launch the fused tick kernel (kernels.cu). grad_mode: HP_GRAD_*.
 // Returns a cudaError_t as int.
 // max_blocks > 0 bounds the grid (exchange launches that share the GPU with

@@ -78,7 +78,8 @@ EXPORTS = {
     "hp_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                   C.POINTER(C.c_int64)]),
     "hp_profile_launches": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
-                                      C.c_void_p, C.POINTER(C.c_int64)]),
+                                      C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.POINTER(C.c_int64)]),
     "hp_s_global": (C.c_int64, [C.c_int32, C.c_int32]),
     "hp_version_floor": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
     "hp_last_error": (C.c_char_p, [C.c_void_p]),
@@ -280,12 +281,16 @@ def _profile_launches(self, max_records: int = 1 << 16):
     ms = np.zeros(max_records, dtype=np.float32)
     by = np.zeros(max_records, dtype=np.float64)
     sh = np.zeros(max_records, dtype=np.int32)
+    sy = np.zeros(max_records, dtype=np.float64)
+    t0 = np.zeros(max_records, dtype=np.float32)
     n = C.c_int64()
     self._chk(self.lib.hp_profile_launches(self.h, max_records, ms.ctypes.data_as(C.c_void_p),
                                            by.ctypes.data_as(C.c_void_p),
-                                           sh.ctypes.data_as(C.c_void_p), C.byref(n)))
+                                           sh.ctypes.data_as(C.c_void_p),
+                                           sy.ctypes.data_as(C.c_void_p),
+                                           t0.ctypes.data_as(C.c_void_p), C.byref(n)))
     k = n.value
-    return ms[:k], by[:k], sh[:k]
+    return ms[:k], by[:k], sh[:k], sy[:k], t0[:k]
 
 
 Context.profile_launches = _profile_launches
