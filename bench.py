@@ -212,12 +212,21 @@ def main():
     ap.add_argument("--merge-ticks", type=int, default=1)
     ap.add_argument("--apply-mode", type=int, default=0,
                     help="0: defer PS applies to the observing pull; 1: apply on arrival")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl", "nvls"],
+                    help="exchange of lockstep batches (distributed placements; include/hetpipe.h "
+                         "HP_XPORT_*): peer = fused NVLink loads, nccl = reduce-scatter/all-gather "
+                         "baseline, nvls = multimem through the NVSwitch")
+    ap.add_argument("--num-vw", type=int, default=0,
+                    help="override the config's VW count (C5E defaults to one VW per GPU)")
     ap.add_argument("--span", type=int, default=0,
                     help="N>1: GPUs per VW of the distributed placement (k<N exchanges over "
                          "NVLink); 0 = ED-local shards (no exchange)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
+    nvw = args.num_vw or (int(os.environ.get("WORLD_SIZE", "1")) if cfg.name == "C5E" else 0)
+    if nvw:
+        cfg = cfg.replace(num_vw=nvw, tau=tuple((list(cfg.tau) * 8)[:nvw]))
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -250,10 +259,16 @@ def main():
     stream = torch.cuda.Stream(local)          # a real stream: the library launches on it
     torch.cuda.set_stream(stream)              # and the timing events below record on it
     placed = ws > 1 and args.span > 0
-    if placed:
+    keep = None
+    xport = {"peer": 0, "nccl": 1, "nvls": 2}[args.transport]
+    if placed and args.transport == "nvls":
+        ctx, keep = hdist.symmetric_context(run_cfg, rank, ws, args.span, device=local,
+                                            stream=stream.cuda_stream, merge_ticks=args.merge_ticks,
+                                            apply_mode=args.apply_mode, transport=xport)
+    elif placed:
         ctx = hdist.placed_context(run_cfg, rank, ws, args.span, device=local,
                                    stream=stream.cuda_stream, merge_ticks=args.merge_ticks,
-                                   apply_mode=args.apply_mode)
+                                   apply_mode=args.apply_mode, transport=xport)
     else:
         ctx = hdist.rank_context(run_cfg, rank, ws, device=local, stream=stream.cuda_stream,
                                  merge_ticks=args.merge_ticks, apply_mode=args.apply_mode)
@@ -301,6 +316,8 @@ def main():
         sh = int(sh) & 0xFFFFFFFF
         key = (f"c{sh & 15}i{(sh >> 4) & 15}a{(sh >> 8) & 255}g{(sh >> 16) & 255}"
                f"f{(sh >> 24) & 127}")
+        if (sh >> 24) & 127 == 127:
+            key = "nccl_reduce_scatter" if (sh >> 8) & 255 else "nccl_all_gather"
         if sh >> 31 or (sh >> 8) & 255:
             sync_us.append(1e3 * float(t_ms))
         e = mix.setdefault(key, [0, 0.0, 0.0])
@@ -323,8 +340,9 @@ def main():
         dist.all_reduce(nvl, op=dist.ReduceOp.MAX)
     nvl_bytes_max = float(nvl.item())
     sync_waits = [int(x) for x in st1.wait_ticks[:N]]
+    lock_batches = st1.lockstep_batches - st0.lockstep_batches
     ctx.close()
-    del ctx
+    del ctx, keep
     torch.cuda.empty_cache()
 
     # ---------------- e2e: host gradients in, w_global out, through the C-ABI
@@ -388,6 +406,8 @@ def main():
                     else "ED-local shards" if ws > 1 else "single GPU"),
                    "grad": "Philox FLOAT in-kernel", "pull": "EAGER", "local": "STRICT",
                    "apply": "on arrival" if args.apply_mode else "deferred to the observing pull",
+                   "transport": args.transport if placed else None,
+                   "lockstep_batches": lock_batches if placed else None,
                    "l2": "inputs larger than L2 (>= 13 x 230 MiB buffers per GPU)"},
         "images_per_sec_equiv": commits * 32 * cfg.Nm / (ms_max / 1e3),
         "sync_only": ({"value": commits * cfg.nparams / (sync_ms_max / 1e3), "unit": UNIT,

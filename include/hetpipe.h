@@ -65,6 +65,24 @@ enum { HP_W0_ZERO = 0, HP_W0_PHILOX = 1 };
 enum { HP_PULL_EAGER = 0, HP_PULL_LAZY = 1 };
 enum { HP_LOCAL_STRICT = 0, HP_LOCAL_AT_LEAST = 1 };
 enum { HP_APPLY_DEFERRED = 0, HP_APPLY_ON_ARRIVAL = 1 };
+/* Exchange of a LOCKSTEP batch (world > 1, one full-replica VW per GPU (N = G,
+   vw_span 1), SGD, every VW pushing the same wave and pulling in one batch, as
+   in D = 0 with equal speeds); every other batch uses PEER:
+     PEER  each PS shard owner reads every pushed u~ slice from the GPU that
+           holds it inside the apply kernel (NVLink loads, commit order,
+           bit-exact), pulls read the w_global shards the same way;
+     NCCL  u~ summed per shard by NCCL (grouped ncclReduce, one root per shard =
+           reduce-scatter with uneven shards), applied by the owner, w_global
+           shards broadcast into every w_local (grouped ncclBroadcast =
+           all-gather): the unfused baseline;
+     NVLS  one kernel per owner: multimem.ld_reduce of the shard range of every
+           GPU's acc slot (the NVSwitch sums), w_global += sum, multimem.st of
+           the result into every GPU's w_local (needs the symmetric arena of
+           hp_connect_symmetric with a multicast mapping).
+   NCCL and NVLS apply the wave's N updates as ONE sum (switch / NCCL order), so
+   they match the sequential commit-order apply within rounding (reading Z15,
+   normwise <= 1e-5), not bit-exactly; the trace is identical. */
+enum { HP_XPORT_PEER = 0, HP_XPORT_NCCL = 1, HP_XPORT_NVLS = 2 };
 
 typedef struct {
   int32_t num_vw;          /* N virtual workers, 1..8 */
@@ -93,6 +111,13 @@ typedef struct {
                               no exchange); k < G exchanges over NVLink. */
   int32_t device;          /* CUDA device ordinal */
   void* stream;            /* cudaStream_t to run on; NULL = library-owned stream */
+  int32_t transport;       /* HP_XPORT_* (world > 1): exchange of lockstep batches */
+  int32_t reserved;
+  void* arena;             /* optional caller-owned device arena of >= hp_arena_bytes()
+                              bytes, 256-byte aligned, BORROWED for the context's
+                              lifetime (e.g. a torch symmetric-memory buffer whose peer
+                              and multicast mappings go to hp_connect_symmetric);
+                              NULL = the library allocates it */
 } hp_config;
 
 /* Fill cfg with defaults (N=1, Nm=1, D=0, lr=0.01, FLOAT grads, PHILOX w0,
@@ -111,6 +136,17 @@ void hp_config_default(hp_config* cfg);
 hp_status hp_comm_unique_id(void* out128);
 hp_status hp_ipc_handle(hp_ctx* ctx, void* out64);
 hp_status hp_connect(hp_ctx* ctx, const void* handles, const void* comm_id);
+/* Device bytes of this rank's arena for cfg (the same on every rank of a
+   placement whose ranks hold congruent VW sets, e.g. one VW per GPU); < 0 on a
+   bad config. */
+int64_t hp_arena_bytes(const hp_config* cfg);
+/* As hp_connect, for a context whose cfg.arena is a symmetric allocation:
+   peer_bases[q] (world entries, q = rank is this arena) is rank q's arena mapped
+   into this process, mc_base the multicast mapping of the arenas (NULL if none;
+   HP_XPORT_NVLS needs it). No CUDA IPC is used. Errors: HP_ERR_STATE (not
+   world > 1, no external arena, or already connected), HP_ERR_COMM. */
+hp_status hp_connect_symmetric(hp_ctx* ctx, const void* const* peer_bases, void* mc_base,
+                               const void* comm_id);
 
 /* north_star entry point: hp_init(num_vw, Nm, D, nparams, lr) with the other
    fields at their defaults. Allocates ~ (N*(1+R) + 1 (+1 momentum)) * 4 * P
@@ -201,7 +237,11 @@ typedef struct {
   double alg_bytes;         /* algorithmic HBM bytes of all launches */
   int64_t wait_ticks[8];    /* per VW simulated wait */
   int64_t pulls[8];         /* per VW pulls */
-  double nvl_bytes;         /* bytes this rank's kernels read from peer GPUs */
+  double nvl_bytes;         /* NVLink ingress bytes of this rank's exchange (algorithmic:
+                               PEER = its kernels' reads from peer GPUs; NVLS = the
+                               switch's reduced u~ + the w_local multicast stores it
+                               receives; NCCL = the data the collectives deliver) */
+  int64_t lockstep_batches; /* batches exchanged by the NCCL / NVLS transport */
 } hp_stats;
 hp_status hp_get_stats(hp_ctx* ctx, hp_stats* out);
 
@@ -213,7 +253,9 @@ hp_status hp_profile_read(hp_ctx* ctx, double* kernel_ms, double* alg_bytes,
 /* Per-launch detail of the same window, up to max records: duration (ms),
    algorithmic bytes, and shape = nc | ni<<4 | na<<8 | ng<<16 | nf<<24 | pull<<31
    (completes, inline folds, memory applies, w_local groups, group folds, and
-   whether a pull is in the fused launch), and sync_bytes = the part of
+   whether a pull is in the fused launch; nf = 127 marks an NCCL collective of
+   HP_XPORT_NCCL: na = 1 the reduce-scatter, ng = 1 the all-gather), and
+   sync_bytes = the part of
    alg_bytes that is synchronisation (w_global/m traffic, u~ reads of the
    applies, pull writes of w_local; the rest is wave accumulation and folds).
    start_ms = the launch's start relative to the first profiled launch (launches

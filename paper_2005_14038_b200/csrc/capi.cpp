@@ -156,12 +156,15 @@ void hp_config_default(hp_config* c) {
   c->vw_span = 1;
   c->device = 0;
   c->stream = nullptr;
+  c->transport = HP_XPORT_PEER;
+  c->reserved = 0;
+  c->arena = nullptr;
 }
 
-hp_status hp_init_ex(hp_ctx** out, const hp_config* cfg_in) {
-  if (!out || !cfg_in) return HP_ERR_INVALID;
-  *out = nullptr;
-  hp_config cfg = *cfg_in;
+}  // extern "C"
+
+namespace {
+const char* validate(hp_config& cfg) {
   if (cfg.param_count < 0) cfg.param_count = cfg.nparams - cfg.param_begin;
   const char* bad = nullptr;
   if (cfg.num_vw < 1 || cfg.num_vw > 8) bad = "num_vw must be 1..8";
@@ -183,6 +186,31 @@ hp_status hp_init_ex(hp_ctx** out, const hp_config* cfg_in) {
   else if (cfg.world > 1 && (cfg.param_begin != 0 || cfg.param_count != cfg.nparams))
     bad = "world > 1 places the whole model: param_begin 0, param_count -1";
   else if (cfg.world > 1 && cfg.grad_mode == HP_GRAD_EXTERNAL) bad = "EXTERNAL gradients need world 1";
+  else if (cfg.transport < 0 || cfg.transport > 2) bad = "bad transport";
+  return bad;
+}
+}  // namespace
+
+extern "C" {
+
+int64_t hp_arena_bytes(const hp_config* cfg_in) {
+  if (!cfg_in) return -1;
+  hp_config cfg = *cfg_in;
+  if (validate(cfg)) return -1;
+  try {
+    hp::Engine e(cfg);
+    e.plan_layout();
+    return e.arena_bytes();
+  } catch (...) {
+    return -1;
+  }
+}
+
+hp_status hp_init_ex(hp_ctx** out, const hp_config* cfg_in) {
+  if (!out || !cfg_in) return HP_ERR_INVALID;
+  *out = nullptr;
+  hp_config cfg = *cfg_in;
+  const char* bad = validate(cfg);
   if (bad) {
     g_init_error = bad;
     return HP_ERR_INVALID;
@@ -284,6 +312,14 @@ hp_status hp_connect(hp_ctx* ctx, const void* handles, const void* comm_id) {
   HP_ENTRY(ctx)
   if (!handles || !comm_id) return ctx->eng->fail(HP_ERR_INVALID, "NULL handles or id");
   return ctx->eng->connect(handles, comm_id);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_connect_symmetric(hp_ctx* ctx, const void* const* peer_bases, void* mc_base,
+                               const void* comm_id) {
+  HP_ENTRY(ctx)
+  if (!peer_bases || !comm_id) return ctx->eng->fail(HP_ERR_INVALID, "NULL peer_bases or id");
+  return ctx->eng->connect_symmetric(peer_bases, mc_base, comm_id);
   HP_EXIT(ctx)
 }
 

@@ -3,10 +3,12 @@
 // with dlopen so the library uses the NCCL the process already has) and CUDA
 // IPC for mapping every peer's arena (one process per GPU).
 //
-// The data itself never goes through NCCL: the tick kernels read remote acc
-// slices (push) and remote w_global shards (pull) through the mapped peer
-// pointers over NVLink; the barrier only orders those reads against the
-// producers (PAPER.md P:928-930 push/apply, P:949 pull).
+// Under HP_XPORT_PEER / NVLS the data never goes through NCCL: the tick
+// kernels read remote acc slices (push) and remote w_global shards (pull)
+// through the mapped peer pointers (or the multicast mapping) over NVLink; the
+// barrier only orders those accesses against the producers (PAPER.md P:928-930
+// push/apply, P:949 pull). HP_XPORT_NCCL, the unfused baseline, moves lockstep
+// batches with the two grouped collectives below.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -23,6 +25,15 @@ class Comm {
   // Device-side barrier on `stream`: later work on the stream runs only after
   // every rank's stream reached its own barrier call. Returns 0 or an error.
   virtual int barrier(cudaStream_t stream) = 0;
+  // Reduce-scatter with uneven shards: shard q = [b[q], b[q+1]) of every
+  // rank's `send` (fp32, indexed from 0) is summed into rank q's `recv`
+  // (b[q+1]-b[q] floats). One ncclReduce per shard in one group.
+  virtual int reduce_scatter_v(const float* send, float* recv, const int64_t* b,
+                               cudaStream_t stream) = 0;
+  // All-gather with uneven shards: rank q's `send` (its shard) lands at
+  // recv + b[q] on every rank. One ncclBroadcast per shard in one group.
+  virtual int all_gather_v(const float* send, float* recv, const int64_t* b,
+                           cudaStream_t stream) = 0;
   virtual std::string error() const = 0;
 };
 

@@ -17,7 +17,7 @@ typedef struct ncclComm* ncclComm_t;
 struct ncclUniqueId {
   char internal[kCommIdBytes];
 };
-enum { ncclInt32 = 2, ncclSum = 0 };
+enum { ncclInt32 = 2, ncclFloat32 = 7, ncclSum = 0 };
 
 struct Api {
   void* h = nullptr;
@@ -25,6 +25,10 @@ struct Api {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -53,7 +57,12 @@ Api* api(std::string* err) {
   a.AllReduce = (decltype(a.AllReduce))dlsym(a.h, "ncclAllReduce");
   a.CommDestroy = (decltype(a.CommDestroy))dlsym(a.h, "ncclCommDestroy");
   a.GetErrorString = (decltype(a.GetErrorString))dlsym(a.h, "ncclGetErrorString");
-  if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.CommDestroy) {
+  a.Reduce = (decltype(a.Reduce))dlsym(a.h, "ncclReduce");
+  a.Broadcast = (decltype(a.Broadcast))dlsym(a.h, "ncclBroadcast");
+  a.GroupStart = (decltype(a.GroupStart))dlsym(a.h, "ncclGroupStart");
+  a.GroupEnd = (decltype(a.GroupEnd))dlsym(a.h, "ncclGroupEnd");
+  if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.CommDestroy || !a.Reduce ||
+      !a.Broadcast || !a.GroupStart || !a.GroupEnd) {
     a.h = nullptr;
     if (err) *err = "libnccl.so.2 lacks required symbols";
     return nullptr;
@@ -63,7 +72,8 @@ Api* api(std::string* err) {
 
 class NcclComm : public Comm {
  public:
-  NcclComm(Api* a, ncclComm_t c, int* scratch) : a_(a), c_(c), scratch_(scratch) {}
+  NcclComm(Api* a, ncclComm_t c, int* scratch, int world, int rank)
+      : a_(a), c_(c), scratch_(scratch), world_(world), rank_(rank) {}
   ~NcclComm() override {
     if (c_) a_->CommDestroy(c_);
     if (scratch_) cudaFree(scratch_);
@@ -73,12 +83,34 @@ class NcclComm : public Comm {
     if (r != 0) err_ = a_->GetErrorString ? a_->GetErrorString(r) : "ncclAllReduce failed";
     return r;
   }
+  int reduce_scatter_v(const float* send, float* recv, const int64_t* b,
+                       cudaStream_t s) override {
+    ncclResult_t r = a_->GroupStart();
+    for (int q = 0; q < world_ && r == 0; ++q)
+      r = a_->Reduce(send + b[q], q == rank_ ? recv : nullptr, (size_t)(b[q + 1] - b[q]),
+                     ncclFloat32, ncclSum, q, c_, s);
+    const ncclResult_t r2 = a_->GroupEnd();
+    return note(r ? r : r2, "ncclReduce (reduce-scatter)");
+  }
+  int all_gather_v(const float* send, float* recv, const int64_t* b, cudaStream_t s) override {
+    ncclResult_t r = a_->GroupStart();
+    for (int q = 0; q < world_ && r == 0; ++q)
+      r = a_->Broadcast(q == rank_ ? send : nullptr, recv + b[q], (size_t)(b[q + 1] - b[q]),
+                        ncclFloat32, q, c_, s);
+    const ncclResult_t r2 = a_->GroupEnd();
+    return note(r ? r : r2, "ncclBroadcast (all-gather)");
+  }
   std::string error() const override { return err_; }
 
  private:
+  int note(ncclResult_t r, const char* what) {
+    if (r != 0) err_ = std::string(what) + ": " + (a_->GetErrorString ? a_->GetErrorString(r) : "");
+    return r;
+  }
   Api* a_;
   ncclComm_t c_;
   int* scratch_;
+  int world_, rank_;
   std::string err_;
 };
 
@@ -115,7 +147,7 @@ Comm* comm_create(const void* id, int world, int rank, std::string* err) {
     return nullptr;
   }
   cudaMemset(scratch, 0, 2 * sizeof(int));
-  return new NcclComm(a, c, scratch);
+  return new NcclComm(a, c, scratch, world, rank);
 }
 
 }  // namespace hp

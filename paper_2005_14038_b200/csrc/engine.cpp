@@ -54,12 +54,21 @@ RankLayout Engine::layout_of(int q) const {
   L.has.assign(N_, 0);
   L.wl_off.assign(N_, 0);
   L.acc_off.assign(N_, std::vector<size_t>(R_, 0));
+  // the shard regions are sized for the largest shard, so ranks holding
+  // congruent VW sets have identical offsets (the multicast mapping of NVLS
+  // addresses the same offset on every GPU)
+  int64_t smax = 0;
+  for (int r = 0; r < G_; ++r) smax = std::max(smax, shard_b_[r + 1] - shard_b_[r]);
   size_t off = 0;
   L.wg_off = off;
-  off += align256(L.s1 - L.s0);
+  off += align256(smax);
   if (cfg_.momentum != 0.f) {
     L.m_off = off;
-    off += align256(L.s1 - L.s0);
+    off += align256(smax);
+  }
+  if (cfg_.transport == HP_XPORT_NCCL && G_ > 1) {
+    L.x_off = off;
+    off += align256(smax);
   }
   for (int v = 0; v < N_; ++v) {
     for (int j = 0; j < span_; ++j) {
@@ -87,7 +96,7 @@ Engine::~Engine() {
     if (v) cudaStreamDestroy(v);
   for (void* p : opened_) cudaIpcCloseMemHandle(p);
   for (auto e : ev_) cudaEventDestroy(e);
-  if (arena_) cudaFree(arena_);
+  if (arena_ && !ext_arena_) cudaFree(arena_);
   for (auto& v : vw_)
     for (float* g : v.grad_ring) cudaFree(g);
   if (own_stream_ && stream_) cudaStreamDestroy(stream_);
@@ -106,6 +115,19 @@ hp_status Engine::check_cuda(int err, const char* what) {
   return fail(HP_ERR_CUDA, buf);
 }
 
+void Engine::plan_layout() {
+  if (dist_) {
+    shard_b_ = even_bounds(cfg_.nparams, G_);
+    stage_b_ = even_bounds(cfg_.nparams, span_);
+  } else {
+    shard_b_ = {begin_, begin_ + n_};
+    stage_b_ = {begin_, begin_ + n_};
+    G_ = 1;
+    span_ = 1;
+    rank_ = 0;
+  }
+}
+
 hp_status Engine::init() {
   if (cudaSetDevice(cfg_.device) != cudaSuccess) return check_cuda(cudaGetLastError(), "cudaSetDevice");
   if (cfg_.stream) {
@@ -117,19 +139,14 @@ hp_status Engine::init() {
   // arena: w_global, [m], per VW w_local + R acc slots; each 256-byte aligned.
   // Single-rank contexts own [param_begin, +param_count) of every buffer; with
   // world > 1 the placement layout decides (layout_of).
-  if (dist_) {
-    shard_b_ = even_bounds(cfg_.nparams, G_);
-    stage_b_ = even_bounds(cfg_.nparams, span_);
-  } else {
-    shard_b_ = {begin_, begin_ + n_};
-    stage_b_ = {begin_, begin_ + n_};
-    G_ = 1;
-    span_ = 1;
-    rank_ = 0;
-  }
+  plan_layout();
   for (int q = 0; q < G_; ++q) lay_.push_back(layout_of(q));
   const RankLayout& L = lay_[rank_];
-  if (cudaMalloc(&arena_, L.bytes) != cudaSuccess) {
+  if (cfg_.arena) {
+    if ((uintptr_t)cfg_.arena & 255) return fail(HP_ERR_INVALID, "arena not 256-byte aligned");
+    arena_ = cfg_.arena;
+    ext_arena_ = true;
+  } else if (cudaMalloc(&arena_, L.bytes) != cudaSuccess) {
     cudaGetLastError();
     arena_ = nullptr;
     return fail(HP_ERR_OOM, "device arena allocation failed");
@@ -426,36 +443,41 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
         const char* p = (const char*)(d.s[t].ptr + b);
         if (p < lo || p >= hi) remote += 4.0 * (double)(d.s[t].end - b);
       }
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (prof_on_) {
-    while (ev_.size() < ev_used_ + 2) {
-      cudaEvent_t e;
-      if (int err = cudaEventCreate(&e)) return check_cuda(err, "event");
-      ev_.push_back(e);
-    }
-    e0 = ev_[ev_used_];
-    e1 = ev_[ev_used_ + 1];
-    ev_used_ += 2;
-    cudaEventRecord(e0, st);
-  }
+  prof_begin(st);
   int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, st, max_blocks);
-  if (prof_on_) {
-    cudaEventRecord(e1, st);
-    prof_bytes_ += bytes;
-    prof_launches_++;
-    prof_launch_bytes_.push_back(bytes);
-    prof_launch_sync_.push_back(4.0 * (double)n * tick_sync_streams(d));
-    int inl = 0;
-    for (int j = 0; j < d.nc; ++j) inl += (d.c[j].flags & kFoldInline) ? 1 : 0;
-    int pulls = 0;
-    for (int g = 0; g < d.ng; ++g) pulls |= d.g[g].pull != 0;
-    prof_launch_shape_.push_back(d.nc | (inl << 4) | (d.na << 8) | (d.ng << 16) | (d.nf << 24) |
-                                 (int)((unsigned)pulls << 31));
-  }
+  int inl = 0;
+  for (int j = 0; j < d.nc; ++j) inl += (d.c[j].flags & kFoldInline) ? 1 : 0;
+  int pulls = 0;
+  for (int g = 0; g < d.ng; ++g) pulls |= d.g[g].pull != 0;
+  prof_end(st, bytes, 4.0 * (double)n * tick_sync_streams(d),
+           d.nc | (inl << 4) | (d.na << 8) | (d.ng << 16) | (d.nf << 24) |
+               (int)((unsigned)pulls << 31));
   launches_++;
   alg_bytes_ += bytes;
   nvl_bytes_ += remote;
   return check_cuda(err, "tick kernel");
+}
+
+// Per-launch CUDA events of the profile window (hp_profile_enable).
+void Engine::prof_begin(cudaStream_t st) {
+  if (!prof_on_) return;
+  while (ev_.size() < ev_used_ + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    ev_.push_back(e);
+  }
+  cudaEventRecord(ev_[ev_used_], st);
+}
+
+void Engine::prof_end(cudaStream_t st, double bytes, double sync_bytes, int32_t shape) {
+  if (!prof_on_ || ev_.size() < ev_used_ + 2) return;
+  cudaEventRecord(ev_[ev_used_ + 1], st);
+  ev_used_ += 2;
+  prof_bytes_ += bytes;
+  prof_launches_++;
+  prof_launch_bytes_.push_back(bytes);
+  prof_launch_sync_.push_back(sync_bytes);
+  prof_launch_shape_.push_back(shape);
 }
 
 // Append the segments of a source covering global range [a, a+len): the acc
@@ -692,6 +714,9 @@ hp_status Engine::flush_dist() {
     lastc_[v] = pool_event();
     cudaEventRecord(lastc_[v], vs_[v]);
   }
+  // ---- lockstep batches under HP_XPORT_NCCL / NVLS ------------------------
+  const int lslot = lockstep_slot();
+  if (lslot >= 0) return flush_lockstep(lslot);
   // ---- 2. exchange stream: wait only for the producers it reads ------------
   auto xs_wait = [&](int v) {
     if (vw_[v].here && lastc_[v]) cudaStreamWaitEvent(xs_, lastc_[v], 0);
@@ -788,6 +813,138 @@ hp_status Engine::flush_dist() {
   return HP_OK;
 }
 
+// A lockstep batch: one full-replica VW per GPU (N = G, span 1, so VW v lives
+// on GPU v at identical arena offsets), SGD, and the batch applies exactly one
+// push of the same wave c from every VW, and pulls either no VW or every VW
+// (STRICT: the pull is the copy w_local = w_global). Returns the acc slot of
+// wave c, or -1 (the batch takes the PEER path).
+int Engine::lockstep_slot() const {
+  if (cfg_.transport == HP_XPORT_PEER || !dist_ || G_ != N_ || span_ != 1 || m_) return -1;
+  if (cfg_.transport == HP_XPORT_NVLS && !mc_) return -1;
+  if ((int)ba_.size() != N_) return -1;
+  std::vector<char> seen(N_, 0);
+  for (const BApply& a : ba_) {
+    if (a.c != ba_[0].c || seen[a.v]) return -1;
+    seen[a.v] = 1;
+  }
+  if (!bpull_.empty()) {
+    if ((int)bpull_.size() != N_ || cfg_.local_semantics != HP_LOCAL_STRICT) return -1;
+    std::vector<char> pulled(N_, 0);
+    for (int v : bpull_) {
+      if (pulled[v]) return -1;
+      pulled[v] = 1;
+    }
+  }
+  return ba_[0].slot;
+}
+
+// Exchange of a lockstep batch (PAPER.md P:928-929 apply, P:949 pull): the N
+// pushed u~ of wave c are summed per PS shard and applied once, then every VW
+// pulls the new w_global.
+//   NVLS: BARRIER -> one kernel per owner: multimem.ld_reduce of its shard of
+//         every GPU's acc slot, w_global += sum, multimem.st into every GPU's
+//         w_local -> BARRIER.
+//   NCCL: grouped ncclReduce (reduce-scatter) of the acc slot into the staging
+//         shard -> apply launch -> grouped ncclBroadcast (all-gather) of the
+//         w_global shards into w_local.
+// Then each pulled VW's due folds (the backlog, Z17) on the exchange stream.
+hp_status Engine::flush_lockstep(int slot) {
+  for (const BApply& a : ba_)
+    if (vw_[a.v].here && lastc_[a.v]) cudaStreamWaitEvent(xs_, lastc_[a.v], 0);
+  for (int v : bpull_)
+    if (vw_[v].here && lastc_[v]) cudaStreamWaitEvent(xs_, lastc_[v], 0);
+  const int me = rank_;             // VW `me` lives on this GPU
+  VW& s = vw_[me];
+  const bool pull = !bpull_.empty();
+  const RankLayout& L = lay_[me];
+  const double P = (double)cfg_.nparams, n = (double)n_;
+  if (cfg_.transport == HP_XPORT_NVLS) {
+    if (int e = comm_->barrier(xs_)) return fail(HP_ERR_COMM, comm_->error());
+    NvlsDesc d;
+    memset(&d, 0, sizeof d);
+    d.n = n_;
+    d.wg = wg_;
+    d.mc_acc = (const float*)(mc_ + L.acc_off[me][slot]) + begin_;
+    d.mc_wl = pull ? (float*)(mc_ + L.wl_off[me]) + begin_ : nullptr;
+    d.G = G_;
+    for (int q = 0; q < G_; ++q) {
+      d.src[q] = (const float*)(peer_[q] + lay_[q].acc_off[q][slot]) + begin_;
+      d.dst[q] = (float*)(peer_[q] + lay_[q].wl_off[q]) + begin_;
+    }
+    const double bytes = 4.0 * n * (2 + G_ + (pull ? G_ : 0));
+    prof_begin(xs_);
+    const int err = launch_nvls(d, xs_);
+    prof_end(xs_, bytes, bytes, (N_ << 8) | (pull ? (int)(1u << 31) : 0));
+    launches_++;
+    alg_bytes_ += bytes;
+    nvl_bytes_ += 4.0 * n + (pull ? 4.0 * (P - n) : 0.0);
+    if (hp_status st = check_cuda(err, "nvls kernel")) return st;
+    if (int e = comm_->barrier(xs_)) return fail(HP_ERR_COMM, comm_->error());
+  } else {
+    float* x = (float*)((char*)arena_ + L.x_off);
+    // the collectives are profiled like launches: bytes = what they read and
+    // write in this rank's HBM (send buffer + received data)
+    prof_begin(xs_);
+    if (int e = comm_->reduce_scatter_v(s.acc[slot], x, shard_b_.data(), xs_))
+      return fail(HP_ERR_COMM, comm_->error());
+    prof_end(xs_, 4.0 * (P + n), 4.0 * (P + n), (1 << 8) | (127 << 24));
+    TickDesc d;
+    memset(&d, 0, sizeof d);
+    d.s[0].ptr = x;
+    d.s[0].end = n_;
+    d.ns = 1;
+    d.a[0].seg_begin = 0;
+    d.a[0].seg_end = 1;
+    d.na = 1;
+    if (hp_status st = emit(d, begin_, n_, xs_)) return st;
+    if (pull) {
+      prof_begin(xs_);
+      if (int e = comm_->all_gather_v(wg_, s.wl, shard_b_.data(), xs_))
+        return fail(HP_ERR_COMM, comm_->error());
+      prof_end(xs_, 4.0 * (P + n), 4.0 * (P + n), (1 << 16) | (127 << 24) | (int)(1u << 31));
+    }
+    nvl_bytes_ += 4.0 * n * (G_ - 1) + (pull ? 4.0 * (P - n) : 0.0);
+  }
+  applied_ += (int64_t)ba_.size();
+  lockstep_batches_++;
+  for (int v : bpull_) {
+    VW& t = vw_[v];
+    std::vector<int64_t> folds;
+    folds.swap(t.pending_folds);
+    if (!t.here || folds.empty()) continue;
+    size_t fi = 0;
+    while (fi < folds.size()) {
+      TickDesc d;
+      memset(&d, 0, sizeof d);
+      while (fi < folds.size() && d.ng < kMaxG && d.nf < kMaxF) {
+        DGroup& g = d.g[d.ng++];
+        g.wl = t.wl;
+        g.pull = 0;
+        g.f_begin = d.nf;
+        for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
+          DFold& f = d.f[d.nf++];
+          f.v = (uint32_t)v;
+          f.p = (uint32_t)folds[fi];
+          f.grad = nullptr;
+        }
+        g.f_end = d.nf;
+      }
+      if (hp_status st = emit(d, t.a0, t.len, xs_)) return st;
+    }
+  }
+  cudaEvent_t e = pool_event();       // acc slots free, w_local of the pullers written
+  cudaEventRecord(e, xs_);
+  for (const BApply& a : ba_)
+    if (vw_[a.v].here) xdep_[a.v] = e;
+  for (int v : bpull_)
+    if (vw_[v].here) xdep_[v] = e;
+  bc_.clear();
+  ba_.clear();
+  bpull_.clear();
+  phase_ = kNone;
+  return HP_OK;
+}
+
 void Engine::fork_streams() {
   if (forked_) return;
   cudaEvent_t e = pool_event();
@@ -844,6 +1001,8 @@ hp_status Engine::connect(const void* handles, const void* comm_id) {
   if (sticky_) return sticky_;
   if (!dist_) return fail(HP_ERR_STATE, "hp_connect needs world > 1");
   if (comm_) return fail(HP_ERR_STATE, "already connected");
+  if (cfg_.transport == HP_XPORT_NVLS)
+    return fail(HP_ERR_STATE, "HP_XPORT_NVLS needs hp_connect_symmetric with a multicast mapping");
   for (int q = 0; q < G_; ++q) {
     if (q == rank_) continue;
     cudaIpcMemHandle_t h;
@@ -854,6 +1013,27 @@ hp_status Engine::connect(const void* handles, const void* comm_id) {
     opened_.push_back(p);
     peer_[q] = (char*)p;
   }
+  return finish_connect(comm_id);
+}
+
+hp_status Engine::connect_symmetric(const void* const* bases, void* mc, const void* comm_id) {
+  if (sticky_) return sticky_;
+  if (!dist_) return fail(HP_ERR_STATE, "hp_connect_symmetric needs world > 1");
+  if (comm_) return fail(HP_ERR_STATE, "already connected");
+  if (!ext_arena_) return fail(HP_ERR_STATE, "hp_connect_symmetric needs cfg.arena");
+  if (cfg_.transport == HP_XPORT_NVLS && !mc)
+    return fail(HP_ERR_STATE, "HP_XPORT_NVLS needs a multicast mapping");
+  for (int q = 0; q < G_; ++q) {
+    if (!bases[q] || ((uintptr_t)bases[q] & 255)) return fail(HP_ERR_INVALID, "bad peer base");
+    if (q != rank_) peer_[q] = (char*)bases[q];
+  }
+  if ((const char*)bases[rank_] != (const char*)arena_)
+    return fail(HP_ERR_INVALID, "peer_bases[rank] must be cfg.arena");
+  mc_ = (char*)mc;
+  return finish_connect(comm_id);
+}
+
+hp_status Engine::finish_connect(const void* comm_id) {
   std::string err;
   comm_ = comm_create(comm_id, G_, rank_, &err);
   if (!comm_) return fail(HP_ERR_COMM, err);
@@ -917,6 +1097,7 @@ void Engine::stats(hp_stats* out) const {
     out->pulls[v] = vw_[v].pulls;
   }
   out->nvl_bytes = nvl_bytes_;
+  out->lockstep_batches = lockstep_batches_;
 }
 
 hp_status Engine::profile_enable(bool on) {

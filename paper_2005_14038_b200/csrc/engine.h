@@ -28,7 +28,7 @@ namespace hp {
 // any rank can address any peer's buffers through the peer's arena base).
 struct RankLayout {
   int64_t s0 = 0, s1 = 0;             // PS shard [s0, s1) (global params)
-  size_t wg_off = 0, m_off = 0, bytes = 0;
+  size_t wg_off = 0, m_off = 0, x_off = 0, bytes = 0;   // x: NCCL staging (shard)
   std::vector<int64_t> a, len;        // per VW: local stage [a, a+len)
   std::vector<char> has;              // per VW: a stage lives on this rank
   std::vector<size_t> wl_off;
@@ -67,6 +67,9 @@ class Engine {
   hp_status flush_applies();
   hp_status ipc_handle(void* out);
   hp_status connect(const void* handles, const void* comm_id);
+  hp_status connect_symmetric(const void* const* bases, void* mc, const void* comm_id);
+  int64_t arena_bytes() const { return (int64_t)layout_of(rank_).bytes; }
+  void plan_layout();
   bool distributed() const { return dist_; }
   int64_t local_len(int which) const;
   double nvl_bytes() const { return nvl_bytes_; }
@@ -114,6 +117,11 @@ class Engine {
   hp_status flush();
   hp_status flush_local();
   hp_status flush_dist();
+  int lockstep_slot() const;                 // acc slot of a lockstep batch, or -1
+  hp_status flush_lockstep(int slot);        // its NCCL / NVLS exchange
+  hp_status finish_connect(const void* comm_id);
+  void prof_begin(cudaStream_t st);
+  void prof_end(cudaStream_t st, double bytes, double sync_bytes, int32_t shape);
   hp_status emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st = nullptr,
                  int max_blocks = 0);
   void fork_streams();
@@ -138,6 +146,8 @@ class Engine {
   std::vector<int64_t> stage_b_;      // VW stage boundaries over span
   std::vector<RankLayout> lay_;
   std::vector<char*> peer_;           // arena base of every rank (own = arena_)
+  char* mc_ = nullptr;                // multicast mapping of the arenas (NVLS)
+  bool ext_arena_ = false;            // cfg.arena: caller-owned
   std::vector<void*> opened_;         // IPC mappings to close
   Comm* comm_ = nullptr;
   // a9 overlap (world > 1): barrier/apply/pull launches run on an exchange
@@ -152,6 +162,7 @@ class Engine {
   std::vector<cudaEvent_t> evpool_;
   size_t evnext_ = 0;
   double nvl_bytes_ = 0;
+  int64_t lockstep_batches_ = 0;
   int N_, Nm_, R_;
   int64_t W_, last_p_, n_, begin_;
   cudaStream_t stream_ = nullptr;

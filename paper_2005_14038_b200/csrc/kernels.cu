@@ -222,6 +222,72 @@ __global__ void __launch_bounds__(256) tick_kernel(const __grid_constant__ TickD
   }
 }
 
+// ---------------------------------------------------------------------------
+// NVLS lockstep exchange (NvlsDesc): the NVSwitch sums the N pushed u~ of this
+// rank's shard range (multimem.ld_reduce, fp32 add in the switch), the owner
+// adds the sum to w_global (one rounding: reading Z15) and multicasts the
+// result into every GPU's w_local (multimem.st = the pull). One kernel
+// replaces reduce-scatter + apply + all-gather.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float4 mc_ld_reduce4(const float* mc) {
+  float4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(mc)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ float mc_ld_reduce1(const float* mc) {
+  float r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(r) : "l"(mc) : "memory");
+  return r;
+}
+__device__ __forceinline__ void mc_st4(float* mc, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};"
+               ::"l"(mc), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mc_st1(float* mc, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
+}
+
+template <int U>
+__global__ void __launch_bounds__(256) nvls_kernel(const __grid_constant__ NvlsDesc d) {
+  const int64_t nfull = d.n >> 2;
+  const int64_t S = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float4* wg4 = reinterpret_cast<float4*>(d.wg);
+  int64_t q = t0;
+  for (; q + (U - 1) * S < nfull; q += U * S) {
+    float4 s[U], w[U];
+#pragma unroll
+    for (int x = 0; x < U; ++x) {
+      s[x] = mc_ld_reduce4(d.mc_acc + 4 * (q + x * S));
+      w[x] = __ldcs(wg4 + q + x * S);
+    }
+#pragma unroll
+    for (int x = 0; x < U; ++x) {
+      w[x] = f4add(w[x], s[x]);
+      __stcs(wg4 + q + x * S, w[x]);
+      if (d.mc_wl) mc_st4(d.mc_wl + 4 * (q + x * S), w[x]);
+    }
+  }
+  for (; q < nfull; q += S) {
+    float4 w = f4add(__ldcs(wg4 + q), mc_ld_reduce4(d.mc_acc + 4 * q));
+    __stcs(wg4 + q, w);
+    if (d.mc_wl) mc_st4(d.mc_wl + 4 * q, w);
+  }
+  if (t0 == 0)
+    for (int64_t i = nfull * 4; i < d.n; ++i) {
+      const float w = __fadd_rn(d.wg[i], mc_ld_reduce1(d.mc_acc + i));
+      d.wg[i] = w;
+      if (d.mc_wl) mc_st1(d.mc_wl + i, w);
+    }
+  // the multicast stores must be visible system-wide before the barrier that
+  // follows this kernel releases the other ranks to read their w_local
+  __threadfence_system();
+}
+
 // w0 (Z8): zero or Philox stream 1, counter (i>>2, 0, 0, 1).
 __global__ void init_kernel(float* out, int64_t n, int64_t param_begin, int w0_mode,
                             int grad_mode, uint32_t k0, uint32_t k1) {
@@ -302,6 +368,23 @@ int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream, i
     case 1: return momentum ? launch_gm<1, true>(d, s, mb) : launch_gm<1, false>(d, s, mb);
     default: return momentum ? launch_gm<2, true>(d, s, mb) : launch_gm<2, false>(d, s, mb);
   }
+}
+
+int launch_nvls(const NvlsDesc& d, void* stream) {
+  if (d.n <= 0) return 0;
+  static int grid_max = 0;
+  if (grid_max == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nvls_kernel<4>, 256, 0);
+    grid_max = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  int64_t blocks = ((d.n >> 2) + 255) / 256;
+  if (blocks > grid_max) blocks = grid_max;
+  if (blocks < 1) blocks = 1;
+  nvls_kernel<4><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d);
+  return (int)cudaGetLastError();
 }
 
 int launch_init(float* out, int64_t n, int64_t param_begin, int w0_mode, int grad_mode,

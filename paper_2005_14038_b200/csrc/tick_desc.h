@@ -122,6 +122,24 @@ inline int tick_sync_streams(const TickDesc& d) {
   return s;
 }
 
+// Lockstep exchange through the NVSwitch (HP_XPORT_NVLS, include/hetpipe.h):
+// over this rank's PS shard, u = multimem.ld_reduce(mc_acc) (the sum of every
+// GPU's pushed u~ at that index), w_global += u, and if mc_wl is set
+// multimem.st(mc_wl, w_global) writes the pulled value into every GPU's
+// w_local. src/dst are the same buffers through unicast peer mappings (used
+// only by the host emulation in tests/emu; the device kernel uses mc_*).
+struct NvlsDesc {
+  int64_t n;             // params of this rank's PS shard
+  float* wg;             // w_global shard
+  const float* mc_acc;   // multicast address of the acc slot at the shard's first param
+  float* mc_wl;          // multicast address of w_local at the shard's first param, or nullptr
+  int32_t G;
+  int32_t pad;
+  const float* src[8];   // per rank: acc slot at the shard's first param (unicast)
+  float* dst[8];         // per rank: w_local at the shard's first param (unicast)
+};
+int launch_nvls(const NvlsDesc& d, void* stream);
+
 // Launch the fused tick kernel (kernels.cu). grad_mode: HP_GRAD_*.
 // Returns a cudaError_t as int.
 // max_blocks > 0 bounds the grid (exchange launches that share the GPU with

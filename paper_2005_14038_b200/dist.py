@@ -45,3 +45,30 @@ def placed_context(cfg, rank: int, world: int, span: int, device: int = 0, strea
     dist.all_gather_object(handles, ctx.ipc_handle(), group=pg)
     ctx.connect(handles, ids[0])
     return ctx
+
+
+def symmetric_context(cfg, rank: int, world: int, span: int, device: int = 0, stream: int = 0,
+                      pg=None, **overrides):
+    """Collective: like placed_context, but the arena is a torch symmetric-memory
+    allocation (device memory plumbing: torch maps every peer's arena and, on
+    NVSwitch systems, a multicast mapping of all of them), handed to the library
+    through hp_config.arena + hp_connect_symmetric. Needed for HP_XPORT_NVLS.
+    Returns (ctx, keepalive): keep `keepalive` referenced while ctx lives."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+    c = hetpipe.config_from(cfg, world=world, rank=rank, vw_span=span, device=device,
+                            stream=stream or None, **overrides)
+    nbytes = hetpipe.arena_bytes(c)
+    sizes = [None] * world
+    dist.all_gather_object(sizes, nbytes, group=pg)
+    nbytes = max(sizes)                  # one size for the symmetric allocation
+    buf = symm.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+    h = symm.rendezvous(buf, pg if pg is not None else dist.group.WORLD)
+    c.arena = buf.data_ptr()
+    ctx = hetpipe.Context(c)
+    ids = [hetpipe.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0, group=pg)
+    mc = int(getattr(h, "multicast_ptr", 0) or 0)
+    ctx.connect_symmetric([int(p) for p in h.buffer_ptrs], mc, ids[0])
+    return ctx, (buf, h)

@@ -31,14 +31,19 @@ class hp_config(C.Structure):
                 ("pull_policy", C.c_int32), ("local_semantics", C.c_int32),
                 ("apply_mode", C.c_int32), ("acc_slots", C.c_int32),
                 ("merge_ticks", C.c_int32), ("world", C.c_int32), ("rank", C.c_int32),
-                ("vw_span", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p)]
+                ("vw_span", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p),
+                ("transport", C.c_int32), ("reserved", C.c_int32), ("arena", C.c_void_p)]
+
+XPORT_PEER, XPORT_NCCL, XPORT_NVLS = 0, 1, 2
+XPORTS = {"peer": XPORT_PEER, "nccl": XPORT_NCCL, "nvls": XPORT_NVLS}
 
 
 class hp_stats(C.Structure):
     _fields_ = [("commits", C.c_int64), ("applied", C.c_int64),
                 ("launches", C.c_int64), ("ticks", C.c_int64),
                 ("alg_bytes", C.c_double), ("wait_ticks", C.c_int64 * 8),
-                ("pulls", C.c_int64 * 8), ("nvl_bytes", C.c_double)]
+                ("pulls", C.c_int64 * 8), ("nvl_bytes", C.c_double),
+                ("lockstep_batches", C.c_int64)]
 
 
 class HetPipeError(RuntimeError):
@@ -65,6 +70,8 @@ EXPORTS = {
     "hp_comm_unique_id": (C.c_int, [C.c_void_p]),
     "hp_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
     "hp_connect": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hp_arena_bytes": (C.c_int64, [C.POINTER(hp_config)]),
+    "hp_connect_symmetric": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hp_schedule_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "hp_schedule_advance": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
     "hp_run_schedule": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -194,6 +201,11 @@ class Context:
         cb = C.create_string_buffer(comm_id, 128)
         self._chk(self.lib.hp_connect(self.h, hb, cb))
 
+    def connect_symmetric(self, bases: Sequence[int], mc_base: int, comm_id: bytes) -> None:
+        arr = (C.c_void_p * len(bases))(*bases)
+        cb = C.create_string_buffer(comm_id, 128)
+        self._chk(self.lib.hp_connect_symmetric(self.h, arr, mc_base or None, cb))
+
     def set_tick(self, t: int) -> int:
         return self._chk(self.lib.hp_set_tick(self.h, t))
 
@@ -303,6 +315,13 @@ def comm_unique_id(lib: Optional[C.CDLL] = None) -> bytes:
     if st != HP_OK:
         raise HetPipeError(st, lib.hp_last_error(None).decode())
     return buf.raw
+
+
+def arena_bytes(cfg: hp_config, lib: Optional[C.CDLL] = None) -> int:
+    n = (lib if lib is not None else load()).hp_arena_bytes(C.byref(cfg))
+    if n < 0:
+        raise HetPipeError(HP_ERR_INVALID, "hp_arena_bytes: bad config")
+    return n
 
 
 def s_global(Nm: int, D: int) -> int:

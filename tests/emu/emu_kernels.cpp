@@ -79,6 +79,20 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
   return 0;
 }
 
+// NVLS lockstep exchange through the unicast mappings: the switch's sum is
+// emulated in rank order (the device order is the switch's, reading Z15).
+int launch_nvls(const NvlsDesc& d, void*) {
+  for (int64_t i = 0; i < d.n; ++i) {
+    float s = d.src[0][i];
+    for (int q = 1; q < d.G; ++q) s = s + d.src[q][i];
+    const float w = d.wg[i] + s;
+    d.wg[i] = w;
+    if (d.mc_wl)
+      for (int q = 0; q < d.G; ++q) d.dst[q][i] = w;
+  }
+  return 0;
+}
+
 int launch_init(float* out, int64_t n, int64_t begin, int w0_mode, int gm, uint32_t k0,
                 uint32_t k1, void*) {
   for (int64_t i = 0; i < n; ++i) {

@@ -85,7 +85,12 @@ C4 = WSPConfig("C4", 4, 8, 32, VGG19_PARAMS, 132, TAU_ED)
 C5 = WSPConfig("C5", 8, 8, 0, VGG19_PARAMS, 132,
                (250, 250, 330, 330, 346, 346, 421, 421), momentum=0.9)
 
-CONFIGS = {c.name: c for c in (C1, C1_SKEW, C2, C3, C4, C5)}
+# C5's equal-speed SGD variant (SURVEY.md 8(d) "plus an equal-speed variant"):
+# with D = 0 every VW pushes and pulls in the same tick, the lockstep batch the
+# NCCL / NVLS transports exchange (include/hetpipe.h HP_XPORT_*); one VW per GPU
+# (num_vw = G at run time).
+C5E = WSPConfig("C5E", 8, 8, 0, VGG19_PARAMS, 132, (325,) * 8)
+CONFIGS = {c.name: c for c in (C1, C1_SKEW, C2, C3, C4, C5, C5E)}
 
 
 def even_shards(nparams: int, nshards: int, align: int = 32) -> Sequence[int]:
