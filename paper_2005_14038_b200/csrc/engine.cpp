@@ -94,6 +94,8 @@ Engine::~Engine() {
   if (xs_) cudaStreamDestroy(xs_);
   for (auto v : vs_)
     if (v) cudaStreamDestroy(v);
+  for (auto v : fs_)
+    if (v) cudaStreamDestroy(v);
   for (void* p : opened_) cudaIpcCloseMemHandle(p);
   for (auto e : ev_) cudaEventDestroy(e);
   if (arena_ && !ext_arena_) cudaFree(arena_);
@@ -669,8 +671,10 @@ hp_status Engine::flush_dist() {
     }
     TickDesc d;
     memset(&d, 0, sizeof d);
+    int cslot[kMaxC];
     for (const BComplete& b : bc_) {
       if (b.v != v) continue;
+      cslot[d.nc] = b.slot;
       DComplete& c = d.c[d.nc++];
       c.acc = s.acc[b.slot];
       c.grad = nullptr;
@@ -683,19 +687,38 @@ hp_status Engine::flush_dist() {
     std::vector<int64_t> folds;
     if (!pulled[v] && !hold) folds.swap(s.pending_folds);
     if (d.nc == 0 && folds.empty()) continue;
-    if (xdep_[v]) {
-      cudaStreamWaitEvent(vs_[v], xdep_[v], 0);
-      xdep_[v] = nullptr;
-    }
-    if (folds.size() == 1 && d.nc == 1 && (int64_t)d.c[0].p == folds[0]) {
-      d.c[0].flags |= kFoldInline;
-      d.c[0].wl = s.wl;
-      folds.clear();
+    auto wait_clear = [](cudaStream_t st, cudaEvent_t& e) {
+      if (e) cudaStreamWaitEvent(st, e, 0);
+      e = nullptr;
+    };
+    cudaStream_t fst = vs_[v];          // stream of the w_local folds
+    if (split_folds_) {
+      // acc part now (its slot is free once the exchange that read it is done)
+      if (d.nc) {
+        for (int j = 0; j < d.nc; ++j) wait_clear(vs_[v], xacc_[v][cslot[j]]);
+        if (hp_status st = emit(d, s.a0, s.len, vs_[v])) return st;
+        lastc_[v] = pool_event();
+        cudaEventRecord(lastc_[v], vs_[v]);
+        memset(&d, 0, sizeof d);
+      }
+      if (folds.empty()) continue;
+      fst = fs_[v];                     // folds after the pull that rewrote w_local
+      wait_clear(fst, xwl_[v]);
+      if (lastw_[v]) cudaStreamWaitEvent(fst, lastw_[v], 0);
+    } else {
+      for (int j = 0; j < d.nc; ++j) wait_clear(vs_[v], xacc_[v][cslot[j]]);
+      wait_clear(vs_[v], xwl_[v]);
+      if (lastw_[v]) cudaStreamWaitEvent(vs_[v], lastw_[v], 0);
+      if (folds.size() == 1 && d.nc == 1 && (int64_t)d.c[0].p == folds[0]) {
+        d.c[0].flags |= kFoldInline;
+        d.c[0].wl = s.wl;
+        folds.clear();
+      }
     }
     size_t fi = 0;
     while (fi < folds.size()) {
       if (d.ng == kMaxG || d.nf == kMaxF) {
-        if (hp_status st = emit(d, s.a0, s.len, vs_[v])) return st;
+        if (hp_status st = emit(d, s.a0, s.len, fst)) return st;
         memset(&d, 0, sizeof d);
       }
       DGroup& g = d.g[d.ng++];
@@ -710,9 +733,11 @@ hp_status Engine::flush_dist() {
       }
       g.f_end = d.nf;
     }
-    if (hp_status st = emit(d, s.a0, s.len, vs_[v])) return st;
-    lastc_[v] = pool_event();
-    cudaEventRecord(lastc_[v], vs_[v]);
+    if (hp_status st = emit(d, s.a0, s.len, fst)) return st;
+    cudaEvent_t e = pool_event();
+    cudaEventRecord(e, fst);
+    if (d.nc || fst == vs_[v]) lastc_[v] = e;
+    lastw_[v] = e;
   }
   // ---- lockstep batches under HP_XPORT_NCCL / NVLS ------------------------
   const int lslot = lockstep_slot();
@@ -721,9 +746,15 @@ hp_status Engine::flush_dist() {
   auto xs_wait = [&](int v) {
     if (vw_[v].here && lastc_[v]) cudaStreamWaitEvent(xs_, lastc_[v], 0);
   };
+  auto xs_wait_wl = [&](int v) {      // a pull rewrites w_local: after its folds
+    if (vw_[v].here && lastw_[v]) cudaStreamWaitEvent(xs_, lastw_[v], 0);
+  };
   if (!ba_.empty()) {
     for (const BApply& a : ba_) xs_wait(a.v);
-    for (int v : bpull_) xs_wait(v);
+    for (int v : bpull_) {
+      xs_wait(v);
+      xs_wait_wl(v);
+    }
     if (int e = comm_->barrier(xs_)) return fail(HP_ERR_COMM, comm_->error());
     size_t k = 0;
     while (k < ba_.size()) {
@@ -744,9 +775,12 @@ hp_status Engine::flush_dist() {
     cudaEvent_t e = pool_event();       // acc slots read by the applies are free
     cudaEventRecord(e, xs_);
     for (const BApply& a : ba_)
-      if (vw_[a.v].here) xdep_[a.v] = e;
+      if (vw_[a.v].here) xacc_[a.v][a.slot] = e;
   } else {
-    for (int v : bpull_) xs_wait(v);
+    for (int v : bpull_) {
+      xs_wait(v);
+      xs_wait_wl(v);
+    }
   }
   // ---- 3. pulls: per local stage range one launch reads w_global from the
   //      shard owners once (into registers) and writes every pulled w_local of
@@ -804,7 +838,11 @@ hp_status Engine::flush_dist() {
     cudaEvent_t e = pool_event();       // w_local of the pulled VWs is written
     cudaEventRecord(e, xs_);
     for (int v : bpull_)
-      if (vw_[v].here) xdep_[v] = e;
+      if (vw_[v].here) {
+        xwl_[v] = e;
+        lastw_[v] = nullptr;              // ordered behind e
+        if (!strict) xacc_[v][vw_[v].c_local % R_] = e;   // read as the partial u~
+      }
   }
   bc_.clear();
   ba_.clear();
@@ -851,8 +889,10 @@ int Engine::lockstep_slot() const {
 hp_status Engine::flush_lockstep(int slot) {
   for (const BApply& a : ba_)
     if (vw_[a.v].here && lastc_[a.v]) cudaStreamWaitEvent(xs_, lastc_[a.v], 0);
-  for (int v : bpull_)
+  for (int v : bpull_) {
     if (vw_[v].here && lastc_[v]) cudaStreamWaitEvent(xs_, lastc_[v], 0);
+    if (vw_[v].here && lastw_[v]) cudaStreamWaitEvent(xs_, lastw_[v], 0);
+  }
   const int me = rank_;             // VW `me` lives on this GPU
   VW& s = vw_[me];
   const bool pull = !bpull_.empty();
@@ -873,7 +913,7 @@ hp_status Engine::flush_lockstep(int slot) {
     }
     const double bytes = 4.0 * n * (2 + G_ + (pull ? G_ : 0));
     prof_begin(xs_);
-    const int err = launch_nvls(d, xs_);
+    const int err = launch_nvls(d, xs_, xblocks_);
     prof_end(xs_, bytes, bytes, (N_ << 8) | (pull ? (int)(1u << 31) : 0));
     launches_++;
     alg_bytes_ += bytes;
@@ -935,9 +975,12 @@ hp_status Engine::flush_lockstep(int slot) {
   cudaEvent_t e = pool_event();       // acc slots free, w_local of the pullers written
   cudaEventRecord(e, xs_);
   for (const BApply& a : ba_)
-    if (vw_[a.v].here) xdep_[a.v] = e;
+    if (vw_[a.v].here) xacc_[a.v][a.slot] = e;
   for (int v : bpull_)
-    if (vw_[v].here) xdep_[v] = e;
+    if (vw_[v].here) {
+      xwl_[v] = e;
+      lastw_[v] = nullptr;
+    }
   bc_.clear();
   ba_.clear();
   bpull_.clear();
@@ -950,8 +993,10 @@ void Engine::fork_streams() {
   cudaEvent_t e = pool_event();
   cudaEventRecord(e, stream_);
   cudaStreamWaitEvent(xs_, e, 0);
-  for (int v = 0; v < N_; ++v)
+  for (int v = 0; v < N_; ++v) {
     if (vs_[v]) cudaStreamWaitEvent(vs_[v], e, 0);
+    if (fs_[v]) cudaStreamWaitEvent(fs_[v], e, 0);
+  }
   forked_ = true;
 }
 
@@ -977,13 +1022,17 @@ hp_status Engine::join_exchange() {
   cudaEventRecord(e, xs_);
   cudaStreamWaitEvent(stream_, e, 0);
   for (int v = 0; v < N_; ++v) {
-    if (!vs_[v]) continue;
-    cudaEvent_t ev = pool_event();
-    cudaEventRecord(ev, vs_[v]);
-    cudaStreamWaitEvent(stream_, ev, 0);
+    for (cudaStream_t sv : {vs_[v], fs_[v]}) {
+      if (!sv) continue;
+      cudaEvent_t ev = pool_event();
+      cudaEventRecord(ev, sv);
+      cudaStreamWaitEvent(stream_, ev, 0);
+    }
   }
-  std::fill(xdep_.begin(), xdep_.end(), nullptr);
+  for (auto& x : xacc_) std::fill(x.begin(), x.end(), nullptr);
+  std::fill(xwl_.begin(), xwl_.end(), nullptr);
   std::fill(lastc_.begin(), lastc_.end(), nullptr);
+  std::fill(lastw_.begin(), lastw_.end(), nullptr);
   forked_ = false;
   return check_cuda(cudaGetLastError(), "join");
 }
@@ -1037,13 +1086,30 @@ hp_status Engine::finish_connect(const void* comm_id) {
   std::string err;
   comm_ = comm_create(comm_id, G_, rank_, &err);
   if (!comm_) return fail(HP_ERR_COMM, err);
-  if (int e = cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking)) return check_cuda(e, "stream");
-  xdep_.assign(N_, nullptr);
+  // Stream priorities (HP_PRIO, default on): the exchange and the folds that
+  // wait for it are the round's critical path; the accumulation of the next
+  // wave has slack (the acc ring), so its CTAs yield to them.
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (const char* pr = getenv("HP_PRIO"))
+    if (atoi(pr) == 0) prio_lo = prio_hi = 0;
+  if (int e = cudaStreamCreateWithPriority(&xs_, cudaStreamNonBlocking, prio_hi))
+    return check_cuda(e, "stream");
+  xacc_.assign(N_, std::vector<cudaEvent_t>(R_, nullptr));
+  xwl_.assign(N_, nullptr);
   lastc_.assign(N_, nullptr);
+  lastw_.assign(N_, nullptr);
   vs_.assign(N_, nullptr);
+  fs_.assign(N_, nullptr);
+  if (const char* sf = getenv("HP_SPLIT_FOLDS")) split_folds_ = atoi(sf) != 0;
   for (int v = 0; v < N_; ++v)
     if (vw_[v].here)
-      if (int e = cudaStreamCreateWithFlags(&vs_[v], cudaStreamNonBlocking)) return check_cuda(e, "stream");
+    {
+      if (int e = cudaStreamCreateWithPriority(&vs_[v], cudaStreamNonBlocking, prio_lo))
+        return check_cuda(e, "stream");
+      if (int e = cudaStreamCreateWithPriority(&fs_[v], cudaStreamNonBlocking, prio_hi))
+        return check_cuda(e, "stream");
+    }
   if (const char* xb = getenv("HP_XBLOCKS")) xblocks_ = atoi(xb);
   // everyone's init writes are complete before anyone reads a peer
   if (int e = comm_->barrier(stream_)) return fail(HP_ERR_COMM, comm_->error());

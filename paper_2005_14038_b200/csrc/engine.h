@@ -154,9 +154,17 @@ class Engine {
   // stream; a compute-stream launch waits only for the exchange events of the
   // VWs whose buffers it touches.
   cudaStream_t xs_ = nullptr;
-  std::vector<cudaEvent_t> xdep_;     // per VW: exchange op that last touched it
-  std::vector<cudaEvent_t> lastc_;    // per VW: its last accumulation launch
+  // Per local VW: accumulation (acc ring) runs on vs_, folds into w_local on
+  // fs_ (split_folds_), so the next wave's accumulation does not wait for the
+  // pull that rewrites w_local (row a9); exchange ops wait for exactly the
+  // producers they read and publish what they freed / wrote.
+  std::vector<std::vector<cudaEvent_t>> xacc_;  // [vw][slot]: exchange that last read the slot
+  std::vector<cudaEvent_t> xwl_;      // exchange (pull) that last wrote the VW's w_local
+  std::vector<cudaEvent_t> lastc_;    // its last acc-writing launch
+  std::vector<cudaEvent_t> lastw_;    // its last w_local-writing launch (vs_ or fs_)
   std::vector<cudaStream_t> vs_;      // per local VW: accumulation stream
+  std::vector<cudaStream_t> fs_;      // per local VW: fold stream
+  bool split_folds_ = false;          // HP_SPLIT_FOLDS=1: acc and folds in separate launches
   bool forked_ = false;               // side streams ordered after the context stream
   int xblocks_ = 0;                   // grid bound of exchange launches (HP_XBLOCKS)
   std::vector<cudaEvent_t> evpool_;

@@ -370,7 +370,7 @@ int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream, i
   }
 }
 
-int launch_nvls(const NvlsDesc& d, void* stream) {
+int launch_nvls(const NvlsDesc& d, void* stream, int max_blocks) {
   if (d.n <= 0) return 0;
   static int grid_max = 0;
   if (grid_max == 0) {
@@ -382,6 +382,7 @@ int launch_nvls(const NvlsDesc& d, void* stream) {
   }
   int64_t blocks = ((d.n >> 2) + 255) / 256;
   if (blocks > grid_max) blocks = grid_max;
+  if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
   nvls_kernel<4><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d);
   return (int)cudaGetLastError();

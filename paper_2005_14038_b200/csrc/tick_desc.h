@@ -138,7 +138,7 @@ struct NvlsDesc {
   const float* src[8];   // per rank: acc slot at the shard's first param (unicast)
   float* dst[8];         // per rank: w_local at the shard's first param (unicast)
 };
-int launch_nvls(const NvlsDesc& d, void* stream);
+int launch_nvls(const NvlsDesc& d, void* stream, int max_blocks = 0);
 
 // Launch the fused tick kernel (kernels.cu). grad_mode: HP_GRAD_*.
 // Returns a cudaError_t as int.

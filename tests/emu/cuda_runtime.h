@@ -26,6 +26,14 @@ inline cudaError_t cudaStreamCreateWithFlags(cudaStream_t* s, unsigned) {
   *s = (cudaStream_t)(uintptr_t)1;
   return cudaSuccess;
 }
+inline cudaError_t cudaStreamCreateWithPriority(cudaStream_t* s, unsigned f, int) {
+  return cudaStreamCreateWithFlags(s, f);
+}
+inline cudaError_t cudaDeviceGetStreamPriorityRange(int* lo, int* hi) {
+  *lo = 0;
+  *hi = -1;
+  return cudaSuccess;
+}
 inline cudaError_t cudaStreamDestroy(cudaStream_t) { return cudaSuccess; }
 inline cudaError_t cudaMalloc(void** p, size_t n) {
   *p = aligned_alloc(256, (n + 255) / 256 * 256);

@@ -81,7 +81,7 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
 
 // NVLS lockstep exchange through the unicast mappings: the switch's sum is
 // emulated in rank order (the device order is the switch's, reading Z15).
-int launch_nvls(const NvlsDesc& d, void*) {
+int launch_nvls(const NvlsDesc& d, void*, int) {
   for (int64_t i = 0; i < d.n; ++i) {
     float s = d.src[0][i];
     for (int q = 1; q < d.G; ++q) s = s + d.src[q][i];
