@@ -206,6 +206,8 @@ def main():
     ap.add_argument("--impl", default="hetpipe", choices=["hetpipe", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--profile-steps", type=int, default=20,
+                    help="steps of the separate per-launch-profiled pass after the timed region")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-params", type=int, default=1 << 18)
@@ -254,7 +256,8 @@ def main():
 
     lo, hi = hdist.shard_bounds(cfg.nparams, ws, rank)
     N = cfg.num_vw
-    waves = args.warmup + args.steps + 2
+    prof_steps = max(1, min(args.steps, args.profile_steps))
+    waves = args.warmup + args.steps + prof_steps + 2
     run_cfg = cfg.replace(waves=waves)
     stream = torch.cuda.Stream(local)          # a real stream: the library launches on it
     torch.cuda.set_stream(stream)              # and the timing events below record on it
@@ -279,10 +282,10 @@ def main():
     torch.cuda.synchronize()
     barrier()
     st0 = ctx.stats()
-    ctx.profile_enable(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     barrier()
+    # ---- timed region: K steps, no per-launch instrumentation
     ev0.record(stream)
     for k in range(args.steps):
         ctx.schedule_advance(N * (args.warmup + k + 1))
@@ -290,7 +293,21 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clocks = sampler.stop()
-    ms = ev0.elapsed_time(ev1)
+    ms_timed = ev0.elapsed_time(ev1)
+    st1 = ctx.stats()
+    # ---- profiled pass over the next steps of the same schedule: per-launch
+    # CUDA events on the launch streams (roofline, launch mix, sync latency)
+    ctx.profile_enable(True)
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    pe0.record(stream)
+    for k in range(prof_steps):
+        ctx.schedule_advance(N * (args.warmup + args.steps + k + 1))
+    pe1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = pe0.elapsed_time(pe1)
     kern_ms, kern_bytes, kern_launches = ctx.profile_read()
     l_ms, l_bytes, l_shape, l_sync, l_t0 = ctx.profile_launches()
     # device time during which at least one tick kernel runs (union of the
@@ -310,29 +327,30 @@ def main():
     # pull ops are fused with accumulation, so they have no launch of their own)
     sync_ms = float(sum(float(t) * float(sy) / float(by)
                         for t, by, sy in zip(l_ms, l_bytes, l_sync) if by > 0))
+    s_ms, s_vw = ctx.profile_sync_latency()
+    sync_us = [1e3 * float(x) for x in s_ms]
     mix = {}
-    sync_us = []
     for t_ms, by, sh in zip(l_ms, l_bytes, l_shape):
         sh = int(sh) & 0xFFFFFFFF
         key = (f"c{sh & 15}i{(sh >> 4) & 15}a{(sh >> 8) & 255}g{(sh >> 16) & 255}"
                f"f{(sh >> 24) & 127}")
         if (sh >> 24) & 127 == 127:
             key = "nccl_reduce_scatter" if (sh >> 8) & 255 else "nccl_all_gather"
-        if sh >> 31 or (sh >> 8) & 255:
-            sync_us.append(1e3 * float(t_ms))
         e = mix.setdefault(key, [0, 0.0, 0.0])
         e[0] += 1
         e[1] += float(t_ms)
         e[2] += float(by)
     launch_mix = {k: {"n": n, "us_mean": 1e3 * t / n, "GBps": b / (t / 1e3) / 1e9}
                   for k, (n, t, b) in sorted(mix.items(), key=lambda kv: -kv[1][1])}
-    st1 = ctx.stats()
+    st2 = ctx.stats()
     commits = st1.commits - st0.commits
-    t = torch.tensor([ms, sync_ms], dtype=torch.float64, device=f"cuda:{local}")
+    pcommits = st2.commits - st1.commits
+    t = torch.tensor([ms_timed, sync_ms * commits / max(pcommits, 1)], dtype=torch.float64,
+                     device=f"cuda:{local}")
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t[0].item())
-    sync_ms_max = float(t[1].item())
+    sync_ms_max = float(t[1].item())     # scaled from the profiled pass to K steps
     value = commits * cfg.nparams / (ms_max / 1e3)
     launches = st1.launches - st0.launches
     nvl = torch.tensor([st1.nvl_bytes - st0.nvl_bytes], dtype=torch.float64, device=f"cuda:{local}")
@@ -426,9 +444,11 @@ def main():
                    "peak_GBps": 770.0, "peak_kind": "guide-measured peer copy per direction"},
         "wave_sync_latency_us": (
             {"p50": float(np.percentile(sync_us, 50)), "p99": float(np.percentile(sync_us, 99)),
-             "n": len(sync_us),
-             "def": "device time of each launch that applies pushed waves or pulls "
-                    "(push -> apply -> pull of a round, fused)"} if sync_us else None),
+             "max": float(np.max(sync_us)), "n": len(sync_us),
+             "def": "per (VW, wave), rank 0: device time from the start of the launch carrying "
+                    "the VW's wave-end COMPLETE (u~ final = push) to the end of the launch that "
+                    "wrote its pulled w_local (hp_profile_sync_latency); includes gate waits"}
+            if sync_us else None),
         "kernel_share_of_step": busy_ms / ms if ms > 0 else None,
         "launch_mix": launch_mix,
         "gpu_launches": launches,

@@ -265,6 +265,14 @@ hp_status hp_profile_launches(hp_ctx* ctx, int64_t max, float* ms, double* alg_b
                               int32_t* shape, double* sync_bytes, float* start_ms,
                               int64_t* n);
 
+/* Wave-sync latency of the same window, one record per
+   (VW, wave) whose push and pull both fall in it: device time from the start
+   of the launch that carried the VW's wave-end COMPLETE (its u~ final: the
+   push) to the end of the launch (or NCCL collective) that wrote its pulled
+   w_local (a LAZY admission without a pull ends no record; a VW that waited at
+   its gate includes the wait). ms[i], vw[i]; *n = records written. */
+hp_status hp_profile_sync_latency(hp_ctx* ctx, int64_t max, float* ms, int32_t* vw, int64_t* n);
+
 /* Closed forms of section 5 (no context needed). */
 int64_t hp_s_global(int32_t Nm, int32_t D);                  /* (D+1)*Nm + Nm - 2 */
 int64_t hp_version_floor(int64_t p, int32_t Nm, int32_t D);  /* max(0, p - s_global - 1) */

@@ -427,6 +427,12 @@ hp_status hp_profile_launches(hp_ctx* ctx, int64_t max, float* ms, double* alg_b
   HP_EXIT(ctx)
 }
 
+hp_status hp_profile_sync_latency(hp_ctx* ctx, int64_t max, float* ms, int32_t* vw, int64_t* n) {
+  HP_ENTRY(ctx)
+  return ctx->eng->profile_sync(max, ms, vw, n);
+  HP_EXIT(ctx)
+}
+
 int64_t hp_s_global(int32_t Nm, int32_t D) {
   // s_global = (D+1)(s_local+1) + s_local - 1 with s_local = Nm-1
   return (int64_t)(D + 1) * Nm + (Nm - 1) - 1;

@@ -454,10 +454,53 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   prof_end(st, bytes, 4.0 * (double)n * tick_sync_streams(d),
            d.nc | (inl << 4) | (d.na << 8) | (d.ng << 16) | (d.nf << 24) |
                (int)((unsigned)pulls << 31));
+  note_sync(d);
   launches_++;
   alg_bytes_ += bytes;
   nvl_bytes_ += remote;
   return check_cuda(err, "tick kernel");
+}
+
+// Wave-sync latency bookkeeping (profile window only): a launch with VW v's
+// wave-end COMPLETE starts v's push; the launch that writes v's pulled
+// w_local ends its sync (SURVEY.md 8(d) "wave-sync latency").
+void Engine::note_sync(const TickDesc& d) {
+  if (!prof_on_ || prof_launches_ == 0) return;
+  const int64_t idx = prof_launches_ - 1;
+  for (int j = 0; j < d.nc; ++j)
+    if (d.c[j].p % (uint32_t)Nm_ == 0 && push_launch_[d.c[j].v] < 0) push_launch_[d.c[j].v] = idx;
+  std::vector<int> pulled;
+  for (int g = 0; g < d.ng; ++g)
+    if (d.g[g].pull)
+      for (int v = 0; v < N_; ++v)
+        if (vw_[v].wl == d.g[g].wl) pulled.push_back(v);
+  note_pulls(pulled);
+}
+
+void Engine::note_pulls(const std::vector<int>& vws) {
+  if (!prof_on_ || prof_launches_ == 0) return;
+  const int64_t idx = prof_launches_ - 1;
+  for (int v : vws)
+    if (push_launch_[v] >= 0) {
+      sync_recs_.push_back({v, push_launch_[v], idx});
+      push_launch_[v] = -1;
+    }
+}
+
+hp_status Engine::profile_sync(int64_t max, float* ms, int32_t* vw, int64_t* n) {
+  if (sticky_) return sticky_;
+  if (hp_status st = join_exchange()) return st;
+  if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "profile sync")) return st;
+  const int64_t cnt = std::min<int64_t>(max, (int64_t)sync_recs_.size());
+  for (int64_t i = 0; i < cnt; ++i) {
+    float t = 0;
+    const SyncRec& r = sync_recs_[i];
+    if (int e = cudaEventElapsedTime(&t, ev_[2 * r.from], ev_[2 * r.to + 1])) return check_cuda(e, "elapsed");
+    if (ms) ms[i] = t;
+    if (vw) vw[i] = r.v;
+  }
+  if (n) *n = cnt;
+  return HP_OK;
 }
 
 // Per-launch CUDA events of the profile window (hp_profile_enable).
@@ -915,6 +958,7 @@ hp_status Engine::flush_lockstep(int slot) {
     prof_begin(xs_);
     const int err = launch_nvls(d, xs_, xblocks_);
     prof_end(xs_, bytes, bytes, (N_ << 8) | (pull ? (int)(1u << 31) : 0));
+    if (pull) note_pulls(bpull_);
     launches_++;
     alg_bytes_ += bytes;
     nvl_bytes_ += 4.0 * n + (pull ? 4.0 * (P - n) : 0.0);
@@ -942,6 +986,7 @@ hp_status Engine::flush_lockstep(int slot) {
       if (int e = comm_->all_gather_v(wg_, s.wl, shard_b_.data(), xs_))
         return fail(HP_ERR_COMM, comm_->error());
       prof_end(xs_, 4.0 * (P + n), 4.0 * (P + n), (1 << 16) | (127 << 24) | (int)(1u << 31));
+      note_pulls(bpull_);
     }
     nvl_bytes_ += 4.0 * n * (G_ - 1) + (pull ? 4.0 * (P - n) : 0.0);
   }
@@ -1175,6 +1220,8 @@ hp_status Engine::profile_enable(bool on) {
   prof_launch_bytes_.clear();
   prof_launch_sync_.clear();
   prof_launch_shape_.clear();
+  push_launch_.assign(N_, -1);
+  sync_recs_.clear();
   return HP_OK;
 }
 

@@ -95,6 +95,7 @@ class Engine {
   void stats(hp_stats* out) const;
   hp_status profile_enable(bool on);
   hp_status profile_read(double* ms, double* bytes, int64_t* launches);
+  hp_status profile_sync(int64_t max, float* ms, int32_t* vw, int64_t* n);
   hp_status profile_launches(int64_t max, float* ms, double* bytes, int32_t* shape,
                              double* sync_bytes, float* start_ms, int64_t* n);
   int64_t ticks = 0;
@@ -200,6 +201,16 @@ class Engine {
   std::vector<double> prof_launch_bytes_;
   std::vector<double> prof_launch_sync_;
   std::vector<int32_t> prof_launch_shape_;
+  // wave-sync latency: profiled launch that carried VW v's wave-end COMPLETE
+  // (its u~ final = the push) -> the launch that wrote its pulled w_local
+  std::vector<int64_t> push_launch_;
+  struct SyncRec {
+    int32_t v;
+    int64_t from, to;
+  };
+  std::vector<SyncRec> sync_recs_;
+  void note_sync(const TickDesc& d);
+  void note_pulls(const std::vector<int>& vws);
   int64_t prof_launches_ = 0;
 
   std::string trace_;

@@ -87,6 +87,8 @@ EXPORTS = {
     "hp_profile_launches": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.POINTER(C.c_int64)]),
+    "hp_profile_sync_latency": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                          C.POINTER(C.c_int64)]),
     "hp_s_global": (C.c_int64, [C.c_int32, C.c_int32]),
     "hp_version_floor": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
     "hp_last_error": (C.c_char_p, [C.c_void_p]),
@@ -306,6 +308,18 @@ def _profile_launches(self, max_records: int = 1 << 16):
 
 
 Context.profile_launches = _profile_launches
+
+
+def _profile_sync_latency(self, max_records: int = 1 << 16):
+    ms = np.zeros(max_records, dtype=np.float32)
+    vw = np.zeros(max_records, dtype=np.int32)
+    n = C.c_int64()
+    self._chk(self.lib.hp_profile_sync_latency(self.h, max_records, ms.ctypes.data_as(C.c_void_p),
+                                               vw.ctypes.data_as(C.c_void_p), C.byref(n)))
+    return ms[:n.value], vw[:n.value]
+
+
+Context.profile_sync_latency = _profile_sync_latency
 
 
 def comm_unique_id(lib: Optional[C.CDLL] = None) -> bytes:

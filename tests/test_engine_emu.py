@@ -86,3 +86,22 @@ def test_same_tick_pushes_out_of_complete_order(hp, seed):
         assert np.array_equal(wg, o.wg)
         for v in range(cfg.num_vw):
             assert np.array_equal(wl[v], o.wl[v])
+
+
+@pytest.mark.parametrize("cfg", [C1, C1_SKEW, C2.replace(nparams=999, waves=6)],
+                         ids=["C1", "C1-skew", "C2"])
+def test_sync_latency_records(hp, cfg):
+    """hp_profile_sync_latency: one record per (VW, wave) whose push and pull
+    fall in the profile window -- under EAGER every admission after a push
+    pulls, so the records equal the pulls, each VW's in wave order."""
+    from paper_2005_14038_b200 import hetpipe
+    ctx = hetpipe.Context(hetpipe.config_from(cfg), lib=hp.lib)
+    ctx.profile_enable(True)
+    ctx.run_schedule(cfg.tau, cfg.latency())
+    ms, vw = ctx.profile_sync_latency()
+    st = ctx.stats()
+    assert len(ms) == sum(st.pulls[:cfg.num_vw])
+    for v in range(cfg.num_vw):
+        assert int((vw == v).sum()) == st.pulls[v]
+    assert np.all(ms >= 0)
+    ctx.close()
