@@ -122,9 +122,12 @@ def main():
         (c5e, 1, "sample", "nccl", False, True),
         (c5e, 1, "sample", "nvls", False, True),
         (c5e, 1, "sample", "peer", True, False),
-        # not lockstep (mixed speeds): the NVLS context takes the PEER path, bit-exact
-        (C5.replace(waves=3, D=4, num_vw=G, tau=(250, 330, 346, 421)[:G], momentum=0.0,
-                    nparams=40_000), 1, None, "nvls", True, False),
+        # never lockstep (heavy-ball momentum is per push, Z11): the NVLS and NCCL
+        # contexts take the PEER path for every batch, bit-exact
+        (C5.replace(waves=3, D=4, num_vw=G, tau=C5.tau[:G], nparams=40_000), 1, None, "nvls",
+         True, False),
+        (C5.replace(waves=3, D=4, num_vw=G, tau=C5.tau[:G], nparams=40_000), 1, None, "nccl",
+         True, False),
     ]
     ok = True
     for cfg, k, mode, xport, exact, want_lock in cases:
