@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-from workloads import CONFIGS, GRAD_EXTERNAL  # noqa: E402
+from workloads import CONFIGS, GRAD_EXTERNAL, PMP_SOURCE  # noqa: E402
 
 METRIC = "synced params/sec"
 UNIT = "params/s"
@@ -218,6 +218,10 @@ def main():
                     help="exchange of lockstep batches (distributed placements; include/hetpipe.h "
                          "HP_XPORT_*): peer = fused NVLink loads, nccl = reduce-scatter/all-gather "
                          "baseline, nvls = multimem through the NVSwitch")
+    ap.add_argument("--timing", default="proxy", choices=["proxy", "pmp"],
+                    help="per-VW tau/L: the speed proxy (reading Z14) or derived from "
+                         "partitioning the model over each VW's GPUs and simulating its "
+                         "pipeline (hp_partition + hp_pipeline_tau_latency, NEXT-1)")
     ap.add_argument("--num-vw", type=int, default=0,
                     help="override the config's VW count (C5E defaults to one VW per GPU)")
     ap.add_argument("--span", type=int, default=0,
@@ -229,6 +233,11 @@ def main():
     nvw = args.num_vw or (int(os.environ.get("WORLD_SIZE", "1")) if cfg.name == "C5E" else 0)
     if nvw:
         cfg = cfg.replace(num_vw=nvw, tau=tuple((list(cfg.tau) * 8)[:nvw]))
+    if args.timing == "pmp":
+        from paper_2005_14038_b200 import schedule
+        model, vws = PMP_SOURCE[cfg.name]
+        tau, lat = schedule.policy_timing(model, "", cfg.Nm, vws[:cfg.num_vw])
+        cfg = cfg.replace(tau=tau, lat=lat)
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -419,7 +428,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "num_vw": N, "Nm": cfg.Nm, "D": cfg.D,
-                   "nparams": cfg.nparams, "tau": list(cfg.tau), "placement":
+                   "nparams": cfg.nparams, "tau": list(cfg.tau),
+                   "lat": list(cfg.latency()), "timing": args.timing, "placement":
                    (f"distributed, {args.span} GPU(s) per VW, PS sharded over {ws}" if placed
                     else "ED-local shards" if ws > 1 else "single GPU"),
                    "grad": "Philox FLOAT in-kernel", "pull": "EAGER", "local": "STRICT",

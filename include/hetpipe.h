@@ -273,6 +273,58 @@ hp_status hp_profile_launches(hp_ctx* ctx, int64_t max, float* ms, double* alg_b
    its gate includes the wait). ms[i], vw[i]; *n = records written. */
 hp_status hp_profile_sync_latency(hp_ctx* ctx, int64_t max, float* ms, int32_t* vw, int64_t* n);
 
+/* ---- Intra-VW pipeline schedule (section 4; no context).
+   The upstream generator of the controller's per-VW timing (tau_v, L_v of
+   hp_schedule_begin). Times are integer nanoseconds (round-half-even). */
+typedef struct {
+  int64_t params;        /* parameters of the unit (a layer, or a ResNet block) */
+  int64_t fwd_flops;     /* forward FLOPs per sample */
+  int64_t act_out;       /* fp32 elements per sample leaving the unit (crosses a cut) */
+  int64_t act_resident;  /* fp32 elements per sample kept until its backward pass */
+} hp_unit;
+typedef struct {
+  double flops_per_s;    /* effective training FLOP/s of this GPU */
+  double mem_bytes;      /* memory capacity */
+  int32_t node;          /* GPUs of one node talk over intra_bps, else inter_bps */
+  int32_t reserved;
+} hp_gpu;
+/* Min-max partition of units[0..L) over the k GPUs of a VW: every
+   stage is a contiguous unit range; every GPU order is tried. Stage q (0-based,
+   in pipeline order) costs fwd = FLOPs x batch / flops_per_s, bwd = 2 x fwd,
+   plus the activation arriving from stage q-1 and the gradient arriving from
+   stage q+1 (act_out x 4 x batch over the link between the two GPUs); it must
+   fit 3 x 4 x params + min(Nm, 2(k-1-q)+1) x 4 x batch x resident bytes in
+   mem_bytes ("the memory requirement will vary depending on the stage",
+   P:783). Minimises the largest stage time; ties go to the lexicographically
+   smallest (GPU order, cuts). Outputs (each may be NULL): order_out[k] (index
+   into gpus of stage q), cuts_out[k+1] (stage q = units [cuts[q], cuts[q+1])),
+   stage_costs_out[4k] (fwd, bwd, comm_in_fwd, comm_in_bwd ns per stage),
+   *bottleneck_ns. Returns HP_WOULD_BLOCK (not an error) when no split fits the
+   memory, HP_ERR_INVALID on bad arguments (k > 8, k > L, ...). */
+hp_status hp_partition(const hp_unit* units, int32_t L, const hp_gpu* gpus, int32_t k,
+                       int32_t Nm, int32_t batch, double intra_bps, double inter_bps,
+                       int32_t* order_out, int32_t* cuts_out, int64_t* stage_costs_out,
+                       int64_t* bottleneck_ns);
+/* Max_m: the largest Nm in [1, 2k-1] with a feasible partition, 0
+   if even Nm = 1 does not fit. */
+int32_t hp_max_m(const hp_unit* units, int32_t L, const hp_gpu* gpus, int32_t k, int32_t batch,
+                 double intra_bps, double inter_bps);
+/* Event-driven pipeline of one VW over P minibatches: per GPU
+   forward tasks in minibatch order (condition 1), backward tasks in minibatch
+   order (2), FIFO among ready tasks (3; ties: backward first, lower minibatch
+   first); the last stage runs forward+backward as one task; minibatch p
+   starts at 0 if p <= Nm, else when p-Nm completes (local staleness Nm-1,
+   P:817); p completes when its backward pass leaves stage 0 (u_p exists).
+   stage_costs[4k] as hp_partition's output. start_out/complete_out: int64[P]
+   (either may be NULL). */
+hp_status hp_pipeline_simulate(const int64_t* stage_costs, int32_t k, int32_t Nm, int64_t P,
+                               int64_t* start_out, int64_t* complete_out);
+/* The tick model's two numbers from that simulation (reading Z13): tau = the
+   mean completion interval over the middle half of a P-minibatch run (P <= 0:
+   24 Nm; floor), latency = minibatch 1's start-to-complete time. */
+hp_status hp_pipeline_tau_latency(const int64_t* stage_costs, int32_t k, int32_t Nm, int64_t P,
+                                  int64_t* tau_ns, int64_t* latency_ns);
+
 /* Closed forms of section 5 (no context needed). */
 int64_t hp_s_global(int32_t Nm, int32_t D);                  /* (D+1)*Nm + Nm - 2 */
 int64_t hp_version_floor(int64_t p, int32_t Nm, int32_t D);  /* max(0, p - s_global - 1) */

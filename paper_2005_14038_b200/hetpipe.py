@@ -46,6 +46,16 @@ class hp_stats(C.Structure):
                 ("lockstep_batches", C.c_int64)]
 
 
+class hp_unit(C.Structure):
+    _fields_ = [("params", C.c_int64), ("fwd_flops", C.c_int64), ("act_out", C.c_int64),
+                ("act_resident", C.c_int64)]
+
+
+class hp_gpu(C.Structure):
+    _fields_ = [("flops_per_s", C.c_double), ("mem_bytes", C.c_double), ("node", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
 class HetPipeError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
@@ -89,6 +99,15 @@ EXPORTS = {
                                       C.POINTER(C.c_int64)]),
     "hp_profile_sync_latency": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                           C.POINTER(C.c_int64)]),
+    "hp_partition": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                               C.c_int32, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_void_p]),
+    "hp_max_m": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                             C.c_double, C.c_double]),
+    "hp_pipeline_simulate": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_void_p,
+                                       C.c_void_p]),
+    "hp_pipeline_tau_latency": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64,
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "hp_s_global": (C.c_int64, [C.c_int32, C.c_int32]),
     "hp_version_floor": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
     "hp_last_error": (C.c_char_p, [C.c_void_p]),
@@ -344,3 +363,72 @@ def s_global(Nm: int, D: int) -> int:
 
 def version_floor(p: int, Nm: int, D: int) -> int:
     return load().hp_version_floor(p, Nm, D)
+
+
+# ---- intra-VW pipeline schedule (include/hetpipe.h hp_partition & co.) -------
+def _units(units):
+    arr = (hp_unit * len(units))()
+    for i, u in enumerate(units):
+        arr[i] = hp_unit(u.params, u.fwd_flops, u.act_out, u.act_resident)
+    return arr
+
+
+def _gpus(gpus):
+    arr = (hp_gpu * len(gpus))()
+    for i, g in enumerate(gpus):
+        arr[i] = hp_gpu(g["flops"], g["mem"], g["node"], 0)
+    return arr
+
+
+def partition(units, gpus, Nm: int, batch: int = 32, intra_bps: float = 15.75e9,
+              inter_bps: float = 56e9 / 8, lib: Optional[C.CDLL] = None):
+    """(bottleneck_ns, order, cuts, stage_costs) or None if nothing fits.
+    units: objects with params/fwd_flops/act_out/act_resident; gpus: dicts
+    {"flops", "mem", "node"}."""
+    lib = lib if lib is not None else load()
+    k = len(gpus)
+    order = (C.c_int32 * k)()
+    cuts = (C.c_int32 * (k + 1))()
+    costs = (C.c_int64 * (4 * k))()
+    b = C.c_int64()
+    st = lib.hp_partition(_units(units), len(units), _gpus(gpus), k, Nm, batch, intra_bps,
+                          inter_bps, order, cuts, costs, C.byref(b))
+    if st == HP_WOULD_BLOCK:
+        return None
+    if st != HP_OK:
+        raise HetPipeError(st, "hp_partition: bad arguments")
+    return (b.value, tuple(order), tuple(cuts),
+            [tuple(costs[4 * q:4 * q + 4]) for q in range(k)])
+
+
+def max_m(units, gpus, batch: int = 32, intra_bps: float = 15.75e9,
+          inter_bps: float = 56e9 / 8, lib: Optional[C.CDLL] = None) -> int:
+    lib = lib if lib is not None else load()
+    return lib.hp_max_m(_units(units), len(units), _gpus(gpus), len(gpus), batch, intra_bps,
+                        inter_bps)
+
+
+def _costs(costs):
+    flat = [int(x) for c in costs for x in c]
+    return (C.c_int64 * len(flat))(*flat)
+
+
+def pipeline_simulate(costs, Nm: int, P: int, lib: Optional[C.CDLL] = None):
+    """(start_ns[P], complete_ns[P]) of minibatches 1..P."""
+    lib = lib if lib is not None else load()
+    s = np.zeros(P, dtype=np.int64)
+    c = np.zeros(P, dtype=np.int64)
+    st = lib.hp_pipeline_simulate(_costs(costs), len(costs), Nm, P, s.ctypes.data_as(C.c_void_p),
+                                  c.ctypes.data_as(C.c_void_p))
+    if st != HP_OK:
+        raise HetPipeError(st, "hp_pipeline_simulate: bad arguments")
+    return s, c
+
+
+def pipeline_tau_latency(costs, Nm: int, P: int = 0, lib: Optional[C.CDLL] = None):
+    lib = lib if lib is not None else load()
+    t, l_ = C.c_int64(), C.c_int64()
+    st = lib.hp_pipeline_tau_latency(_costs(costs), len(costs), Nm, P, C.byref(t), C.byref(l_))
+    if st != HP_OK:
+        raise HetPipeError(st, "hp_pipeline_tau_latency: bad arguments")
+    return t.value, l_.value

@@ -105,3 +105,8 @@ def test_sync_latency_records(hp, cfg):
         assert int((vw == v).sum()) == st.pulls[v]
     assert np.all(ms >= 0)
     ctx.close()
+
+
+@pytest.mark.parametrize("D,policy", [(0, 0), (2, 0), (1, 1)])
+def test_pipeline_derived_timing(hp, D, policy):
+    G.test_pipeline_derived_timing(hp, D, policy)

@@ -279,3 +279,35 @@ def test_c4_sharded_ranks_sampled(hp):
         for v in range(cfg.num_vw):
             assert np.array_equal(ctx.read_weights(v)[idx - lo], o.wl[v])
         ctx.close()
+
+
+def pmp_timing_oracle(model, vws, Nm):
+    """(tau, lat) in microseconds from the ORACLE's partitioner and pipeline
+    simulator (oracle/pipeline.py), the same recipe as
+    paper_2005_14038_b200/schedule.py (whose native partitioner and simulator
+    tests/test_pipeline_schedule.py matches exactly)."""
+    from oracle import pipeline as op
+    from workloads import models as M
+    F = M.v_flops_per_s()
+    tau, lat = [], []
+    for types in vws:
+        g = [{"flops": F * M.GPUS[t].speed, "mem": M.GPUS[t].mem_gb * 1e9, "node": M.NODE_OF[t]}
+             for t in types]
+        b, order, cuts = op.partition_bruteforce(M.MODELS[model](), g, Nm)
+        costs = op.stage_costs(M.MODELS[model](), cuts, [g[i] for i in order])
+        t_ns, l_ns = op.derive_tau_latency(costs, Nm)
+        tau.append(max(1, round(t_ns / 1000)))
+        lat.append(max(1, round(l_ns / 1000)))
+    return tuple(tau), tuple(lat)
+
+
+@pytest.mark.parametrize("D,policy", [(0, 0), (2, 0), (1, 1)])
+def test_pipeline_derived_timing(hp, D, policy):
+    """NEXT-1: tau_v / L_v from partitioning VGG-19 over NP's four VW types
+    (VVVV, RRRR, GGGG, QQQQ) and simulating each VW's pipeline drive the tick
+    controller; the CUDA path still matches the oracle bit for bit."""
+    tau, lat = pmp_timing_oracle("vgg19", ("VVVV", "RRRR", "GGGG", "QQQQ"), 4)
+    cfg = C2.replace(nparams=4099, waves=8, D=D, tau=tau, lat=lat, pull_policy=policy)
+    o = run_schedule(cfg)
+    trace, wg, wl, _, _ = run_device(hp, cfg)
+    assert_same(o, trace, wg, wl)

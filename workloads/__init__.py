@@ -92,6 +92,17 @@ C5 = WSPConfig("C5", 8, 8, 0, VGG19_PARAMS, 132,
 C5E = WSPConfig("C5E", 8, 8, 0, VGG19_PARAMS, 132, (325,) * 8)
 CONFIGS = {c.name: c for c in (C1, C1_SKEW, C2, C3, C4, C5, C5E)}
 
+# Model and VW GPU types behind each config, for the pipeline-derived timing
+# (tau_v, L_v from partitioning the model over the VW's
+# GPUs, replacing the speed proxy; workloads/models.py holds the tables).
+PMP_SOURCE = {
+    "C2": ("resnet152", ("VVVV", "RRRR", "GGGG", "QQQQ")),          # NP
+    "C3": ("resnet152", ("VVQQ", "VVQQ", "RRGG", "RRGG")),          # HD
+    "C4": ("vgg19", ("VRGQ",) * 4),                                 # ED
+    "C5": ("vgg19", ("VVVV", "VVVV", "RRRR", "RRRR", "GGGG", "GGGG", "QQQQ", "QQQQ")),
+    "C5E": ("vgg19", ("VRGQ",) * 8),
+}
+
 
 def even_shards(nparams: int, nshards: int, align: int = 32) -> Sequence[int]:
     """Shard boundaries b_0=0 < ... < b_G = nparams, inner ones multiples of
