@@ -222,6 +222,10 @@ def main():
                     help="per-VW tau/L: the speed proxy (reading Z14) or derived from "
                          "partitioning the model over each VW's GPUs and simulating its "
                          "pipeline (hp_partition + hp_pipeline_tau_latency, NEXT-1)")
+    ap.add_argument("--ps", default="even", choices=["even", "layer_rr"],
+                    help="PS shard boundaries of the distributed placements: even (reading Z12) "
+                         "or the paper's default layer round-robin (P:100-103) on the config's "
+                         "model (uneven shards; hp_config.ps_bounds)")
     ap.add_argument("--num-vw", type=int, default=0,
                     help="override the config's VW count (C5E defaults to one VW per GPU)")
     ap.add_argument("--span", type=int, default=0,
@@ -230,7 +234,8 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
-    nvw = args.num_vw or (int(os.environ.get("WORLD_SIZE", "1")) if cfg.name == "C5E" else 0)
+    nvw = args.num_vw or (int(os.environ.get("WORLD_SIZE", "1")) if cfg.name in ("C5E", "HVD")
+                          else 0)
     if nvw:
         cfg = cfg.replace(num_vw=nvw, tau=tuple((list(cfg.tau) * 8)[:nvw]))
     if args.timing == "pmp":
@@ -273,14 +278,18 @@ def main():
     placed = ws > 1 and args.span > 0
     keep = None
     xport = {"peer": 0, "nccl": 1, "nvls": 2}[args.transport]
+    extra = {}
+    if placed and args.ps == "layer_rr":
+        from workloads import models as wm
+        extra["ps_bounds"] = wm.layer_rr_bounds(wm.MODELS[PMP_SOURCE[cfg.name][0]](), ws)
     if placed and args.transport == "nvls":
         ctx, keep = hdist.symmetric_context(run_cfg, rank, ws, args.span, device=local,
                                             stream=stream.cuda_stream, merge_ticks=args.merge_ticks,
-                                            apply_mode=args.apply_mode, transport=xport)
+                                            apply_mode=args.apply_mode, transport=xport, **extra)
     elif placed:
         ctx = hdist.placed_context(run_cfg, rank, ws, args.span, device=local,
                                    stream=stream.cuda_stream, merge_ticks=args.merge_ticks,
-                                   apply_mode=args.apply_mode, transport=xport)
+                                   apply_mode=args.apply_mode, transport=xport, **extra)
     else:
         ctx = hdist.rank_context(run_cfg, rank, ws, device=local, stream=stream.cuda_stream,
                                  merge_ticks=args.merge_ticks, apply_mode=args.apply_mode)
@@ -435,6 +444,7 @@ def main():
                    "grad": "Philox FLOAT in-kernel", "pull": "EAGER", "local": "STRICT",
                    "apply": "on arrival" if args.apply_mode else "deferred to the observing pull",
                    "transport": args.transport if placed else None,
+                   "ps_shards": args.ps if placed else None,
                    "lockstep_batches": lock_batches if placed else None,
                    "l2": "inputs larger than L2 (>= 13 x 230 MiB buffers per GPU)"},
         "images_per_sec_equiv": commits * 32 * cfg.Nm / (ms_max / 1e3),

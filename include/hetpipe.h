@@ -113,6 +113,13 @@ typedef struct {
   void* stream;            /* cudaStream_t to run on; NULL = library-owned stream */
   int32_t transport;       /* HP_XPORT_* (world > 1): exchange of lockstep batches */
   int32_t reserved;
+  const int64_t* ps_bounds;/* optional PS shard boundaries (world > 1): world+1 values,
+                              0 = b[0] < b[1] < ... < b[world] = nparams, inner ones
+                              multiples of 32; shard q = [b[q], b[q+1]) on GPU q.
+                              NULL = even split (reading Z12). Read during
+                              hp_init_ex / hp_arena_bytes only (copied). Uneven
+                              bounds express e.g. the paper's layer round-robin
+                              placement on a permuted parameter order */
   void* arena;             /* optional caller-owned device arena of >= hp_arena_bytes()
                               bytes, 256-byte aligned, BORROWED for the context's
                               lifetime (e.g. a torch symmetric-memory buffer whose peer

@@ -187,6 +187,13 @@ const char* validate(hp_config& cfg) {
     bad = "world > 1 places the whole model: param_begin 0, param_count -1";
   else if (cfg.world > 1 && cfg.grad_mode == HP_GRAD_EXTERNAL) bad = "EXTERNAL gradients need world 1";
   else if (cfg.transport < 0 || cfg.transport > 2) bad = "bad transport";
+  if (!bad && cfg.world > 1 && cfg.ps_bounds) {
+    const int64_t* b = cfg.ps_bounds;
+    if (b[0] != 0 || b[cfg.world] != cfg.nparams) bad = "ps_bounds must span [0, nparams]";
+    for (int q = 1; q <= cfg.world && !bad; ++q)
+      if (b[q] <= b[q - 1] || (q < cfg.world && b[q] % 32))
+        bad = "ps_bounds must increase, inner bounds multiples of 32";
+  }
   return bad;
 }
 }  // namespace

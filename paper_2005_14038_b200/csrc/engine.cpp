@@ -119,7 +119,8 @@ hp_status Engine::check_cuda(int err, const char* what) {
 
 void Engine::plan_layout() {
   if (dist_) {
-    shard_b_ = even_bounds(cfg_.nparams, G_);
+    if (cfg_.ps_bounds) shard_b_.assign(cfg_.ps_bounds, cfg_.ps_bounds + G_ + 1);
+    else shard_b_ = even_bounds(cfg_.nparams, G_);
     stage_b_ = even_bounds(cfg_.nparams, span_);
   } else {
     shard_b_ = {begin_, begin_ + n_};
@@ -142,6 +143,7 @@ hp_status Engine::init() {
   // Single-rank contexts own [param_begin, +param_count) of every buffer; with
   // world > 1 the placement layout decides (layout_of).
   plan_layout();
+  cfg_.ps_bounds = nullptr;          // borrowed for hp_init_ex only (copied)
   for (int q = 0; q < G_; ++q) lay_.push_back(layout_of(q));
   const RankLayout& L = lay_[rank_];
   if (cfg_.arena) {

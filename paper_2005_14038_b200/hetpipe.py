@@ -32,7 +32,8 @@ class hp_config(C.Structure):
                 ("apply_mode", C.c_int32), ("acc_slots", C.c_int32),
                 ("merge_ticks", C.c_int32), ("world", C.c_int32), ("rank", C.c_int32),
                 ("vw_span", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p),
-                ("transport", C.c_int32), ("reserved", C.c_int32), ("arena", C.c_void_p)]
+                ("transport", C.c_int32), ("reserved", C.c_int32), ("ps_bounds", C.c_void_p),
+                ("arena", C.c_void_p)]
 
 XPORT_PEER, XPORT_NCCL, XPORT_NVLS = 0, 1, 2
 XPORTS = {"peer": XPORT_PEER, "nccl": XPORT_NCCL, "nvls": XPORT_NVLS}
@@ -150,8 +151,14 @@ def config_from(cfg, **overrides) -> hp_config:
     c.lr, c.momentum, c.seed = cfg.lr, cfg.momentum, cfg.seed
     c.grad_mode, c.w0_mode = cfg.grad_mode, cfg.w0_mode
     c.pull_policy, c.local_semantics = cfg.pull_policy, cfg.local_semantics
+    bounds = overrides.pop("ps_bounds", None)
     for k, v in overrides.items():
         setattr(c, k, v)
+    if bounds is not None:
+        arr = (C.c_int64 * len(bounds))(*[int(x) for x in bounds])
+        c._ps_keep = arr                       # alive as long as the config
+        c._ps_list = [int(x) for x in bounds]
+        c.ps_bounds = C.cast(arr, C.c_void_p)
     if c.param_count < 0:
         c.param_count = c.nparams - c.param_begin
     return c
@@ -264,7 +271,7 @@ class Context:
         if c.world <= 1:
             return c.param_count
         if which < 0:
-            b = even_shards(c.nparams, c.world)
+            b = getattr(c, "_ps_list", None) or even_shards(c.nparams, c.world)
             return b[c.rank + 1] - b[c.rank]
         for j in range(c.vw_span):
             if (which * c.vw_span + j) % c.world == c.rank:

@@ -18,18 +18,22 @@ from oracle import run_schedule  # noqa: E402
 from paper_2005_14038_b200 import dist as hdist  # noqa: E402
 from workloads import C3, C4, C5, C5E, GRAD_DYADIC, WSPConfig, sample_indices, even_shards  # noqa: E402
 
+from workloads import models as M  # noqa: E402
+
 XPORT = {"peer": 0, "nccl": 1, "nvls": 2}
 
 
-def run(cfg, G, k, rank, local, sampled, transport="peer"):
+def run(cfg, G, k, rank, local, sampled, transport="peer", bounds=None):
     stream = torch.cuda.Stream(local)
     keep = None
+    extra = {"ps_bounds": bounds} if bounds else {}
     if transport == "nvls":
         ctx, keep = hdist.symmetric_context(cfg, rank, G, k, device=local,
-                                            stream=stream.cuda_stream, transport=XPORT["nvls"])
+                                            stream=stream.cuda_stream, transport=XPORT["nvls"],
+                                            **extra)
     else:
         ctx = hdist.placed_context(cfg, rank, G, k, device=local, stream=stream.cuda_stream,
-                                   transport=XPORT[transport])
+                                   transport=XPORT[transport], **extra)
     ctx.run_schedule(cfg.tau, cfg.latency())
     with tempfile.NamedTemporaryFile(suffix=".trace") as f:
         tr = ctx.trace_lines(f.name)
@@ -44,7 +48,7 @@ def run(cfg, G, k, rank, local, sampled, transport="peer"):
     ctx.close()
     del keep
     if sampled is not None:      # ship only sampled entries (full arrays are GBs)
-        sb = even_shards(cfg.nparams, G)
+        sb = bounds or even_shards(cfg.nparams, G)
         lo = sb[rank]
         wg = {int(i): float(wg[i - lo]) for i in sampled if sb[rank] <= i < sb[rank + 1]}
         m = None if m is None else {int(i): float(m[i - lo]) for i in sampled if sb[rank] <= i < sb[rank + 1]}
@@ -122,6 +126,10 @@ def main():
         (c5e, 1, "sample", "nccl", False, True),
         (c5e, 1, "sample", "nvls", False, True),
         (c5e, 1, "sample", "peer", True, False),
+        # the paper's default layer round-robin PS placement: uneven shards
+        (c5e, 1, "sample", "nvls", False, True, "layer_rr"),
+        (C5.replace(waves=2, D=4, num_vw=G, tau=C5.tau[:G]), 1, "sample", "peer", True, False,
+         "layer_rr"),
         # never lockstep (heavy-ball momentum is per push, Z11): the NVLS and NCCL
         # contexts take the PEER path for every batch, bit-exact
         (C5.replace(waves=3, D=4, num_vw=G, tau=C5.tau[:G], nparams=40_000), 1, None, "nvls",
@@ -130,11 +138,14 @@ def main():
          True, False),
     ]
     ok = True
-    for cfg, k, mode, xport, exact, want_lock in cases:
+    for case in cases:
+        cfg, k, mode, xport, exact, want_lock = case[:6]
         if cfg is None:
             continue
-        sampled = sample_indices(cfg.nparams, 104729, even_shards(cfg.nparams, G)) if mode else None
-        objs = run(cfg, G, k, rank, local, sampled, xport)
+        bounds = (M.layer_rr_bounds(M.vgg19(), G) if len(case) > 6 else None)
+        sampled = (sample_indices(cfg.nparams, 104729, bounds or even_shards(cfg.nparams, G))
+                   if mode else None)
+        objs = run(cfg, G, k, rank, local, sampled, xport, bounds)
         if rank == 0:
             try:
                 check(cfg, G, k, objs, sampled, exact)

@@ -115,3 +115,45 @@ def test_placement_random(lib, seed):
     out = run_placement(lib, cfg, G, k, merge_ticks=rng.randint(0, 1),
                         acc_slots=rng.choice([2, 3]), apply_mode=rng.randint(0, 1))
     check(cfg, G, k, out)
+
+
+def rand_bounds(rng, P, G):
+    inner = sorted(rng.sample(range(1, P // 32), G - 1))
+    return [0] + [32 * x for x in inner] + [P]
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_uneven_ps_shards(lib, seed):
+    """hp_config.ps_bounds: uneven PS shards (e.g. the paper's layer
+    round-robin placement) change where each apply runs and what a
+    pull reads, never the result."""
+    rng = random.Random(500 + seed)
+    G = rng.choice([2, 3, 4])
+    k = rng.choice([1, G])
+    N = rng.randint(1, 4)
+    cfg = WSPConfig("ub", N, rng.randint(1, 3), rng.randint(0, 2), rng.choice([2048, 4099]),
+                    rng.randint(2, 5), tuple(rng.randint(1, 9) for _ in range(N)),
+                    momentum=rng.choice([0.0, 0.9]))
+    b = rand_bounds(rng, cfg.nparams, G)
+    out = run_placement(lib, cfg, G, k, ps_bounds=b)
+    check(cfg, G, k, out)
+    for r in range(G):
+        assert len(out[r][1]) == b[r + 1] - b[r]
+
+
+def test_layer_round_robin_bounds():
+    from workloads import models as M
+    b = M.layer_rr_bounds(M.vgg19(), 8)
+    # fc6 (71.5% of VGG-19) makes one PS shard hold ~72% of the model
+    # (SURVEY.md 8(f) NEXT-3; the paper's default placement, P:100-103)
+    assert abs((b[1] - b[0]) / b[-1] - 0.724) < 0.002
+    assert b[-1] == 143_667_240 and all(x % 32 == 0 for x in b[1:-1])
+
+
+def test_bad_ps_bounds(lib):
+    from paper_2005_14038_b200 import hetpipe
+    cfg = C3.replace(nparams=4099, waves=2)
+    for bad in ([0, 100, 4099], [0, 4096, 4000], [1, 2048, 4099], [0, 2048, 4098]):
+        with pytest.raises(hetpipe.HetPipeError):
+            hetpipe.Context(hetpipe.config_from(cfg, world=2, rank=0, vw_span=1, ps_bounds=bad),
+                            lib=lib)

@@ -140,6 +140,17 @@ def test_non_lockstep_falls_back_to_peer(lib, transport):
     assert out[0][3].lockstep_batches == 0
 
 
+@pytest.mark.parametrize("transport", [NCCL, NVLS], ids=["nccl", "nvls"])
+def test_lockstep_uneven_shards(lib, transport):
+    # layer-round-robin-like uneven PS shards: the reduce-scatter / all-gather
+    # (grouped per shard) and the per-owner NVLS ranges follow the bounds
+    cfg = lockstep_cfg(3, 2, 0, 4099, 5, GRAD_DYADIC)
+    out = run_transport(lib, cfg, 3, transport, ps_bounds=[0, 2976, 3840, 4099])
+    check(cfg, 3, out, exact=True)
+    assert out[0][3].lockstep_batches == cfg.waves
+    assert [len(out[r][1]) for r in range(3)] == [2976, 864, 259]
+
+
 @pytest.mark.parametrize("seed", range(12))
 def test_lockstep_random(lib, seed):
     rng = random.Random(seed)

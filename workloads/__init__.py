@@ -90,7 +90,12 @@ C5 = WSPConfig("C5", 8, 8, 0, VGG19_PARAMS, 132,
 # NCCL / NVLS transports exchange (include/hetpipe.h HP_XPORT_*); one VW per GPU
 # (num_vw = G at run time).
 C5E = WSPConfig("C5E", 8, 8, 0, VGG19_PARAMS, 132, (325,) * 8)
-CONFIGS = {c.name: c for c in (C1, C1_SKEW, C2, C3, C4, C5, C5E)}
+# The Horovod analogue (Horovod is the paper's baseline,
+# P:203-226): the BSP limit of WSP (Nm = 1, D = 0, pin P8) with one VW per GPU
+# and equal speeds = synchronous data-parallel SGD, every minibatch a lockstep
+# batch (all-reduce through NCCL, or the NVLS kernel).
+HVD = WSPConfig("HVD", 8, 1, 0, VGG19_PARAMS, 132, (325,) * 8)
+CONFIGS = {c.name: c for c in (C1, C1_SKEW, C2, C3, C4, C5, C5E, HVD)}
 
 # Model and VW GPU types behind each config, for the pipeline-derived timing
 # (tau_v, L_v from partitioning the model over the VW's
@@ -101,6 +106,7 @@ PMP_SOURCE = {
     "C4": ("vgg19", ("VRGQ",) * 4),                                 # ED
     "C5": ("vgg19", ("VVVV", "VVVV", "RRRR", "RRRR", "GGGG", "GGGG", "QQQQ", "QQQQ")),
     "C5E": ("vgg19", ("VRGQ",) * 8),
+    "HVD": ("vgg19", ("V",) * 8),
 }
 
 

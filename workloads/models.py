@@ -148,3 +148,23 @@ def v_flops_per_s() -> float:
 
 def vw_gpus(policy: str, vw: int) -> List[Tuple[str, int]]:
     return [(t, NODE_OF[t]) for t in POLICIES[policy][vw]]
+
+
+def layer_rr_bounds(units: Sequence[Unit], G: int, align: int = 32) -> List[int]:
+    """PS shard boundaries of the paper's default placement ("we
+    place layers of the model in round-robin fashion over all the parameter
+    servers"): unit i goes to shard i mod G. With the parameters stored shard
+    by shard (a permutation of the model's order) every shard is one
+    contiguous range; inner boundaries are rounded to `align` floats."""
+    sizes = [0] * G
+    for i, u in enumerate(units):
+        sizes[i % G] += u.params
+    P = sum(sizes)
+    b, acc = [0], 0
+    for q in range(G - 1):
+        acc += sizes[q]
+        x = max(b[-1] + align, int(round(acc / align)) * align)
+        b.append(x)
+    b.append(P)
+    assert all(x < y for x, y in zip(b, b[1:]))
+    return b
