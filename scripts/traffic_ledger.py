@@ -1,0 +1,77 @@
+"""Traffic ledger: bytes each placement moves, next to
+the paper's printed figures (context: units not stated, reading
+Z19) and the B200 runs' measured NVLink ingress.
+
+    python scripts/traffic_ledger.py > profiles/r01_traffic_ledger.txt
+"""
+import glob
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2005_14038_b200 import hetpipe, schedule  # noqa: E402
+from workloads import models as M  # noqa: E402
+
+MB = 2 ** 20
+
+
+def horovod_bytes(params, n=16):
+    """Ring all-reduce: each GPU sends (n-1)/n of the model per reduce phase."""
+    return params * 4 * (n - 1) / n
+
+
+def ed_local_activation_bytes(model, Nm=4):
+    """ED (every VW = V,R,G,Q on four nodes): activations forward + gradients
+    backward crossing the node boundary at each of the 3 cuts, per minibatch,
+    with the partition hp_partition picks; the PS traffic is node-local."""
+    units = M.MODELS[model]()
+    b, order, cuts, _ = hetpipe.partition(units, schedule.vw_gpus("VRGQ"), Nm,
+                                          intra_bps=M.PCIE_BPS, inter_bps=M.IB_BPS)
+    return sum(2 * units[c - 1].act_out * M.BATCH * 4 for c in cuts[1:-1]), cuts
+
+
+def default_ps_bytes(model, G=4):
+    """Default placement (layer round-robin over one PS per node): a VW's push
+    + pull cross nodes for every shard not on the stage's node -- with ED each
+    stage's node holds 1/G of the shards' rotation, so ~ (G-1)/G of the model
+    crosses per push and per pull (per VW per wave)."""
+    P = sum(u.params for u in M.MODELS[model]())
+    return 2 * P * 4 * (G - 1) / G
+
+
+def main():
+    print("# Paper cluster (16 GPUs, 4 nodes; P:10-16), MB = 2^20 bytes")
+    for model, paper_hvd, paper_edl in (("vgg19", 515, 103), ("resnet152", 211, 298)):
+        P = sum(u.params for u in M.MODELS[model]())
+        edl, cuts = ed_local_activation_bytes(model)
+        print(f"{model}: params {P * 4 / MB:.1f} MB | Horovod ring (n-1)/n x params = "
+              f"{horovod_bytes(P) / MB:.1f} MB (paper {paper_hvd}) | ED-local activations across "
+              f"nodes per minibatch, cuts {list(cuts)} = {edl / MB:.1f} MB (paper {paper_edl}) | "
+              f"ED default PS push+pull per VW-wave ~ {default_ps_bytes(model) / MB:.1f} MB")
+    print()
+    print("# PS shard imbalance of the layer round-robin placement (largest shard / mean)")
+    for model in ("vgg19", "resnet152"):
+        for G in (2, 4, 8):
+            b = M.layer_rr_bounds(M.MODELS[model](), G)
+            big = max(b[i + 1] - b[i] for i in range(G))
+            print(f"{model} G={G}: largest shard {big / b[-1]:.3f} of the model = "
+                  f"{big * G / b[-1]:.2f} x mean")
+    print()
+    print("# B200 runs (profiles/r01_bench_*.json): measured NVLink ingress per rank per step")
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r01_bench_*g*.json"))):
+        try:
+            d = json.loads(open(f).read().strip().splitlines()[-1])
+        except Exception:
+            continue
+        c = d["config"]
+        nv = d.get("nvlink", {})
+        print(f"{os.path.basename(f)}: {c['workload']} N={c['num_vw']} G={d['n_gpus']} "
+              f"{c.get('placement')} transport={c.get('transport')} ps={c.get('ps_shards')}: "
+              f"{nv.get('bytes_per_step_max_rank', 0) / MB:.0f} MB/step, {d['ms_per_step']:.3f} ms/step")
+
+
+if __name__ == "__main__":
+    main()

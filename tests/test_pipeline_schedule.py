@@ -35,6 +35,9 @@ def test_model_tables_match_paper_sizes():
     # fc6 is 71.5% of VGG-19 (SURVEY.md 8(d) workload structure)
     assert abs(M.vgg19()[16].params / 143_667_240 - 0.715) < 0.001
     assert len(M.resnet152()) == 52 and len(M.vgg19()) == 19
+    # Horovod moves 515MB across the 16-GPU cluster for VGG-19 = a ring
+    # all-reduce's (n-1)/n of the 548 MB model (SURVEY.md reading Z19)
+    assert abs(143_667_240 * 4 * 15 / 16 / 2 ** 20 - 515) / 515 < 0.005
 
 
 def test_stage_depth_examples():
