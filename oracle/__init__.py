@@ -20,9 +20,9 @@ snapshots with D>0 and heterogeneous speeds are pinned only by conservation
 (see DESIGN.md "Parity pins").
 """
 from .philox import philox4x32_10, philox_words
-from .wsp import (OracleRun, WSPOracle, gradient, initial_weights, run_schedule,
-                  s_global, version_floor, wave_range)
+from .wsp import (OracleRun, WSPOracle, convex_target, gradient, initial_weights,
+                  run_schedule, s_global, version_floor, wave_range)
 
-__all__ = ["philox4x32_10", "philox_words", "OracleRun", "WSPOracle", "gradient",
-           "initial_weights", "run_schedule", "s_global", "version_floor",
+__all__ = ["philox4x32_10", "philox_words", "OracleRun", "WSPOracle", "convex_target",
+           "gradient", "initial_weights", "run_schedule", "s_global", "version_floor",
            "wave_range"]

@@ -33,7 +33,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from workloads import (GRAD_DYADIC, GRAD_FLOAT, LOCAL_AT_LEAST, LOCAL_STRICT,
+from workloads import (GRAD_CONVEX, GRAD_DYADIC, GRAD_FLOAT, LOCAL_AT_LEAST, LOCAL_STRICT,
                        PULL_EAGER, PULL_LAZY, W0_PHILOX, W0_ZERO, WSPConfig)
 
 from .philox import philox4x32_10
@@ -80,15 +80,31 @@ def _draws(idx: np.ndarray, vw: int, p: int, stream: int, seed: int) -> np.ndarr
     return table[inv, idx & 3]
 
 
-def gradient(idx: np.ndarray, vw: int, p: int, cfg: WSPConfig) -> np.ndarray:
+def gradient(idx: np.ndarray, vw: int, p: int, cfg: WSPConfig,
+             w: Optional[np.ndarray] = None) -> np.ndarray:
     """g(v,p,i) as float32. FLOAT: (x>>8)*2^-24 - 0.5 (exact, in [-0.5,0.5));
-    DYADIC: (x>>28) - 8 (integers -8..7)."""
+    DYADIC: (x>>28) - 8 (integers -8..7). CONVEX (NEXT-2, the weight-dependent
+    workload of SURVEY.md 8(f)): the gradient of f(w) = a/2 ||w - b||^2 at the
+    weights w = w_p minibatch p read at its START, plus noise:
+    g = fl(fl(a * fl(w - b)) + fl(sigma * xi)), xi = the FLOAT draw."""
     x = _draws(idx, vw, p, 0, cfg.seed)
     if cfg.grad_mode == GRAD_FLOAT:
         return ((x >> 8).astype(np.float64) * 2.0 ** -24 - 0.5).astype(F32)
     if cfg.grad_mode == GRAD_DYADIC:
         return ((x >> 28).astype(np.int64) - 8).astype(F32)
-    raise ValueError("oracle supports FLOAT and DYADIC gradients only")
+    if cfg.grad_mode == GRAD_CONVEX:
+        assert w is not None, "CONVEX gradients need w_p"
+        xi = ((x >> 8).astype(np.float64) * 2.0 ** -24 - 0.5).astype(F32)
+        d = w - convex_target(idx, cfg)
+        return (F32(cfg.conv_a) * d) + (F32(cfg.conv_sigma) * xi)
+    raise ValueError("oracle supports FLOAT, DYADIC and CONVEX gradients only")
+
+
+def convex_target(idx: np.ndarray, cfg: WSPConfig) -> np.ndarray:
+    """b of the CONVEX workload: Philox stream 2, counter (i>>2, 0, 0, 2),
+    2*((x>>8)*2^-24) - 1 in [-1, 1) (exact in float32)."""
+    x = _draws(idx, 0, 0, 2, cfg.seed)
+    return (2.0 * ((x >> 8).astype(np.float64) * 2.0 ** -24) - 1.0).astype(F32)
 
 
 def initial_weights(idx: np.ndarray, cfg: WSPConfig) -> np.ndarray:
@@ -102,9 +118,10 @@ def initial_weights(idx: np.ndarray, cfg: WSPConfig) -> np.ndarray:
     return (2.0 * ((x >> 8).astype(np.float64) * 2.0 ** -24) - 1.0).astype(F32)
 
 
-def update(idx: np.ndarray, vw: int, p: int, cfg: WSPConfig) -> np.ndarray:
+def update(idx: np.ndarray, vw: int, p: int, cfg: WSPConfig,
+           w: Optional[np.ndarray] = None) -> np.ndarray:
     """u_p = fl(-lr * g_p): one float32 rounding (Z2, Z10)."""
-    return F32(-cfg.lr) * gradient(idx, vw, p, cfg)
+    return F32(-cfg.lr) * gradient(idx, vw, p, cfg, w)
 
 
 # --------------------------------------------------------------------------- #
@@ -145,6 +162,9 @@ class WSPOracle:
         self.record_snapshots = record_snapshots
         self.snapshots: List[Tuple[int, int, int, np.ndarray]] = []
         self.start_versions: List[Tuple[int, int, int, int]] = []  # (v, p, a_v, held_K)
+        # CONVEX: w_p, the w_local minibatch p read at its START, until u_p's
+        # last use (its COMPLETE and its fold)
+        self.w_at_start: List[Dict[int, np.ndarray]] = [dict() for _ in range(N)]
 
     # -- helpers ---------------------------------------------------------------
     @property
@@ -157,7 +177,11 @@ class WSPOracle:
                           f"{self.held_K[v]}")
 
     def _u(self, v: int, p: int) -> np.ndarray:
-        return update(self.idx, v, p, self.cfg)
+        return update(self.idx, v, p, self.cfg, self.w_at_start[v].get(p))
+
+    def _folded(self, v: int, p: int) -> None:
+        """u_p's fold happened (its COMPLETE came first): w_p is dead."""
+        self.w_at_start[v].pop(p, None)
 
     # -- events ----------------------------------------------------------------
     def start(self, t: int, v: int, p: int, phase: str = "S") -> None:
@@ -169,6 +193,8 @@ class WSPOracle:
         self.started[v] = p
         self._rec(t, phase, v, "START", p, wave_of(p, cfg.Nm))
         self.start_versions.append((v, p, self.a[v], self.held_K[v]))
+        if cfg.grad_mode == GRAD_CONVEX:
+            self.w_at_start[v][p] = self.wl[v].copy()     # the forward pass reads w_p
         if self.record_snapshots:
             self.snapshots.append((t, v, p, self.wl[v].copy()))
 
@@ -190,12 +216,14 @@ class WSPOracle:
         if not self.at_gate[v]:
             self.wl[v] = self.wl[v] + u          # w_local = w_local + u_p
             self.a[v] = p
+            self._folded(v, p)
             start_next = (not wave_end) and p + Nm <= self.last_p
         else:                                    # waiting at the gate (Z17)
             self.backlog[v].append(p)
             if cfg.local_semantics == LOCAL_AT_LEAST:
                 self.wl[v] = self.wl[v] + u
                 self.a[v] = p
+                self._folded(v, p)
         self._rec(t, "C", v, "COMPLETE", p, wave_of(p, Nm))
         return wave_end, start_next
 
@@ -269,6 +297,7 @@ class WSPOracle:
             if cfg.local_semantics == LOCAL_STRICT:
                 self.wl[v] = self.wl[v] + self._u(v, q)      # deferred fold (Z3)
                 self.a[v] = q
+                self._folded(v, q)
                 self._rec(t, "G", v, "FOLD", q, wave_of(q, cfg.Nm))
             if q + cfg.Nm <= self.last_p:
                 self.start(t, v, q + cfg.Nm, phase="G")

@@ -26,6 +26,9 @@ SEED = 200514038
 GRAD_FLOAT = 0      # g = (x>>8) * 2^-24 - 0.5, uniform in [-0.5, 0.5)
 GRAD_DYADIC = 1     # g = (x>>28) - 8, integers in {-8..7}
 GRAD_EXTERNAL = 2   # caller-supplied gradient buffers (CUDA path only)
+GRAD_CONVEX = 3     # g = a * (w_p - b) + sigma * xi: weight-dependent (NEXT-2), w_p =
+                    # w_local at START(p), b = Philox stream 2 in [-1, 1), xi the FLOAT
+                    # draw of stream 0 in [-0.5, 0.5)
 
 # w0_mode
 W0_ZERO = 0
@@ -65,6 +68,8 @@ class WSPConfig:
     pull_policy: int = PULL_EAGER
     local_semantics: int = LOCAL_STRICT
     lat: Optional[Tuple[int, ...]] = None   # fill latency per VW; None -> Nm * tau
+    conv_a: float = 0.5                     # GRAD_CONVEX curvature a
+    conv_sigma: float = 1.0                 # GRAD_CONVEX noise scale sigma
 
     def latency(self) -> Tuple[int, ...]:
         if self.lat is not None:
