@@ -226,6 +226,10 @@ def main():
                     help="PS shard boundaries of the distributed placements: even (reading Z12) "
                          "or the paper's default layer round-robin (P:100-103) on the config's "
                          "model (uneven shards; hp_config.ps_bounds)")
+    ap.add_argument("--grad", default="float", choices=["float", "convex"],
+                    help="synthetic gradient: weight-independent Philox FLOAT draws, or the "
+                         "weight-dependent CONVEX workload (NEXT-2: every gradient reads the "
+                         "w_local its minibatch saw at START, kept in a stash ring)")
     ap.add_argument("--num-vw", type=int, default=0,
                     help="override the config's VW count (C5E defaults to one VW per GPU)")
     ap.add_argument("--span", type=int, default=0,
@@ -238,6 +242,9 @@ def main():
                           else 0)
     if nvw:
         cfg = cfg.replace(num_vw=nvw, tau=tuple((list(cfg.tau) * 8)[:nvw]))
+    if args.grad == "convex":
+        from workloads import GRAD_CONVEX
+        cfg = cfg.replace(grad_mode=GRAD_CONVEX)
     if args.timing == "pmp":
         from paper_2005_14038_b200 import schedule
         model, vws = PMP_SOURCE[cfg.name]
@@ -441,7 +448,9 @@ def main():
                    "lat": list(cfg.latency()), "timing": args.timing, "placement":
                    (f"distributed, {args.span} GPU(s) per VW, PS sharded over {ws}" if placed
                     else "ED-local shards" if ws > 1 else "single GPU"),
-                   "grad": "Philox FLOAT in-kernel", "pull": "EAGER", "local": "STRICT",
+                   "grad": ("CONVEX a(w_p - b) + sigma xi, w_p from the START stash"
+                            if args.grad == "convex" else "Philox FLOAT in-kernel"),
+                   "pull": "EAGER", "local": "STRICT",
                    "apply": "on arrival" if args.apply_mode else "deferred to the observing pull",
                    "transport": args.transport if placed else None,
                    "ps_shards": args.ps if placed else None,

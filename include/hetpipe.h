@@ -60,7 +60,12 @@ typedef enum {
   HP_ERR_STATE = -6       /* call not valid in this context state */
 } hp_status;
 
-enum { HP_GRAD_FLOAT = 0, HP_GRAD_DYADIC = 1, HP_GRAD_EXTERNAL = 2 };
+/* HP_GRAD_CONVEX: the weight-dependent workload
+   g = a (w_p - b) + sigma xi, the gradient of a/2 ||w - b||^2 plus noise at the
+   weights w_p = w_local minibatch p read at its START (kept in a ring of N_m
+   per-VW stash slots: the "forward pass" of minibatch p); b = Philox stream 2,
+   xi = the FLOAT draw; every op one fp32 rounding. world = 1 contexts only. */
+enum { HP_GRAD_FLOAT = 0, HP_GRAD_DYADIC = 1, HP_GRAD_EXTERNAL = 2, HP_GRAD_CONVEX = 3 };
 enum { HP_W0_ZERO = 0, HP_W0_PHILOX = 1 };
 enum { HP_PULL_EAGER = 0, HP_PULL_LAZY = 1 };
 enum { HP_LOCAL_STRICT = 0, HP_LOCAL_AT_LEAST = 1 };
@@ -113,6 +118,8 @@ typedef struct {
   void* stream;            /* cudaStream_t to run on; NULL = library-owned stream */
   int32_t transport;       /* HP_XPORT_* (world > 1): exchange of lockstep batches */
   int32_t reserved;
+  float conv_a;            /* HP_GRAD_CONVEX curvature a (default 0.5) */
+  float conv_sigma;        /* HP_GRAD_CONVEX noise scale sigma (default 1.0) */
   const int64_t* ps_bounds;/* optional PS shard boundaries (world > 1): world+1 values,
                               0 = b[0] < b[1] < ... < b[world] = nparams, inner ones
                               multiples of 32; shard q = [b[q], b[q+1]) on GPU q.

@@ -157,6 +157,8 @@ void hp_config_default(hp_config* c) {
   c->device = 0;
   c->stream = nullptr;
   c->transport = HP_XPORT_PEER;
+  c->conv_a = 0.5f;
+  c->conv_sigma = 1.0f;
   c->reserved = 0;
   c->arena = nullptr;
 }
@@ -175,7 +177,8 @@ const char* validate(hp_config& cfg) {
   else if (cfg.param_begin < 0 || cfg.param_begin % 32) bad = "param_begin must be a multiple of 32";
   else if (cfg.param_count < 0 || cfg.param_begin + cfg.param_count > cfg.nparams) bad = "bad shard";
   else if (cfg.acc_slots < 2 || cfg.acc_slots > 8) bad = "acc_slots must be 2..8";
-  else if (cfg.grad_mode < 0 || cfg.grad_mode > 2) bad = "bad grad_mode";
+  else if (cfg.grad_mode < 0 || cfg.grad_mode > 3) bad = "bad grad_mode";
+  else if (cfg.world > 1 && cfg.grad_mode == HP_GRAD_CONVEX) bad = "CONVEX gradients need world 1";
   else if (cfg.w0_mode < 0 || cfg.w0_mode > 1) bad = "bad w0_mode";
   else if (cfg.pull_policy < 0 || cfg.pull_policy > 1) bad = "bad pull_policy";
   else if (cfg.local_semantics < 0 || cfg.local_semantics > 1) bad = "bad local_semantics";

@@ -26,6 +26,7 @@ Engine::Engine(const hp_config& cfg) : cfg_(cfg) {
   rank_ = cfg.rank;
   span_ = cfg.vw_span;
   dist_ = G_ > 1;
+  convex_ = cfg.grad_mode == HP_GRAD_CONVEX;
 }
 
 namespace {
@@ -54,6 +55,7 @@ RankLayout Engine::layout_of(int q) const {
   L.has.assign(N_, 0);
   L.wl_off.assign(N_, 0);
   L.acc_off.assign(N_, std::vector<size_t>(R_, 0));
+  L.stash_off.assign(N_, std::vector<size_t>(cfg_.grad_mode == HP_GRAD_CONVEX ? Nm_ : 0, 0));
   // the shard regions are sized for the largest shard, so ranks holding
   // congruent VW sets have identical offsets (the multicast mapping of NVLS
   // addresses the same offset on every GPU)
@@ -80,6 +82,10 @@ RankLayout Engine::layout_of(int q) const {
       off += align256(L.len[v]);
       for (int r = 0; r < R_; ++r) {
         L.acc_off[v][r] = off;
+        off += align256(L.len[v]);
+      }
+      for (auto& so : L.stash_off[v]) {
+        so = off;
         off += align256(L.len[v]);
       }
     }
@@ -169,6 +175,7 @@ hp_status Engine::init() {
     if (!s.here) continue;
     s.wl = (float*)(base + L.wl_off[v]);
     for (int r = 0; r < R_; ++r) s.acc.push_back((float*)(base + L.acc_off[v][r]));
+    for (size_t so : L.stash_off[v]) s.stash.push_back((float*)(base + so));
   }
   peer_.assign(G_, nullptr);
   peer_[rank_] = base;
@@ -180,6 +187,11 @@ hp_status Engine::init() {
       st = check_cuda(launch_init(v.wl, v.len, v.a0, cfg_.w0_mode, cfg_.grad_mode, k0, k1, stream_),
                       "init");
   if (st == HP_OK && m_) st = check_cuda(cudaMemsetAsync(m_, 0, (size_t)n_ * 4, stream_), "memset");
+  for (auto& v : vw_)                 // CONVEX: minibatches 1..Nm read w0
+    for (float* sl : v.stash)
+      if (st == HP_OK)
+        st = check_cuda(cudaMemcpyAsync(sl, v.wl, (size_t)v.len * 4, cudaMemcpyDeviceToDevice,
+                                        stream_), "stash init");
   if (st != HP_OK) return st;
   // minibatches 1..Nm of every VW start at t=0 with w0
   for (int v = 0; v < N_; ++v) {
@@ -234,9 +246,13 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
   if (ext && !grad_dev && !grad_host) return fail(HP_ERR_INVALID, "EXTERNAL mode needs a gradient");
   if (!ext && (grad_dev || grad_host)) return fail(HP_ERR_INVALID, "gradient given in synthetic mode");
   if (grad_dev && ((uintptr_t)grad_dev & 15)) return fail(HP_ERR_INVALID, "gradient not 16-byte aligned");
-  // phase order inside a batch: COMPLETE < PUSH < PULL; one COMPLETE per VW
+  // phase order inside a batch: COMPLETE < PUSH < PULL; one COMPLETE per VW;
+  // CONVEX: a complete reads w_p from its stash slot in phase B, so a pending
+  // STASH of this VW (phase D) must be on the device first
   bool again = phase_ > kPhComplete;
   for (auto& b : bc_) again |= b.v == v;
+  if (convex_)
+    for (int64_t q : s.pending_folds) again |= q < 0;
   if (again || (int)bc_.size() >= kMaxC)
     if (hp_status st = flush()) return st;
   const int64_t c = wave_of(p, Nm_);
@@ -279,6 +295,7 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
     if (!wave_end && p + Nm_ <= last_p_) {  // START(p+Nm) without waiting
       s.started = p + Nm_;
       ungated_.push_back({v, p + Nm_});
+      if (convex_) s.pending_folds.push_back(-(p + Nm_));
     }
   } else {                                  // waiting at the gate (Z17)
     s.backlog.push_back(p);
@@ -347,6 +364,15 @@ hp_status Engine::admit(int v, std::vector<int64_t>* started) {
     s.wait += tick_ - s.t_block;
     s.blocked = false;
   }
+  // CONVEX: a START recorded before this pull must read the pre-pull w_local
+  // (never the case in the tick model: STARTs wait while the VW is at its
+  // gate; kept as a guard)
+  if (open.second && convex_) {
+    bool stash_due = false;
+    for (int64_t q : s.pending_folds) stash_due |= q < 0;
+    if (stash_due)
+      if (hp_status st = flush()) return st;
+  }
   s.at_gate = false;
   if (open.second) {                                  // PULL
     for (auto& a : pending_applies_) ba_.push_back(a); // w_global must be current
@@ -355,7 +381,8 @@ hp_status Engine::admit(int v, std::vector<int64_t>* started) {
     auto& pf = s.pending_folds;
     if (cfg_.local_semantics == HP_LOCAL_STRICT) {
       const int64_t pushed_to = s.c_local * Nm_;      // folds inside pushed waves die
-      pf.erase(std::remove_if(pf.begin(), pf.end(), [&](int64_t q) { return q <= pushed_to; }),
+      pf.erase(std::remove_if(pf.begin(), pf.end(),
+                              [&](int64_t q) { return q > 0 && q <= pushed_to; }),
                pf.end());
       s.a = pushed_to;
     } else {
@@ -371,6 +398,7 @@ hp_status Engine::admit(int v, std::vector<int64_t>* started) {
   }
   s.started = gated_p;
   rec('G', v, "START", gated_p, wave_of(gated_p, Nm_));
+  if (convex_) s.pending_folds.push_back(-gated_p);
   if (started) started->push_back(gated_p);
   for (int64_t q : s.backlog) {                       // Z17: replay in order
     if (cfg_.local_semantics == HP_LOCAL_STRICT) {
@@ -381,6 +409,7 @@ hp_status Engine::admit(int v, std::vector<int64_t>* started) {
     if (q + Nm_ <= last_p_) {
       s.started = q + Nm_;
       rec('G', v, "START", q + Nm_, wave_of(q + Nm_, Nm_));
+      if (convex_) s.pending_folds.push_back(-(q + Nm_));
       if (started) started->push_back(q + Nm_);
     }
   }
@@ -415,6 +444,8 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   d.m = m_;
   d.neg_lr = -cfg_.lr;
   d.mu = cfg_.momentum;
+  d.conv_a = cfg_.conv_a;
+  d.conv_sigma = cfg_.conv_sigma;
   d.key0 = (uint32_t)(cfg_.seed & 0xffffffffu);
   d.key1 = (uint32_t)(cfg_.seed >> 32);
   bool any_pull = false, apply_now = false;
@@ -582,6 +613,7 @@ hp_status Engine::flush_local() {
     c.acc = vw_[b.v].acc[b.slot];
     c.grad = b.grad;
     c.wl = nullptr;
+    c.stash = convex_ ? vw_[b.v].stash[(b.p - 1) % Nm_] : nullptr;
     c.v = (uint32_t)b.v;
     c.p = (uint32_t)b.p;
     c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc;
@@ -648,12 +680,15 @@ hp_status Engine::flush_local() {
     if (!pulled && (hold || s.pending_folds.empty())) continue;
     std::vector<int64_t> folds;
     if (!hold) folds.swap(s.pending_folds);
-    if (!pulled && folds.size() == 1) {
+    // the batch's own complete is the VW's only due fold (and, CONVEX, the
+    // START that follows it): fold inline in phase B
+    const bool tail_stash = folds.size() == 2 && folds[1] == -(folds[0] + Nm_);
+    if (!pulled && (folds.size() == 1 || tail_stash) && folds[0] > 0) {
       int jj = -1;
       for (int j = 0; j < d.nc; ++j)
         if (bc_[j].v == v && bc_[j].p == folds[0]) jj = j;
       if (jj >= 0) {
-        d.c[jj].flags |= kFoldInline;
+        d.c[jj].flags |= kFoldInline | (tail_stash ? kStashAfter : 0u);
         d.c[jj].wl = s.wl;
         continue;
       }
@@ -673,9 +708,12 @@ hp_status Engine::flush_local() {
       g.f_begin = d.nf;
       for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
         DFold& f = d.f[d.nf++];
+        const int64_t q = folds[fi] > 0 ? folds[fi] : -folds[fi];
         f.v = (uint32_t)v;
-        f.p = (uint32_t)folds[fi];
-        f.grad = fold_grad(v, folds[fi]);
+        f.p = (uint32_t)q;
+        f.op = folds[fi] > 0 ? 0u : 1u;
+        f.grad = folds[fi] > 0 ? fold_grad(v, q) : nullptr;
+        f.stash = convex_ ? s.stash[(q - 1) % Nm_] : nullptr;
       }
       g.f_end = d.nf;
     } while (fi < folds.size());

@@ -33,6 +33,7 @@ struct RankLayout {
   std::vector<char> has;              // per VW: a stage lives on this rank
   std::vector<size_t> wl_off;
   std::vector<std::vector<size_t>> acc_off;
+  std::vector<std::vector<size_t>> stash_off;   // CONVEX
 };
 
 struct VW {
@@ -43,11 +44,14 @@ struct VW {
   int64_t t_block = 0, wait = 0, pulls = 0;
   int64_t acc_count = 0;         // completions in the open wave
   std::vector<int64_t> backlog;  // completions while waiting at the gate (Z17)
-  std::vector<int64_t> pending_folds;  // u_p not yet folded into w_local on device
+  // Ops on w_local not yet on the device, in order: p > 0 = FOLD u_p; p < 0 =
+  // STASH (CONVEX: START(-p) reads w_local now, into stash slot (-p-1) mod Nm)
+  std::vector<int64_t> pending_folds;
   int64_t a0 = 0, len = 0;       // this rank's stage of the VW (global range)
   bool here = false;             // the VW has a stage (possibly empty) on this rank
   float* wl = nullptr;
   std::vector<float*> acc;       // ring of R slots; wave c -> slot c % R
+  std::vector<float*> stash;     // CONVEX: ring of Nm slots; w_p -> slot (p-1) % Nm
   std::vector<const float*> grad_of_slot;  // EXTERNAL: grad of minibatch p in slot (p-1)%Nm
   std::vector<float*> grad_ring;           // library-owned copies of host gradients
 };
@@ -173,6 +177,7 @@ class Engine {
   double nvl_bytes_ = 0;
   int64_t lockstep_batches_ = 0;
   int N_, Nm_, R_;
+  bool convex_ = false;               // HP_GRAD_CONVEX: stash ring + STASH ops
   int64_t W_, last_p_, n_, begin_;
   cudaStream_t stream_ = nullptr;
   bool own_stream_ = false;

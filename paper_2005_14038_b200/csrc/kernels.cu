@@ -92,6 +92,23 @@ __device__ __forceinline__ float4 synth_u(const TickDesc& d, uint32_t v, uint32_
                      __fmul_rn(d.neg_lr, grad_of<GM>(x.z)), __fmul_rn(d.neg_lr, grad_of<GM>(x.w)));
 }
 
+// CONVEX (GM == 3): u = fl(-lr * fl(fl(a * fl(w - b)) + fl(sigma * xi))) with
+// w = w_p (the weights minibatch p read at START), b = Philox stream 2
+// (2*((x>>8)*2^-24) - 1), xi = the FLOAT draw of stream 0.
+__device__ __forceinline__ float convex_u1(const TickDesc& d, float w, uint32_t xb, uint32_t xx) {
+  const float b = __fsub_rn(__fmul_rn(2.0f, __fmul_rn((float)(xb >> 8), 0x1p-24f)), 1.0f);
+  const float xi = __fsub_rn(__fmul_rn((float)(xx >> 8), 0x1p-24f), 0.5f);
+  const float g = __fadd_rn(__fmul_rn(d.conv_a, __fsub_rn(w, b)), __fmul_rn(d.conv_sigma, xi));
+  return __fmul_rn(d.neg_lr, g);
+}
+__device__ __forceinline__ float4 convex_u(const TickDesc& d, uint32_t v, uint32_t p, uint64_t blk,
+                                           float4 w) {
+  const uint4 xb = philox4x32_10((uint32_t)blk, 0u, 0u, 2u, d.key0, d.key1);
+  const uint4 xx = philox4x32_10((uint32_t)blk, v, p, 0u, d.key0, d.key1);
+  return make_float4(convex_u1(d, w.x, xb.x, xx.x), convex_u1(d, w.y, xb.y, xx.y),
+                     convex_u1(d, w.z, xb.z, xx.z), convex_u1(d, w.w, xb.w, xx.w));
+}
+
 // Source of chunk q among segments [b, e): first with 4q < end (ends are
 // multiples of 32 params, so a chunk never straddles two segments).
 __device__ __forceinline__ const float* seg_ptr(const TickDesc& d, int b, int e, int64_t q) {
@@ -152,16 +169,23 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
       if (fl & kLoadAcc) ain[x] = ld4<CNT>(c.acc, q);
       if (fl & kFoldInline) win[x] = ld4<CNT>(c.wl, q);
       if (GM == 2) gin[x] = ld4<CNT>(c.grad, q);
+      if (GM == 3) gin[x] = ld4<CNT>(c.stash, q);             // w_p
     }
 #pragma unroll
     for (int x = 0; x < U; ++x) {
       const int64_t q = q0 + x * qs;
+      const uint64_t blk = (uint64_t)(d.blk_base + q);
       const float4 u = (GM == 2) ? f4scale(d.neg_lr, gin[x])
-                                 : synth_u<GM>(d, c.v, c.p, (uint64_t)(d.blk_base + q));
+                       : (GM == 3) ? convex_u(d, c.v, c.p, blk, gin[x])
+                                   : synth_u<GM>(d, c.v, c.p, blk);
       const float4 a = (fl & kFirst) ? u : f4add(ain[x], u);   // wave aggregate
       if (fl & kStoreAcc) st4<CNT>(c.acc, q, a);
       if (fl & kApplyNow) apply<MOM>(wg[x], mm[x], a, d.mu);
-      if (fl & kFoldInline) st4<CNT>(c.wl, q, f4add(win[x], u));
+      if (fl & kFoldInline) {
+        const float4 w = f4add(win[x], u);
+        st4<CNT>(c.wl, q, w);
+        if (GM == 3 && (fl & kStashAfter)) st4<CNT>(c.stash, q, w);   // START(p+Nm)
+      }
     }
   }
   // ---- C. store w_global / m ------------------------------------------------
@@ -186,11 +210,23 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
     }
     for (int fi = g.f_begin; fi < g.f_end; ++fi) {
       const DFold& f = d.f[fi];
+      if (GM == 3 && f.op == 1) {                              // STASH: a START reads w
+#pragma unroll
+        for (int x = 0; x < U; ++x) st4<CNT>(f.stash, q0 + x * qs, w[x]);
+        continue;
+      }
+      float4 sw[U];
+      if (GM == 3) {
+#pragma unroll
+        for (int x = 0; x < U; ++x) sw[x] = ld4<CNT>(f.stash, q0 + x * qs);
+      }
 #pragma unroll
       for (int x = 0; x < U; ++x) {
         const int64_t q = q0 + x * qs;
+        const uint64_t blk = (uint64_t)(d.blk_base + q);
         const float4 uf = (GM == 2) ? f4scale(d.neg_lr, ld4<CNT>(f.grad, q))
-                                    : synth_u<GM>(d, f.v, f.p, (uint64_t)(d.blk_base + q));
+                          : (GM == 3) ? convex_u(d, f.v, f.p, blk, sw[x])
+                                      : synth_u<GM>(d, f.v, f.p, blk);
         w[x] = f4add(w[x], uf);
       }
     }
@@ -366,6 +402,7 @@ int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream, i
   switch (grad_mode) {
     case 0: return momentum ? launch_gm<0, true>(d, s, mb) : launch_gm<0, false>(d, s, mb);
     case 1: return momentum ? launch_gm<1, true>(d, s, mb) : launch_gm<1, false>(d, s, mb);
+    case 3: return momentum ? launch_gm<3, true>(d, s, mb) : launch_gm<3, false>(d, s, mb);
     default: return momentum ? launch_gm<2, true>(d, s, mb) : launch_gm<2, false>(d, s, mb);
   }
 }

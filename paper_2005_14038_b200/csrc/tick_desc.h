@@ -29,13 +29,15 @@ enum : uint32_t {
   kStoreAcc = 2u,    // write a back to the acc slot
   kLoadAcc = 4u,     // read the acc slot (not first)
   kApplyNow = 8u,    // w_global += a right after this complete (commit order)
-  kFoldInline = 16u  // w_local(v) += u right here (the VW's only due fold)
+  kFoldInline = 16u, // w_local(v) += u right here (the VW's only due fold)
+  kStashAfter = 32u  // CONVEX: START(p+Nm) reads the folded w_local -> stash slot
 };
 
 struct DComplete {
   float* acc;          // acc slot of the wave p belongs to
   const float* grad;   // EXTERNAL gradient (local shard) or nullptr
   float* wl;           // w_local for kFoldInline, else nullptr
+  float* stash;        // CONVEX: slot (p-1) mod Nm holding w_p (kStashAfter rewrites it)
   uint32_t v, p;
   uint32_t flags;
   uint32_t pad;
@@ -53,9 +55,15 @@ struct DApply {
   int32_t seg_begin, seg_end;   // acc slice(s) holding u~ of an earlier push
 };
 
+// One op of a w_local group, in order: FOLD w += u_p (u regenerated, or from
+// `grad`; CONVEX reads w_p from `stash`), or STASH (CONVEX: a START reads w
+// now: stash <- w).
 struct DFold {
   const float* grad;   // EXTERNAL gradient or nullptr (synthetic: regenerate)
+  float* stash;        // CONVEX: FOLD reads w_p here; STASH writes w here
   uint32_t v, p;
+  uint32_t op;         // 0 FOLD, 1 STASH
+  uint32_t pad;
 };
 
 struct DGroup {
@@ -75,6 +83,7 @@ struct TickDesc {
   float* m;             // momentum shard (nullptr for SGD)
   float neg_lr;         // -lr (negation is exact, Z10)
   float mu;             // momentum
+  float conv_a, conv_sigma;   // CONVEX workload
   uint32_t key0, key1;  // Philox key = seed
   int32_t nc, na, ng, nf;
   int32_t wg_load;      // w_global must be read (applies or pulls present)
@@ -101,11 +110,12 @@ inline int tick_streams(const TickDesc& d) {
   for (int j = 0; j < d.nc; ++j) {
     const uint32_t f = d.c[j].flags;
     s += ((f & kLoadAcc) ? 1 : 0) + ((f & kStoreAcc) ? 1 : 0) + (d.c[j].grad ? 1 : 0) +
-         ((f & kFoldInline) ? 2 : 0);
+         ((f & kFoldInline) ? 2 : 0) + (d.c[j].stash ? 1 : 0) + ((f & kStashAfter) ? 1 : 0);
   }
   for (int g = 0; g < d.ng; ++g) {
     s += 1 + (d.g[g].pull == 1 ? 0 : 1) + (d.g[g].partial ? 1 : 0);
-    for (int k = d.g[g].f_begin; k < d.g[g].f_end; ++k) s += d.f[k].grad ? 1 : 0;
+    for (int k = d.g[g].f_begin; k < d.g[g].f_end; ++k)
+      s += (d.f[k].grad ? 1 : 0) + (d.f[k].stash ? 1 : 0);
   }
   return s;
 }

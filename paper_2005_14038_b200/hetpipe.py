@@ -32,7 +32,8 @@ class hp_config(C.Structure):
                 ("apply_mode", C.c_int32), ("acc_slots", C.c_int32),
                 ("merge_ticks", C.c_int32), ("world", C.c_int32), ("rank", C.c_int32),
                 ("vw_span", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p),
-                ("transport", C.c_int32), ("reserved", C.c_int32), ("ps_bounds", C.c_void_p),
+                ("transport", C.c_int32), ("reserved", C.c_int32),
+                ("conv_a", C.c_float), ("conv_sigma", C.c_float), ("ps_bounds", C.c_void_p),
                 ("arena", C.c_void_p)]
 
 XPORT_PEER, XPORT_NCCL, XPORT_NVLS = 0, 1, 2
@@ -151,6 +152,7 @@ def config_from(cfg, **overrides) -> hp_config:
     c.lr, c.momentum, c.seed = cfg.lr, cfg.momentum, cfg.seed
     c.grad_mode, c.w0_mode = cfg.grad_mode, cfg.w0_mode
     c.pull_policy, c.local_semantics = cfg.pull_policy, cfg.local_semantics
+    c.conv_a, c.conv_sigma = getattr(cfg, "conv_a", 0.5), getattr(cfg, "conv_sigma", 1.0)
     bounds = overrides.pop("ps_bounds", None)
     for k, v in overrides.items():
         setattr(c, k, v)

@@ -24,12 +24,22 @@ void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
   }
 }
 
-float draw_u(const TickDesc& d, int gm, uint32_t v, uint32_t p, int64_t i, const float* grad) {
+float draw_u(const TickDesc& d, int gm, uint32_t v, uint32_t p, int64_t i, const float* grad,
+             const float* stash) {
   if (gm == 2) return d.neg_lr * grad[i];
   const int64_t gi = d.blk_base * 4 + i;
   uint32_t c[4] = {(uint32_t)(gi >> 2), v, p, 0u};
   philox(c, d.key0, d.key1);
   const uint32_t x = c[gi & 3];
+  if (gm == 3) {                    // CONVEX: a (w_p - b) + sigma xi
+    uint32_t cb[4] = {(uint32_t)(gi >> 2), 0u, 0u, 2u};
+    philox(cb, d.key0, d.key1);
+    const float b = 2.0f * ((float)(cb[gi & 3] >> 8) * 0x1p-24f) - 1.0f;
+    const float xi = (float)(x >> 8) * 0x1p-24f - 0.5f;
+    const float t1 = d.conv_a * (stash[i] - b);
+    const float t2 = d.conv_sigma * xi;
+    return d.neg_lr * (t1 + t2);
+  }
   const float g = gm == 1 ? (float)((int)(x >> 28) - 8) : (float)(x >> 8) * 0x1p-24f - 0.5f;
   return d.neg_lr * g;
 }
@@ -58,11 +68,14 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
     for (int k = 0; k < d.na; ++k) app(d, mom, wg, m, seg(d, d.a[k].seg_begin, d.a[k].seg_end, i)[i]);
     for (int j = 0; j < d.nc; ++j) {
       const DComplete& c = d.c[j];
-      const float u = draw_u(d, gm, c.v, c.p, i, c.grad);
+      const float u = draw_u(d, gm, c.v, c.p, i, c.grad, c.stash);
       const float a = (c.flags & kFirst) ? u : c.acc[i] + u;
       if (c.flags & kStoreAcc) c.acc[i] = a;
       if (c.flags & kApplyNow) app(d, mom, wg, m, a);
-      if (c.flags & kFoldInline) c.wl[i] = c.wl[i] + u;
+      if (c.flags & kFoldInline) {
+        c.wl[i] = c.wl[i] + u;
+        if (gm == 3 && (c.flags & kStashAfter)) c.stash[i] = c.wl[i];
+      }
     }
     if (d.wg_store) {
       d.wg[i] = wg;
@@ -72,7 +85,11 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
       const DGroup& G = d.g[g];
       float w = G.pull == 0 ? G.wl[i] : G.pull == 2 ? seg(d, G.seg_begin, G.seg_end, i)[i] : wg;
       if (G.pull && G.partial) w = w + G.partial[i];
-      for (int f = G.f_begin; f < G.f_end; ++f) w = w + draw_u(d, gm, d.f[f].v, d.f[f].p, i, d.f[f].grad);
+      for (int f = G.f_begin; f < G.f_end; ++f) {
+        const DFold& F = d.f[f];
+        if (gm == 3 && F.op == 1) F.stash[i] = w;            // STASH: a START reads w
+        else w = w + draw_u(d, gm, F.v, F.p, i, F.grad, F.stash);
+      }
       G.wl[i] = w;
     }
   }

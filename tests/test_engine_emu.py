@@ -110,3 +110,24 @@ def test_sync_latency_records(hp, cfg):
 @pytest.mark.parametrize("D,policy", [(0, 0), (2, 0), (1, 1)])
 def test_pipeline_derived_timing(hp, D, policy):
     G.test_pipeline_derived_timing(hp, D, policy)
+
+
+@pytest.mark.parametrize("seed", range(80))
+def test_convex_random(hp, seed):
+    G.test_convex_random_bit_exact(hp, seed % 40) if seed < 40 else _convex_more(hp, seed)
+
+
+def _convex_more(hp, seed):
+    import random as _r
+    from workloads import GRAD_CONVEX
+    rng = _r.Random(seed)
+    cfg = G._rand_cfg(3000 + seed).replace(grad_mode=GRAD_CONVEX, lr=0.05, w0_mode=1,
+                                           conv_sigma=rng.choice([0.0, 1.0]))
+    o = run_schedule(cfg)
+    trace, wg, wl, _, _ = G.run_device(hp, cfg, rng.randint(0, 1), rng.choice([2, 3]),
+                                       merge_ticks=rng.randint(0, 1))
+    G.assert_same(o, trace, wg, wl)
+
+
+def test_convex_per_tick_states(hp):
+    G.test_convex_per_tick_states(hp)

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from oracle import gradient, run_schedule
-from workloads import (C1, C1_SKEW, C2, C3, C4, C5, GRAD_DYADIC, GRAD_EXTERNAL,
+from workloads import (C1, C1_SKEW, C2, C3, C4, C5, GRAD_CONVEX, GRAD_DYADIC, GRAD_EXTERNAL,
                        GRAD_FLOAT, LOCAL_AT_LEAST, LOCAL_STRICT, PULL_EAGER,
                        PULL_LAZY, W0_PHILOX, W0_ZERO, WSPConfig, sample_indices)
 
@@ -311,3 +311,45 @@ def test_pipeline_derived_timing(hp, D, policy):
     o = run_schedule(cfg)
     trace, wg, wl, _, _ = run_device(hp, cfg)
     assert_same(o, trace, wg, wl)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_convex_random_bit_exact(hp, seed):
+    """NEXT-2 CONVEX workload: every gradient reads the w_local its minibatch
+    saw at START (the device stash ring), so a wrong version anywhere changes
+    the numbers. Random configs, all modes: identical traces, bit-exact arrays."""
+    rng = random.Random(7000 + seed)
+    base = _rand_cfg(seed)
+    cfg = base.replace(grad_mode=GRAD_CONVEX, lr=0.05, conv_a=rng.choice([0.5, 1.0]),
+                       conv_sigma=rng.choice([0.0, 1.0]), w0_mode=W0_PHILOX)
+    o = run_schedule(cfg)
+    trace, wg, wl, m, _ = run_device(hp, cfg, apply_mode=rng.randint(0, 1),
+                                     acc_slots=rng.choice([2, 3, 8]),
+                                     merge_ticks=rng.randint(0, 1))
+    assert_same(o, trace, wg, wl)
+    if cfg.momentum:
+        assert np.array_equal(m, o.m)
+
+
+def test_convex_per_tick_states(hp):
+    """CONVEX: the device w_local after every commit equals the oracle's."""
+    cfg = C2.replace(nparams=2053, waves=6, D=1, tau=(5, 7, 9, 12), grad_mode=GRAD_CONVEX,
+                     lr=0.05)
+    states = []
+
+    def on_tick(t, sm):
+        states.append((t, len(sm.commit), sm.wg.copy(), [w.copy() for w in sm.wl],
+                       list(sm.at_gate)))
+
+    run_schedule(cfg, on_tick=on_tick)
+    ctx = hp.Context(hp.config_from(cfg))
+    ctx.schedule_begin(cfg.tau, cfg.latency())
+    for target in range(1, cfg.num_vw * cfg.waves + 1):
+        reached = ctx.schedule_advance(target)
+        t, ncommit, wg, wl, at_gate = next(s for s in states if s[1] >= target)
+        assert reached == ncommit
+        assert np.array_equal(ctx.read_weights(-1), wg)
+        for v in range(cfg.num_vw):
+            if not at_gate[v]:
+                assert np.array_equal(ctx.read_weights(v), wl[v]), (target, v)
+    ctx.close()
