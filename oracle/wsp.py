@@ -49,20 +49,28 @@ def wave_range(c: int, Nm: int) -> Tuple[int, int]:
     return c * Nm + 1, (c + 1) * Nm
 
 
-def s_global(Nm: int, D: int) -> int:
-    """s_global = (D+1)*(s_local+1) + s_local - 1 (P:999), s_local = Nm-1 (P:817)."""
+def s_global(Nm: int, D: int, F: int = 1) -> int:
+    """s_global = (D+1)*(s_local+1) + s_local - 1 (P:999), s_local = Nm-1 (P:817);
+    with the update frequency factor F (one clock = F waves):
+    F*(D+1)*(s_local+1) + (F-1)*(s_local+1) + s_local - 1 = F*(D+2)*(s_local+1) - 2."""
     s_local = Nm - 1
-    return (D + 1) * (s_local + 1) + s_local - 1
+    return F * (D + 1) * (s_local + 1) + (F - 1) * (s_local + 1) + s_local - 1
 
 
-def version_floor(p: int, Nm: int, D: int) -> int:
+def version_floor(p: int, Nm: int, D: int, F: int = 1) -> int:
     """Minibatch p must reflect the global updates of minibatches 1..p-(s_global+1)
     (P:998); 0 inside the initial region p <= (D+1)(s_local+1)+s_local."""
-    return max(0, p - (s_global(Nm, D) + 1))
+    return max(0, p - (s_global(Nm, D, F) + 1))
 
 
 def wave_of(p: int, Nm: int) -> int:
     return (p - 1) // Nm
+
+
+def clock_range(c: int, U: int) -> Tuple[int, int]:
+    """Minibatches aggregated by clock c: c*F*(s_local+1)+1 .. (c+1)*F*(s_local+1)
+    (P:1086-1087), U = F*Nm (= wave_range for F = 1)."""
+    return c * U + 1, (c + 1) * U
 
 
 # --------------------------------------------------------------------------- #
@@ -165,11 +173,19 @@ class WSPOracle:
         # CONVEX: w_p, the w_local minibatch p read at its START, until u_p's
         # last use (its COMPLETE and its fold)
         self.w_at_start: List[Dict[int, np.ndarray]] = [dict() for _ in range(N)]
+        # F > 1, STRICT: the aggregate of the VW's own unpushed updates when it
+        # reached its gate, kept if later completions (the backlog) join acc
+        self.acc_at_gate: List[Optional[np.ndarray]] = [None] * N
 
     # -- helpers ---------------------------------------------------------------
     @property
+    def U(self) -> int:
+        """Minibatches per clock: F waves of Nm (F = 1: one wave)."""
+        return self.cfg.F * self.cfg.Nm
+
+    @property
     def last_p(self) -> int:
-        return self.cfg.waves * self.cfg.Nm
+        return self.cfg.waves * self.U
 
     def _rec(self, t: int, phase: str, v: int, kind: str, p: int, c: int) -> None:
         self.trace.append(f"{t} {phase} {v} {kind} {p} {c} {self.c_local[v]} "
@@ -191,7 +207,7 @@ class WSPOracle:
         if cfg.local_semantics == LOCAL_STRICT:
             assert self.a[v] == max(0, p - cfg.Nm), (v, p, self.a[v])   # Z3
         self.started[v] = p
-        self._rec(t, phase, v, "START", p, wave_of(p, cfg.Nm))
+        self._rec(t, phase, v, "START", p, wave_of(p, self.U))
         self.start_versions.append((v, p, self.a[v], self.held_K[v]))
         if cfg.grad_mode == GRAD_CONVEX:
             self.w_at_start[v][p] = self.wl[v].copy()     # the forward pass reads w_p
@@ -199,39 +215,47 @@ class WSPOracle:
             self.snapshots.append((t, v, p, self.wl[v].copy()))
 
     def complete(self, t: int, v: int, p: int) -> Tuple[bool, bool]:
-        """COMPLETE(v,p). Returns (wave_end, ungated_start_of_p+Nm)."""
+        """COMPLETE(v,p). Returns (clock_end, ungated_start_of_p+Nm)."""
         cfg = self.cfg
-        Nm = cfg.Nm
+        Nm, U = cfg.Nm, self.U
         assert p == self.completed[v] + 1 and p <= self.started[v], (v, p)
         self.completed[v] = p
         u = self._u(v, p)
-        if (p - 1) % Nm == 0:                    # first minibatch of its wave
+        if self.at_gate[v] and not self.backlog[v] and self.acc_count[v]:
+            self.acc_at_gate[v] = self.acc[v].copy()     # before the backlog joins
+        if (p - 1) % U == 0:                     # first minibatch of its clock
             self.acc[v] = u.copy()
             self.acc_count[v] = 1
         else:
             self.acc[v] = self.acc[v] + u        # aggregated updates (P:922)
             self.acc_count[v] += 1
-        wave_end = p % Nm == 0
+        wave_end = p % U == 0
+        # START(p+Nm) is the gated one iff p+Nm = (c+2)*U (P:952-955; with F:
+        # "continues to execute up to (F-1)(s_local+1) + s_local minibatches", P:1101)
+        gated_next = (p + Nm) % U == 0 and 2 * U <= p + Nm <= self.last_p
         start_next = False
         if not self.at_gate[v]:
             self.wl[v] = self.wl[v] + u          # w_local = w_local + u_p (P:839)
             self.a[v] = p
             self._folded(v, p)
-            start_next = (not wave_end) and p + Nm <= self.last_p
+            if gated_next:
+                self.at_gate[v] = True           # evaluated in this tick's GATE phase
+                self.acc_at_gate[v] = None
+            start_next = (not gated_next) and p + Nm <= self.last_p
         else:                                    # waiting at the gate (Z17)
             self.backlog[v].append(p)
             if cfg.local_semantics == LOCAL_AT_LEAST:
                 self.wl[v] = self.wl[v] + u
                 self.a[v] = p
                 self._folded(v, p)
-        self._rec(t, "C", v, "COMPLETE", p, wave_of(p, Nm))
+        self._rec(t, "C", v, "COMPLETE", p, wave_of(p, U))
         return wave_end, start_next
 
     def push(self, t: int, v: int, c: int) -> None:
         """PUSH(v,c) and the PS apply on arrival (Z4, Z11)."""
         cfg = self.cfg
         assert c == self.c_local[v], "out-of-order or duplicate push"
-        assert self.completed[v] == (c + 1) * cfg.Nm, "incomplete wave"
+        assert self.completed[v] == (c + 1) * self.U, "incomplete wave"
         ut = self.acc[v]
         if cfg.momentum == 0.0:
             self.wg = self.wg + ut                         # w_global = w_global + u~
@@ -242,9 +266,7 @@ class WSPOracle:
         self.c_local[v] = c + 1
         self.c_global = min(self.c_local)
         self.acc_count[v] = 0
-        if c + 2 <= cfg.waves:                             # a gated START remains
-            self.at_gate[v] = True
-        self._rec(t, "P", v, "PUSH", (c + 1) * cfg.Nm, c)
+        self._rec(t, "P", v, "PUSH", (c + 1) * self.U, c)
 
     def gate_open(self, v: int) -> Tuple[bool, bool]:
         """(admissible, needs_pull) for the VW waiting at its gate."""
@@ -260,8 +282,16 @@ class WSPOracle:
         """w_local <- w_global (STRICT) or w_global + partial u~ (AT_LEAST)."""
         cfg = self.cfg
         if cfg.local_semantics == LOCAL_STRICT:
-            self.wl[v] = self.wg.copy()
-            self.a[v] = self.c_local[v] * cfg.Nm
+            # own updates up to p - Nm of the gated p = (c_local+1)*U: the pushed
+            # ones are in w_global; with F > 1 those of the open clock are added
+            # as their aggregate (reading Z25)
+            gate_a = (self.c_local[v] + 1) * self.U - cfg.Nm
+            if gate_a > self.c_local[v] * self.U:
+                part = self.acc_at_gate[v] if self.backlog[v] else self.acc[v]
+                self.wl[v] = self.wg + part
+            else:
+                self.wl[v] = self.wg.copy()
+            self.a[v] = gate_a
         else:
             self.wl[v] = (self.wg + self.acc[v]) if self.acc_count[v] else self.wg.copy()
             self.a[v] = self.completed[v]
@@ -274,7 +304,7 @@ class WSPOracle:
         cfg = self.cfg
         ok, needs_pull = self.gate_open(v)
         c = self.c_local[v] - 1
-        gated_p = self.c_local[v] * cfg.Nm + cfg.Nm          # (c+2)*Nm
+        gated_p = (self.c_local[v] + 1) * self.U             # (c+2)*U
         if not ok:
             if not self.blocked[v]:
                 self.blocked[v] = True
@@ -298,7 +328,7 @@ class WSPOracle:
                 self.wl[v] = self.wl[v] + self._u(v, q)      # deferred fold (Z3)
                 self.a[v] = q
                 self._folded(v, q)
-                self._rec(t, "G", v, "FOLD", q, wave_of(q, cfg.Nm))
+                self._rec(t, "G", v, "FOLD", q, wave_of(q, self.U))
             if q + cfg.Nm <= self.last_p:
                 self.start(t, v, q + cfg.Nm, phase="G")
                 started.append(q + cfg.Nm)
@@ -363,7 +393,7 @@ def run_schedule(cfg: WSPConfig, idx: Optional[np.ndarray] = None,
         for v, p in comps:                                   # COMPLETE phase
             wave_end, start_next = sm.complete(t, v, p)
             if wave_end:
-                pushes.append((v, wave_of(p, Nm)))
+                pushes.append((v, wave_of(p, sm.U)))
             if start_next:
                 ungated.append((v, p + Nm))
         for v, c in pushes:                                  # PUSH/APPLY phase

@@ -70,6 +70,8 @@ class WSPConfig:
     lat: Optional[Tuple[int, ...]] = None   # fill latency per VW; None -> Nm * tau
     conv_a: float = 0.5                     # GRAD_CONVEX curvature a
     conv_sigma: float = 1.0                 # GRAD_CONVEX noise scale sigma
+    F: int = 1                              # update frequency factor (NEXT-4): one clock
+                                            # = F waves; `waves` counts clocks
 
     def latency(self) -> Tuple[int, ...]:
         if self.lat is not None:
