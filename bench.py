@@ -230,6 +230,9 @@ def main():
                     help="synthetic gradient: weight-independent Philox FLOAT draws, or the "
                          "weight-dependent CONVEX workload (NEXT-2: every gradient reads the "
                          "w_local its minibatch saw at START, kept in a stash ring)")
+    ap.add_argument("--update-freq", type=int, default=1,
+                    help="F (NEXT-4): one clock = F waves; a step is still one WSP round "
+                         "(N pushes), each push carrying F*Nm minibatches")
     ap.add_argument("--num-vw", type=int, default=0,
                     help="override the config's VW count (C5E defaults to one VW per GPU)")
     ap.add_argument("--span", type=int, default=0,
@@ -242,6 +245,8 @@ def main():
                           else 0)
     if nvw:
         cfg = cfg.replace(num_vw=nvw, tau=tuple((list(cfg.tau) * 8)[:nvw]))
+    if args.update_freq > 1:
+        cfg = cfg.replace(F=args.update_freq)
     if args.grad == "convex":
         from workloads import GRAD_CONVEX
         cfg = cfg.replace(grad_mode=GRAD_CONVEX)
@@ -443,7 +448,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg.name, "num_vw": N, "Nm": cfg.Nm, "D": cfg.D,
+        "config": {"workload": cfg.name, "num_vw": N, "Nm": cfg.Nm, "D": cfg.D, "F": cfg.F,
                    "nparams": cfg.nparams, "tau": list(cfg.tau),
                    "lat": list(cfg.latency()), "timing": args.timing, "placement":
                    (f"distributed, {args.span} GPU(s) per VW, PS sharded over {ws}" if placed
@@ -456,7 +461,7 @@ def main():
                    "ps_shards": args.ps if placed else None,
                    "lockstep_batches": lock_batches if placed else None,
                    "l2": "inputs larger than L2 (>= 13 x 230 MiB buffers per GPU)"},
-        "images_per_sec_equiv": commits * 32 * cfg.Nm / (ms_max / 1e3),
+        "images_per_sec_equiv": commits * 32 * cfg.Nm * cfg.F / (ms_max / 1e3),
         "sync_only": ({"value": commits * cfg.nparams / (sync_ms_max / 1e3), "unit": UNIT,
                        "ms_per_step": sync_ms_max / args.steps,
                        "def": "push+apply+pull only: each launch's device time attributed to "

@@ -118,6 +118,12 @@ typedef struct {
   void* stream;            /* cudaStream_t to run on; NULL = library-owned stream */
   int32_t transport;       /* HP_XPORT_* (world > 1): exchange of lockstep batches */
   int32_t reserved;
+  int32_t update_freq;     /* F >= 1 (the paper's drafted update
+                              frequency factor): one clock = F waves; a VW
+                              aggregates and pushes F*Nm minibatches per clock, its gated
+                              STARTs are (c+2)*F*Nm, s_global = F(D+2)Nm - 2; `waves`
+                              counts clocks. F > 1 needs world = 1. Default 1 */
+  int32_t reserved2;
   float conv_a;            /* HP_GRAD_CONVEX curvature a (default 0.5) */
   float conv_sigma;        /* HP_GRAD_CONVEX noise scale sigma (default 1.0) */
   const int64_t* ps_bounds;/* optional PS shard boundaries (world > 1): world+1 values,
@@ -341,6 +347,7 @@ hp_status hp_pipeline_tau_latency(const int64_t* stage_costs, int32_t k, int32_t
 
 /* Closed forms of section 5 (no context needed). */
 int64_t hp_s_global(int32_t Nm, int32_t D);                  /* (D+1)*Nm + Nm - 2 */
+int64_t hp_s_global_f(int32_t Nm, int32_t D, int32_t F);     /* F(D+2)Nm - 2 */
 int64_t hp_version_floor(int64_t p, int32_t Nm, int32_t D);  /* max(0, p - s_global - 1) */
 
 const char* hp_last_error(const hp_ctx* ctx);   /* NULL ctx: last init error */

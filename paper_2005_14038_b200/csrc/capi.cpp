@@ -74,7 +74,7 @@ class Controller {
         hg = host_[k];
       }
       if (hp_status st = e_->complete(vp.first, vp.second, nullptr, hg, &wave_end)) return st;
-      if (wave_end) pushes.push_back({vp.first, (vp.second - 1) / cfg.Nm});
+      if (wave_end) pushes.push_back({vp.first, (vp.second - 1) / ((int64_t)cfg.Nm * cfg.update_freq)});
     }
     for (auto& vc : pushes)  // PUSH/APPLY phase
       if (hp_status st = e_->push(vc.first, vc.second)) return st;
@@ -157,6 +157,7 @@ void hp_config_default(hp_config* c) {
   c->device = 0;
   c->stream = nullptr;
   c->transport = HP_XPORT_PEER;
+  c->update_freq = 1;
   c->conv_a = 0.5f;
   c->conv_sigma = 1.0f;
   c->reserved = 0;
@@ -190,6 +191,8 @@ const char* validate(hp_config& cfg) {
     bad = "world > 1 places the whole model: param_begin 0, param_count -1";
   else if (cfg.world > 1 && cfg.grad_mode == HP_GRAD_EXTERNAL) bad = "EXTERNAL gradients need world 1";
   else if (cfg.transport < 0 || cfg.transport > 2) bad = "bad transport";
+  else if (cfg.update_freq < 1 || cfg.update_freq > 64) bad = "update_freq must be 1..64";
+  else if (cfg.update_freq > 1 && cfg.world > 1) bad = "update_freq > 1 needs world 1";
   if (!bad && cfg.world > 1 && cfg.ps_bounds) {
     const int64_t* b = cfg.ps_bounds;
     if (b[0] != 0 || b[cfg.world] != cfg.nparams) bad = "ps_bounds must span [0, nparams]";
@@ -446,6 +449,11 @@ hp_status hp_profile_sync_latency(hp_ctx* ctx, int64_t max, float* ms, int32_t* 
 int64_t hp_s_global(int32_t Nm, int32_t D) {
   // s_global = (D+1)(s_local+1) + s_local - 1 with s_local = Nm-1
   return (int64_t)(D + 1) * Nm + (Nm - 1) - 1;
+}
+
+int64_t hp_s_global_f(int32_t Nm, int32_t D, int32_t F) {
+  // F(D+1)(s_local+1) + (F-1)(s_local+1) + s_local - 1 = F(D+2)(s_local+1) - 2
+  return (int64_t)F * (D + 2) * Nm - 2;
 }
 
 int64_t hp_version_floor(int64_t p, int32_t Nm, int32_t D) {

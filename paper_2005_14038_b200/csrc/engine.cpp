@@ -18,7 +18,8 @@ Engine::Engine(const hp_config& cfg) : cfg_(cfg) {
   Nm_ = cfg.Nm;
   R_ = cfg.acc_slots;
   W_ = cfg.waves;
-  last_p_ = W_ * (int64_t)Nm_;
+  U_ = (int64_t)Nm_ * cfg.update_freq;
+  last_p_ = W_ * U_;
   begin_ = cfg.param_begin;
   n_ = cfg.param_count;
   vw_.resize(N_);
@@ -56,6 +57,7 @@ RankLayout Engine::layout_of(int q) const {
   L.wl_off.assign(N_, 0);
   L.acc_off.assign(N_, std::vector<size_t>(R_, 0));
   L.stash_off.assign(N_, std::vector<size_t>(cfg_.grad_mode == HP_GRAD_CONVEX ? Nm_ : 0, 0));
+  L.snap_off.assign(N_, 0);
   // the shard regions are sized for the largest shard, so ranks holding
   // congruent VW sets have identical offsets (the multicast mapping of NVLS
   // addresses the same offset on every GPU)
@@ -86,6 +88,10 @@ RankLayout Engine::layout_of(int q) const {
       }
       for (auto& so : L.stash_off[v]) {
         so = off;
+        off += align256(L.len[v]);
+      }
+      if (cfg_.update_freq > 1 && cfg_.local_semantics == HP_LOCAL_STRICT) {
+        L.snap_off[v] = off;
         off += align256(L.len[v]);
       }
     }
@@ -176,6 +182,7 @@ hp_status Engine::init() {
     s.wl = (float*)(base + L.wl_off[v]);
     for (int r = 0; r < R_; ++r) s.acc.push_back((float*)(base + L.acc_off[v][r]));
     for (size_t so : L.stash_off[v]) s.stash.push_back((float*)(base + so));
+    if (L.snap_off[v]) s.snap = (float*)(base + L.snap_off[v]);
   }
   peer_.assign(G_, nullptr);
   peer_[rank_] = base;
@@ -197,7 +204,7 @@ hp_status Engine::init() {
   for (int v = 0; v < N_; ++v) {
     for (int64_t p = 1; p <= std::min<int64_t>(Nm_, last_p_); ++p) {
       vw_[v].started = p;
-      rec('S', v, "START", p, wave_of(p, Nm_));
+      rec('S', v, "START", p, wave_of(p, U_));
     }
   }
   return check_cuda(cudaStreamSynchronize(stream_), "init sync");
@@ -255,9 +262,19 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
     for (int64_t q : s.pending_folds) again |= q < 0;
   if (again || (int)bc_.size() >= kMaxC)
     if (hp_status st = flush()) return st;
-  const int64_t c = wave_of(p, Nm_);
+  const int64_t c = wave_of(p, U_);            // the clock p belongs to (F waves)
   const int slot = (int)(c % R_);
-  const bool first = (p - 1) % Nm_ == 0;
+  const bool first = (p - 1) % U_ == 0;
+  // F > 1, STRICT: the first completion joining a waiting VW's open clock
+  // snapshots that clock's aggregate for the pull (reading Z25)
+  if (s.at_gate && U_ > Nm_ && cfg_.local_semantics == HP_LOCAL_STRICT && s.backlog.empty() &&
+      s.acc_count > 0 && !first) {
+    if (hp_status st = flush()) return st;
+    if (hp_status st = check_cuda(cudaMemcpyAsync(s.snap, s.acc[slot], (size_t)s.len * 4,
+                                                  cudaMemcpyDeviceToDevice, stream_), "snapshot"))
+      return st;
+    s.snap_valid = true;
+  }
   if (first) {  // the slot must not hold a pushed wave that is not applied yet
     bool busy = false;
     for (auto& a : pending_applies_) busy |= (a.v == v && a.slot == slot);
@@ -285,14 +302,19 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
   }
   if (ext) s.grad_of_slot[(p - 1) % Nm_] = g;
   phase_ = kPhComplete;
-  const bool wave_end = p % Nm_ == 0;
+  const bool wave_end = p % U_ == 0;          // the clock's last minibatch: push
+  // START(p+Nm) is the gated one iff p+Nm = (c+2)*U (with F)
+  const bool gated_next = (p + Nm_) % U_ == 0 && p + Nm_ >= 2 * U_ && p + Nm_ <= last_p_;
   bc_.push_back({v, p, slot, first, wave_end, g});
   s.completed = p;
   s.acc_count = first ? 1 : s.acc_count + 1;
   if (!s.at_gate) {
     s.pending_folds.push_back(p);          // w_local = w_local + u_p
     s.a = p;
-    if (!wave_end && p + Nm_ <= last_p_) {  // START(p+Nm) without waiting
+    if (gated_next) {                      // evaluated in this tick's GATE phase
+      s.at_gate = true;
+      s.snap_valid = false;
+    } else if (p + Nm_ <= last_p_) {       // START(p+Nm) without waiting
       s.started = p + Nm_;
       ungated_.push_back({v, p + Nm_});
       if (convex_) s.pending_folds.push_back(-(p + Nm_));
@@ -314,7 +336,7 @@ hp_status Engine::push(int v, int64_t c) {
   if (v < 0 || v >= N_) return fail(HP_ERR_INVALID, "vw out of range");
   VW& s = vw_[v];
   if (c != s.c_local) return fail(HP_ERR_PROTOCOL, "duplicate or out-of-order push");
-  if (s.completed < (c + 1) * Nm_) return fail(HP_ERR_PROTOCOL, "push of an incomplete wave");
+  if (s.completed < (c + 1) * U_) return fail(HP_ERR_PROTOCOL, "push of an incomplete wave");
   if (phase_ > kPhPush)
     if (hp_status st = flush()) return st;
   phase_ = kPhPush;
@@ -325,12 +347,11 @@ hp_status Engine::push(int v, int64_t c) {
   for (auto& x : vw_) mn = std::min(mn, x.c_local);
   c_global_ = mn;
   s.acc_count = 0;
-  if (c + 2 <= W_) s.at_gate = true;                   // a gated START remains
   if (cfg_.apply_mode == HP_APPLY_ON_ARRIVAL) {        // apply on receipt
     for (auto& a : pending_applies_) ba_.push_back(a);
     pending_applies_.clear();
   }
-  rec('P', v, "PUSH", (c + 1) * Nm_, c);
+  rec('P', v, "PUSH", (c + 1) * U_, c);
   return HP_OK;
 }
 
@@ -350,7 +371,7 @@ hp_status Engine::admit(int v, std::vector<int64_t>* started) {
   if (!s.at_gate) return fail(HP_ERR_PROTOCOL, "pull outside the gate");
   const auto open = gate_open(v);
   const int64_t c = s.c_local - 1;
-  const int64_t gated_p = s.c_local * Nm_ + Nm_;     // (c+2)*Nm
+  const int64_t gated_p = (s.c_local + 1) * U_;      // (c+2)*U
   if (!open.first) {
     if (!s.blocked) {
       s.blocked = true;
@@ -379,16 +400,24 @@ hp_status Engine::admit(int v, std::vector<int64_t>* started) {
     pending_applies_.clear();
     bpull_.push_back(v);
     auto& pf = s.pending_folds;
+    s.pull_partial = nullptr;
     if (cfg_.local_semantics == HP_LOCAL_STRICT) {
-      const int64_t pushed_to = s.c_local * Nm_;      // folds inside pushed waves die
+      // own updates up to gated_p - Nm: the pushed ones are in w_global, those
+      // of the open clock (F > 1 only) come as their aggregate (reading Z25);
+      // folds they cover die
+      const int64_t pushed_to = s.c_local * U_, gate_a = gated_p - Nm_;
       pf.erase(std::remove_if(pf.begin(), pf.end(),
-                              [&](int64_t q) { return q > 0 && q <= pushed_to; }),
+                              [&](int64_t q) { return q > 0 && q <= gate_a; }),
                pf.end());
-      s.a = pushed_to;
+      if (gate_a > pushed_to && s.here)
+        s.pull_partial = s.snap_valid ? s.snap : s.acc[s.c_local % R_];
+      s.a = gate_a;
     } else {
       pf.clear();                                     // in w_global or the partial u~
+      if (s.acc_count > 0 && s.here) s.pull_partial = s.acc[s.c_local % R_];
       s.a = s.completed;
     }
+    s.snap_valid = false;
     s.held_g = c_global_;
     s.held_K = (int64_t)commit_.size();
     s.pulls++;
@@ -397,18 +426,18 @@ hp_status Engine::admit(int v, std::vector<int64_t>* started) {
     rec('G', v, "ADMIT", gated_p, c);
   }
   s.started = gated_p;
-  rec('G', v, "START", gated_p, wave_of(gated_p, Nm_));
+  rec('G', v, "START", gated_p, wave_of(gated_p, U_));
   if (convex_) s.pending_folds.push_back(-gated_p);
   if (started) started->push_back(gated_p);
   for (int64_t q : s.backlog) {                       // Z17: replay in order
     if (cfg_.local_semantics == HP_LOCAL_STRICT) {
       s.pending_folds.push_back(q);
       s.a = q;
-      rec('G', v, "FOLD", q, wave_of(q, Nm_));
+      rec('G', v, "FOLD", q, wave_of(q, U_));
     }
     if (q + Nm_ <= last_p_) {
       s.started = q + Nm_;
-      rec('G', v, "START", q + Nm_, wave_of(q + Nm_, Nm_));
+      rec('G', v, "START", q + Nm_, wave_of(q + Nm_, U_));
       if (convex_) s.pending_folds.push_back(-(q + Nm_));
       if (started) started->push_back(q + Nm_);
     }
@@ -420,7 +449,7 @@ hp_status Engine::admit(int v, std::vector<int64_t>* started) {
 hp_status Engine::tick_end(std::vector<std::pair<int, int64_t>>* ungated) {
   if (sticky_) return sticky_;
   for (auto& vp : ungated_) {
-    rec('S', vp.first, "START", vp.second, wave_of(vp.second, Nm_));
+    rec('S', vp.first, "START", vp.second, wave_of(vp.second, U_));
     if (ungated) ungated->push_back(vp);
   }
   ungated_.clear();
@@ -501,7 +530,7 @@ void Engine::note_sync(const TickDesc& d) {
   if (!prof_on_ || prof_launches_ == 0) return;
   const int64_t idx = prof_launches_ - 1;
   for (int j = 0; j < d.nc; ++j)
-    if (d.c[j].p % (uint32_t)Nm_ == 0 && push_launch_[d.c[j].v] < 0) push_launch_[d.c[j].v] = idx;
+    if (d.c[j].p % (uint32_t)U_ == 0 && push_launch_[d.c[j].v] < 0) push_launch_[d.c[j].v] = idx;
   std::vector<int> pulled;
   for (int g = 0; g < d.ng; ++g)
     if (d.g[g].pull)
@@ -628,7 +657,7 @@ hp_status Engine::flush_local() {
     const BApply& a = ba_[reg_from - 1];
     int jj = -1;
     for (int j = 0; j < d.nc; ++j)
-      if (bc_[j].v == a.v && bc_[j].wave_end && wave_of(bc_[j].p, Nm_) == a.c) jj = j;
+      if (bc_[j].v == a.v && bc_[j].wave_end && wave_of(bc_[j].p, U_) == a.c) jj = j;
     if (jj < 0 || jj >= next_j) break;
     next_j = jj;
     --reg_from;
@@ -638,7 +667,7 @@ hp_status Engine::flush_local() {
   bool split = false;
   for (size_t k = 0; k < reg_from; ++k)
     for (int j = 0; j < d.nc; ++j)
-      split |= bc_[j].v == ba_[k].v && bc_[j].wave_end && wave_of(bc_[j].p, Nm_) == ba_[k].c;
+      split |= bc_[j].v == ba_[k].v && bc_[j].wave_end && wave_of(bc_[j].p, U_) == ba_[k].c;
   if (split) {
     if (hp_status st = emit(d, begin_, n_)) return st;   // completes only: acc stored
     d.nc = 0;
@@ -646,7 +675,7 @@ hp_status Engine::flush_local() {
   }
   for (size_t k = reg_from; k < ba_.size(); ++k) {
     for (int j = 0; j < d.nc; ++j) {
-      if (bc_[j].v == ba_[k].v && bc_[j].wave_end && wave_of(bc_[j].p, Nm_) == ba_[k].c) {
+      if (bc_[j].v == ba_[k].v && bc_[j].wave_end && wave_of(bc_[j].p, U_) == ba_[k].c) {
         d.c[j].flags |= kApplyNow;
         d.c[j].flags &= ~kStoreAcc;
       }
@@ -702,9 +731,9 @@ hp_status Engine::flush_local() {
       DGroup& g = d.g[d.ng++];
       g.wl = s.wl;
       g.pull = (pulled && fi == 0) ? 1 : 0;
-      g.partial = nullptr;
-      if (g.pull && !strict && s.acc_count > 0)   // AT_LEAST: w_global + partial u~
-        g.partial = s.acc[s.c_local % R_];        // stored in phase B if completed now
+      // w_global + the own unpushed aggregate (AT_LEAST; STRICT with F > 1),
+      // stored in phase B if completed now
+      g.partial = g.pull ? s.pull_partial : nullptr;
       g.f_begin = d.nf;
       for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
         DFold& f = d.f[d.nf++];
@@ -903,7 +932,7 @@ hp_status Engine::flush_dist() {
         g.wl = s.wl;
         g.partial = nullptr;
         g.pull = first_part ? 1 : 0;     // 1: base = the w_global registers
-        if (first_part && !strict && s.acc_count > 0) g.partial = s.acc[s.c_local % R_];
+        if (first_part) g.partial = s.pull_partial;
         first_part = false;
         g.f_begin = d.nf;
         for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
@@ -1216,7 +1245,7 @@ hp_status Engine::flush_applies() {
 
 hp_status Engine::sync() {
   if (sticky_) return sticky_;
-  for (auto& vp : ungated_) rec('S', vp.first, "START", vp.second, wave_of(vp.second, Nm_));
+  for (auto& vp : ungated_) rec('S', vp.first, "START", vp.second, wave_of(vp.second, U_));
   ungated_.clear();
   if (hp_status st = flush_applies()) return st;
   if (hp_status st = join_exchange()) return st;

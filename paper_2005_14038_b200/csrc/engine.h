@@ -34,6 +34,7 @@ struct RankLayout {
   std::vector<size_t> wl_off;
   std::vector<std::vector<size_t>> acc_off;
   std::vector<std::vector<size_t>> stash_off;   // CONVEX
+  std::vector<size_t> snap_off;                 // F > 1, STRICT
 };
 
 struct VW {
@@ -52,6 +53,9 @@ struct VW {
   float* wl = nullptr;
   std::vector<float*> acc;       // ring of R slots; wave c -> slot c % R
   std::vector<float*> stash;     // CONVEX: ring of Nm slots; w_p -> slot (p-1) % Nm
+  float* snap = nullptr;         // F > 1, STRICT: acc of the open clock when the VW
+  bool snap_valid = false;       //   reached its gate, if the backlog joined acc since
+  const float* pull_partial = nullptr;  // pull base = w_global + this (or nullptr)
   std::vector<const float*> grad_of_slot;  // EXTERNAL: grad of minibatch p in slot (p-1)%Nm
   std::vector<float*> grad_ring;           // library-owned copies of host gradients
 };
@@ -177,6 +181,7 @@ class Engine {
   double nvl_bytes_ = 0;
   int64_t lockstep_batches_ = 0;
   int N_, Nm_, R_;
+  int64_t U_ = 1;                     // minibatches per clock: F * Nm (NEXT-4)
   bool convex_ = false;               // HP_GRAD_CONVEX: stash ring + STASH ops
   int64_t W_, last_p_, n_, begin_;
   cudaStream_t stream_ = nullptr;

@@ -33,6 +33,7 @@ class hp_config(C.Structure):
                 ("merge_ticks", C.c_int32), ("world", C.c_int32), ("rank", C.c_int32),
                 ("vw_span", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p),
                 ("transport", C.c_int32), ("reserved", C.c_int32),
+                ("update_freq", C.c_int32), ("reserved2", C.c_int32),
                 ("conv_a", C.c_float), ("conv_sigma", C.c_float), ("ps_bounds", C.c_void_p),
                 ("arena", C.c_void_p)]
 
@@ -111,6 +112,7 @@ EXPORTS = {
     "hp_pipeline_tau_latency": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64,
                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "hp_s_global": (C.c_int64, [C.c_int32, C.c_int32]),
+    "hp_s_global_f": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "hp_version_floor": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
     "hp_last_error": (C.c_char_p, [C.c_void_p]),
     "hp_version": (C.c_char_p, []),
@@ -153,6 +155,7 @@ def config_from(cfg, **overrides) -> hp_config:
     c.grad_mode, c.w0_mode = cfg.grad_mode, cfg.w0_mode
     c.pull_policy, c.local_semantics = cfg.pull_policy, cfg.local_semantics
     c.conv_a, c.conv_sigma = getattr(cfg, "conv_a", 0.5), getattr(cfg, "conv_sigma", 1.0)
+    c.update_freq = getattr(cfg, "F", 1)
     bounds = overrides.pop("ps_bounds", None)
     for k, v in overrides.items():
         setattr(c, k, v)

@@ -131,3 +131,14 @@ def _convex_more(hp, seed):
 
 def test_convex_per_tick_states(hp):
     G.test_convex_per_tick_states(hp)
+
+
+@pytest.mark.parametrize("seed", range(120))
+def test_update_frequency_random(hp, seed):
+    G.test_update_frequency_random_bit_exact(hp, seed)
+
+
+@pytest.mark.parametrize("F,Nm,D,tau,mode", [(2, 3, 0, (2, 9), 0), (2, 2, 0, (3, 7, 5), 0),
+                                             (3, 2, 1, (2, 11), 3), (2, 4, 0, (5, 6, 13), 3)])
+def test_update_frequency_blocked_strict(hp, F, Nm, D, tau, mode):
+    G.test_update_frequency_blocked_strict(hp, F, Nm, D, tau, mode)

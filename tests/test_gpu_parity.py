@@ -353,3 +353,38 @@ def test_convex_per_tick_states(hp):
             if not at_gate[v]:
                 assert np.array_equal(ctx.read_weights(v), wl[v]), (target, v)
     ctx.close()
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_update_frequency_random_bit_exact(hp, seed):
+    """NEXT-4: one clock = F waves (aggregate and push F*Nm minibatches, gate
+    at (c+2)*F*Nm, STRICT pulls add the open clock's own aggregate). Random
+    configs in every mode, incl. CONVEX: identical traces, bit-exact arrays."""
+    rng = random.Random(9000 + seed)
+    base = _rand_cfg(seed)
+    cfg = base.replace(F=rng.randint(2, 4), waves=max(1, base.waves // 2))
+    if rng.random() < 0.3:
+        cfg = cfg.replace(grad_mode=GRAD_CONVEX, lr=0.05, w0_mode=W0_PHILOX)
+    o = run_schedule(cfg)
+    trace, wg, wl, m, _ = run_device(hp, cfg, apply_mode=rng.randint(0, 1),
+                                     acc_slots=rng.choice([2, 3]),
+                                     merge_ticks=rng.randint(0, 1))
+    assert_same(o, trace, wg, wl)
+    if cfg.momentum:
+        assert np.array_equal(m, o.m)
+
+
+@pytest.mark.parametrize("F,Nm,D,tau,mode", [(2, 3, 0, (2, 9), GRAD_FLOAT),
+                                             (2, 2, 0, (3, 7, 5), GRAD_FLOAT),
+                                             (3, 2, 1, (2, 11), GRAD_CONVEX),
+                                             (2, 4, 0, (5, 6, 13), GRAD_CONVEX)])
+def test_update_frequency_blocked_strict(hp, F, Nm, D, tau, mode):
+    """F > 1, STRICT, a fast VW waiting at its gate while its in-flight
+    minibatches complete: the pull must add the open clock's aggregate as it
+    stood at the gate (the device snapshot), not the backlog's updates."""
+    cfg = WSPConfig("fb", len(tau), Nm, D, 1027, 5, tau, F=F, grad_mode=mode,
+                    lr=0.05 if mode == GRAD_CONVEX else 0.01)
+    o = run_schedule(cfg)
+    for merge in (0, 1):
+        trace, wg, wl, _, _ = run_device(hp, cfg, merge_ticks=merge)
+        assert_same(o, trace, wg, wl)
