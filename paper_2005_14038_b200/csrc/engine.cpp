@@ -484,7 +484,9 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   d.wg_load = (d.wg_store || any_pull) ? 1 : 0;
   if (d.nc == 0 && d.na == 0 && d.ng == 0) return HP_OK;
   const int streams = tick_streams(d);
-  const double bytes = 4.0 * (double)n * streams;
+  double pstore = 0;                     // owner-side pull stores (partial ranges)
+  for (int k = 0; k < d.np; ++k) pstore += 4.0 * (double)(d.pd[k].hi - d.pd[k].lo);
+  const double bytes = 4.0 * (double)n * streams + pstore;
   // remote (NVLink) reads: segments whose pointer is outside this rank's arena
   double remote = 0;
   const char* lo = (const char*)arena_;
@@ -513,7 +515,7 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   for (int j = 0; j < d.nc; ++j) inl += (d.c[j].flags & kFoldInline) ? 1 : 0;
   int pulls = 0;
   for (int g = 0; g < d.ng; ++g) pulls |= d.g[g].pull != 0;
-  prof_end(st, bytes, 4.0 * (double)n * tick_sync_streams(d),
+  prof_end(st, bytes, 4.0 * (double)n * tick_sync_streams(d) + pstore,
            d.nc | (inl << 4) | (d.na << 8) | (d.ng << 16) | (d.nf << 24) |
                (int)((unsigned)pulls << 31));
   note_sync(d);
@@ -861,6 +863,23 @@ hp_status Engine::flush_dist() {
   auto xs_wait_wl = [&](int v) {      // a pull rewrites w_local: after its folds
     if (vw_[v].here && lastw_[v]) cudaStreamWaitEvent(xs_, lastw_[v], 0);
   };
+  // Owner-side pull (STRICT: the pull is the copy w_local = w_global): the
+  // last apply launch also stores the final w_global of this rank's shard into
+  // every pulled VW's w_local slice, wherever it lives (NVLink stores, under the
+  // loads of the applies); the post-apply barrier publishes them. HP_PULL_PUSH=0
+  // keeps the separate reader-side pull launches.
+  std::vector<DStore> ptargets;
+  for (int v : bpull_)
+    for (int q = 0; q < G_; ++q) {
+      const RankLayout& L = lay_[q];
+      if (!L.has[v]) continue;
+      const int64_t x0 = std::max(L.a[v], begin_), x1 = std::min(L.a[v] + L.len[v], begin_ + n_);
+      if (x0 >= x1) continue;
+      float* base = (float*)(peer_[q] + L.wl_off[v]);
+      ptargets.push_back({base + (begin_ - L.a[v]), x0 - begin_, x1 - begin_});   // i -> [begin_+i-a]
+    }
+  const bool fuse_pull = push_pull_ && strict && !ba_.empty() && !bpull_.empty() &&
+                         ptargets.size() <= (size_t)kMaxP;
   if (!ba_.empty()) {
     for (const BApply& a : ba_) xs_wait(a.v);
     for (int v : bpull_) {
@@ -880,6 +899,8 @@ hp_status Engine::flush_dist() {
         d.na++;
         ++k;
       }
+      if (fuse_pull && k == ba_.size())
+        for (const DStore& t : ptargets) d.pd[d.np++] = t;
       if (hp_status st = emit(d, begin_, n_, xs_, xblocks_)) return st;
     }
     applied_ += (int64_t)ba_.size();
@@ -906,6 +927,37 @@ hp_status Engine::flush_dist() {
     }
     if (std::find(pranges.begin(), pranges.end(), std::make_pair(s.a0, s.len)) == pranges.end())
       pranges.push_back({s.a0, s.len});
+  }
+  if (fuse_pull) {   // the owners stored w_global into w_local: only the folds remain
+    for (int v : bpull_) {
+      VW& s = vw_[v];
+      if (!s.here) continue;
+      const int64_t ov = std::max<int64_t>(
+          0, std::min(s.a0 + s.len, begin_ + n_) - std::max(s.a0, begin_));
+      nvl_bytes_ += 4.0 * (double)(s.len - ov);   // received from the other owners
+      std::vector<int64_t> folds;
+      folds.swap(s.pending_folds);
+      size_t fi = 0;
+      while (fi < folds.size()) {
+        TickDesc d;
+        memset(&d, 0, sizeof d);
+        while (fi < folds.size() && d.ng < kMaxG && d.nf < kMaxF) {
+          DGroup& g = d.g[d.ng++];
+          g.wl = s.wl;
+          g.pull = 0;
+          g.f_begin = d.nf;
+          for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
+            DFold& f = d.f[d.nf++];
+            f.v = (uint32_t)v;
+            f.p = (uint32_t)folds[fi];
+            f.grad = nullptr;
+          }
+          g.f_end = d.nf;
+        }
+        if (hp_status st = emit(d, s.a0, s.len, xs_, xblocks_)) return st;
+      }
+    }
+    pranges.clear();
   }
   for (auto& rg : pranges) {
     TickDesc d;
@@ -1216,6 +1268,7 @@ hp_status Engine::finish_connect(const void* comm_id) {
   vs_.assign(N_, nullptr);
   fs_.assign(N_, nullptr);
   if (const char* sf = getenv("HP_SPLIT_FOLDS")) split_folds_ = atoi(sf) != 0;
+  if (const char* pp = getenv("HP_PULL_PUSH")) push_pull_ = atoi(pp) != 0;
   for (int v = 0; v < N_; ++v)
     if (vw_[v].here)
     {

@@ -174,6 +174,7 @@ class Engine {
   std::vector<cudaStream_t> vs_;      // per local VW: accumulation stream
   std::vector<cudaStream_t> fs_;      // per local VW: fold stream
   bool split_folds_ = false;          // HP_SPLIT_FOLDS=1: acc and folds in separate launches
+  bool push_pull_ = true;             // owner-side pull (HP_PULL_PUSH=0: reader-side)
   bool forked_ = false;               // side streams ordered after the context stream
   int xblocks_ = 0;                   // grid bound of exchange launches (HP_XBLOCKS)
   std::vector<cudaEvent_t> evpool_;

@@ -195,6 +195,15 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
       st4<CNT>(d.wg, q0 + x * qs, wg[x]);
       if (MOM) st4<CNT>(d.m, q0 + x * qs, mm[x]);
     }
+    // owner-side pull: the final w_global into every pulled w_local slice
+    // (NVLink stores to the GPU that holds it; ranges are multiples of 32)
+    for (int k = 0; k < d.np; ++k) {
+#pragma unroll
+      for (int x = 0; x < U; ++x) {
+        const int64_t q = q0 + x * qs;
+        if (4 * q >= d.pd[k].lo && 4 * q < d.pd[k].hi) st4<CNT>(d.pd[k].ptr, q, wg[x]);
+      }
+    }
   }
   // ---- D. w_local groups: pull base then due folds ---------
   for (int gi = 0; gi < d.ng; ++gi) {

@@ -23,6 +23,7 @@ constexpr int kMaxA = 16;   // memory-sourced applies per launch
 constexpr int kMaxG = 8;    // w_local groups per launch (one per VW)
 constexpr int kMaxF = 40;   // folds per launch
 constexpr int kMaxS = 32;   // source segments per launch
+constexpr int kMaxP = 16;   // pushed-pull store targets per launch
 
 enum : uint32_t {
   kFirst = 1u,       // first minibatch of its wave: a = u
@@ -49,6 +50,14 @@ struct DComplete {
 struct DSeg {
   const float* ptr;
   int64_t end;
+};
+
+// Pull by the shard owner (distributed placements): after phase C the final
+// w_global of local index i in [lo, hi) is also stored at ptr[i], a pulled
+// VW's w_local slice that may live on a peer GPU (NVLink stores).
+struct DStore {
+  float* ptr;
+  int64_t lo, hi;
 };
 
 struct DApply {
@@ -96,7 +105,8 @@ struct TickDesc {
   int32_t ns;
   int32_t wgs_begin, wgs_end;   // if non-empty: w_global registers are loaded from
                                 // these segments (remote shards) instead of wg
-  int32_t pad2;
+  int32_t np;                   // store targets of the owner-side pull
+  DStore pd[kMaxP];
 };
 
 static_assert(sizeof(TickDesc) <= 4096, "TickDesc must fit a kernel parameter");
@@ -104,7 +114,7 @@ static_assert(sizeof(TickDesc) <= 4096, "TickDesc must fit a kernel parameter");
 // Buffer passes of one launch (each = 4 bytes per param): the algorithmic
 // bytes the fused tick must move, used for the roofline.
 inline int tick_streams(const TickDesc& d) {
-  int s = d.wg_load + (d.wg_store ? 1 : 0);
+  int s = d.wg_load + (d.wg_store ? 1 : 0);   // (+ the owner-side pull stores: emit())
   if (d.m && d.wg_store) s += 2;
   s += d.na;
   for (int j = 0; j < d.nc; ++j) {

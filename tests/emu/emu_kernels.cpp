@@ -80,6 +80,8 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
     if (d.wg_store) {
       d.wg[i] = wg;
       if (mom) d.m[i] = m;
+      for (int k = 0; k < d.np; ++k)
+        if (i >= d.pd[k].lo && i < d.pd[k].hi) d.pd[k].ptr[i] = wg;
     }
     for (int g = 0; g < d.ng; ++g) {
       const DGroup& G = d.g[g];
