@@ -868,16 +868,31 @@ hp_status Engine::flush_dist() {
   // every pulled VW's w_local slice, wherever it lives (NVLink stores, under the
   // loads of the applies); the post-apply barrier publishes them. HP_PULL_PUSH=0
   // keeps the separate reader-side pull launches.
-  std::vector<DStore> ptargets;
+  // One target per (GPU, stage range): the first pulled VW there (its
+  // "primary"); the other pulled VWs of that GPU and range copy it locally
+  // afterwards (fan-out, as the reader-side pull reads a remote shard once).
+  struct Prim {
+    int q;
+    int64_t a, len;
+    int v;
+  };
+  std::vector<Prim> prims;
   for (int v : bpull_)
     for (int q = 0; q < G_; ++q) {
       const RankLayout& L = lay_[q];
       if (!L.has[v]) continue;
-      const int64_t x0 = std::max(L.a[v], begin_), x1 = std::min(L.a[v] + L.len[v], begin_ + n_);
-      if (x0 >= x1) continue;
-      float* base = (float*)(peer_[q] + L.wl_off[v]);
-      ptargets.push_back({base + (begin_ - L.a[v]), x0 - begin_, x1 - begin_});   // i -> [begin_+i-a]
+      bool seen = false;
+      for (const Prim& pr : prims) seen |= pr.q == q && pr.a == L.a[v] && pr.len == L.len[v];
+      if (!seen) prims.push_back({q, L.a[v], L.len[v], v});
     }
+  std::vector<DStore> ptargets;
+  for (const Prim& pr : prims) {
+    const RankLayout& L = lay_[pr.q];
+    const int64_t x0 = std::max(pr.a, begin_), x1 = std::min(pr.a + pr.len, begin_ + n_);
+    if (x0 >= x1) continue;
+    float* base = (float*)(peer_[pr.q] + L.wl_off[pr.v]);
+    ptargets.push_back({base + (begin_ - pr.a), x0 - begin_, x1 - begin_});   // i -> [begin_+i-a]
+  }
   const bool fuse_pull = push_pull_ && strict && !ba_.empty() && !bpull_.empty() &&
                          ptargets.size() <= (size_t)kMaxP;
   if (!ba_.empty()) {
@@ -928,23 +943,49 @@ hp_status Engine::flush_dist() {
     if (std::find(pranges.begin(), pranges.end(), std::make_pair(s.a0, s.len)) == pranges.end())
       pranges.push_back({s.a0, s.len});
   }
-  if (fuse_pull) {   // the owners stored w_global into w_local: only the folds remain
-    for (int v : bpull_) {
-      VW& s = vw_[v];
-      if (!s.here) continue;
+  if (fuse_pull) {   // the owners stored w_global into the primaries' w_local
+    note_pulls(bpull_);                  // (wave-sync latency: ends with this apply)
+    for (auto& rg : pranges) {
+      int prim = -1;
+      for (const Prim& pr : prims)
+        if (pr.q == rank_ && pr.a == rg.first && pr.len == rg.second) prim = pr.v;
       const int64_t ov = std::max<int64_t>(
-          0, std::min(s.a0 + s.len, begin_ + n_) - std::max(s.a0, begin_));
-      nvl_bytes_ += 4.0 * (double)(s.len - ov);   // received from the other owners
-      std::vector<int64_t> folds;
-      folds.swap(s.pending_folds);
-      size_t fi = 0;
-      while (fi < folds.size()) {
-        TickDesc d;
-        memset(&d, 0, sizeof d);
-        while (fi < folds.size() && d.ng < kMaxG && d.nf < kMaxF) {
+          0, std::min(rg.first + rg.second, begin_ + n_) - std::max(rg.first, begin_));
+      nvl_bytes_ += 4.0 * (double)(rg.second - ov);   // received from the other owners
+      // the other pulled VWs of this range copy the primary (groups before the
+      // primary's own folds: the kernel runs groups in order per element),
+      // then every VW's due folds
+      std::vector<int> order;
+      for (int v : bpull_)
+        if (vw_[v].here && vw_[v].a0 == rg.first && vw_[v].len == rg.second && v != prim)
+          order.push_back(v);
+      order.push_back(prim);
+      TickDesc d;
+      memset(&d, 0, sizeof d);
+      for (int v : order) {
+        VW& s = vw_[v];
+        std::vector<int64_t> folds;
+        folds.swap(s.pending_folds);
+        if (v == prim && folds.empty()) continue;
+        size_t fi = 0;
+        bool first_part = true;
+        do {
+          if (d.ng == kMaxG || d.nf == kMaxF || d.ns == kMaxS) {
+            if (hp_status st = emit(d, rg.first, rg.second, xs_, xblocks_)) return st;
+            memset(&d, 0, sizeof d);
+          }
           DGroup& g = d.g[d.ng++];
           g.wl = s.wl;
           g.pull = 0;
+          if (first_part && v != prim) {       // base = the primary's pulled w_local
+            g.pull = 2;
+            g.seg_begin = d.ns;
+            d.s[d.ns].ptr = vw_[prim].wl;
+            d.s[d.ns].end = rg.second;
+            d.ns++;
+            g.seg_end = d.ns;
+          }
+          first_part = false;
           g.f_begin = d.nf;
           for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
             DFold& f = d.f[d.nf++];
@@ -953,9 +994,10 @@ hp_status Engine::flush_dist() {
             f.grad = nullptr;
           }
           g.f_end = d.nf;
-        }
-        if (hp_status st = emit(d, s.a0, s.len, xs_, xblocks_)) return st;
+        } while (fi < folds.size());
       }
+      if (d.ng)
+        if (hp_status st = emit(d, rg.first, rg.second, xs_, xblocks_)) return st;
     }
     pranges.clear();
   }
