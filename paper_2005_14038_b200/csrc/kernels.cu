@@ -416,22 +416,35 @@ int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream, i
   }
 }
 
-int launch_nvls(const NvlsDesc& d, void* stream, int max_blocks) {
-  if (d.n <= 0) return 0;
+template <int U>
+int launch_nvls_u(const NvlsDesc& d, cudaStream_t s, int max_blocks) {
   static int grid_max = 0;
   if (grid_max == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nvls_kernel<4>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nvls_kernel<U>, 256, 0);
     grid_max = sms * (per_sm > 0 ? per_sm : 1);
   }
   int64_t blocks = ((d.n >> 2) + 255) / 256;
   if (blocks > grid_max) blocks = grid_max;
   if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  nvls_kernel<4><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d);
+  nvls_kernel<U><<<(unsigned)blocks, 256, 0, s>>>(d);
   return (int)cudaGetLastError();
+}
+
+int launch_nvls(const NvlsDesc& d, void* stream, int max_blocks) {
+  if (d.n <= 0) return 0;
+  static int u = -1;   // HP_NVLS_U: multicast loads in flight per thread (2, 4, 8)
+  if (u < 0) {
+    const char* e = getenv("HP_NVLS_U");
+    u = e ? atoi(e) : 4;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (u >= 8) return launch_nvls_u<8>(d, s, max_blocks);
+  if (u <= 2) return launch_nvls_u<2>(d, s, max_blocks);
+  return launch_nvls_u<4>(d, s, max_blocks);
 }
 
 int launch_init(float* out, int64_t n, int64_t param_begin, int w0_mode, int grad_mode,
