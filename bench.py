@@ -358,6 +358,17 @@ def main():
     sync_ms = float(sum(float(t) * float(sy) / float(by)
                         for t, by, sy in zip(l_ms, l_bytes, l_sync) if by > 0))
     s_ms, s_vw = ctx.profile_sync_latency()
+    l_link = ctx.profile_link()
+    xl = [(float(t), float(b)) for t, b in zip(l_ms, l_link) if b > 0]
+    xch = None
+    if xl:
+        xt, xb = sum(t for t, _ in xl), sum(b for _, b in xl)
+        xch = {"launches": len(xl), "ms": xt, "link_bytes": xb,
+               "achieved_GBps": xb / (xt / 1e3) / 1e9, "peak_GBps": 770.0,
+               "frac": xb / (xt / 1e3) / 1e9 / 770.0, "bound": "nvlink",
+               "def": "exchange launches only (peer loads/stores, NVLS multimem, NCCL "
+                      "collectives): algorithmic NVLink bytes per direction / their device "
+                      "time, rank 0; peak = guide-measured peer copy per direction"}
     sync_us = [1e3 * float(x) for x in s_ms]
     mix = {}
     for t_ms, by, sh in zip(l_ms, l_bytes, l_shape):
@@ -473,6 +484,7 @@ def main():
                      "peak_kind": peak_kind, "kernel": "hp::tick_kernel (all launches)",
                      "kernel_ms": kern_ms, "busy_ms": busy_ms, "launches": kern_launches,
                      "alg_bytes_per_launch": kern_bytes / max(kern_launches, 1)},
+        "exchange_roofline": xch,
         "nvlink": {"bytes_per_step_max_rank": nvl_bytes_max / args.steps,
                    "GBps_over_step": nvl_bytes_max / (ms_max / 1e3) / 1e9,
                    "peak_GBps": 770.0, "peak_kind": "guide-measured peer copy per direction"},

@@ -285,6 +285,12 @@ hp_status hp_profile_launches(hp_ctx* ctx, int64_t max, float* ms, double* alg_b
                               int32_t* shape, double* sync_bytes, float* start_ms,
                               int64_t* n);
 
+/* Per-launch NVLink bytes of the same window (one entry per hp_profile_launches
+   record): the algorithmic bytes per direction (max of in, out) the launch's
+   peer / multicast accesses or NCCL collective move through this GPU's links;
+   0 for launches that touch only local memory. */
+hp_status hp_profile_link(hp_ctx* ctx, int64_t max, double* link_bytes, int64_t* n);
+
 /* Wave-sync latency of the same window, one record per
    (VW, wave) whose push and pull both fall in it: device time from the start
    of the launch that carried the VW's wave-end COMPLETE (its u~ final: the

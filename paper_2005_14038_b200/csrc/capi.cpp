@@ -440,6 +440,12 @@ hp_status hp_profile_launches(hp_ctx* ctx, int64_t max, float* ms, double* alg_b
   HP_EXIT(ctx)
 }
 
+hp_status hp_profile_link(hp_ctx* ctx, int64_t max, double* link_bytes, int64_t* n) {
+  HP_ENTRY(ctx)
+  return ctx->eng->profile_link(max, link_bytes, n);
+  HP_EXIT(ctx)
+}
+
 hp_status hp_profile_sync_latency(hp_ctx* ctx, int64_t max, float* ms, int32_t* vw, int64_t* n) {
   HP_ENTRY(ctx)
   return ctx->eng->profile_sync(max, ms, vw, n);

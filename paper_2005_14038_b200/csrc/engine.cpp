@@ -484,8 +484,13 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   d.wg_load = (d.wg_store || any_pull) ? 1 : 0;
   if (d.nc == 0 && d.na == 0 && d.ng == 0) return HP_OK;
   const int streams = tick_streams(d);
-  double pstore = 0;                     // owner-side pull stores (partial ranges)
-  for (int k = 0; k < d.np; ++k) pstore += 4.0 * (double)(d.pd[k].hi - d.pd[k].lo);
+  double pstore = 0, rstore = 0;         // owner-side pull stores (all / to peers)
+  for (int k = 0; k < d.np; ++k) {
+    pstore += 4.0 * (double)(d.pd[k].hi - d.pd[k].lo);
+    const char* p0 = (const char*)(d.pd[k].ptr + d.pd[k].lo);
+    const char* alo = (const char*)arena_;
+    if (p0 < alo || p0 >= alo + lay_[rank_].bytes) rstore += 4.0 * (double)(d.pd[k].hi - d.pd[k].lo);
+  }
   const double bytes = 4.0 * (double)n * streams + pstore;
   // remote (NVLink) reads: segments whose pointer is outside this rank's arena
   double remote = 0;
@@ -517,7 +522,8 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   for (int g = 0; g < d.ng; ++g) pulls |= d.g[g].pull != 0;
   prof_end(st, bytes, 4.0 * (double)n * tick_sync_streams(d) + pstore,
            d.nc | (inl << 4) | (d.na << 8) | (d.ng << 16) | (d.nf << 24) |
-               (int)((unsigned)pulls << 31));
+               (int)((unsigned)pulls << 31),
+           std::max(remote, rstore));
   note_sync(d);
   launches_++;
   alg_bytes_ += bytes;
@@ -578,7 +584,8 @@ void Engine::prof_begin(cudaStream_t st) {
   cudaEventRecord(ev_[ev_used_], st);
 }
 
-void Engine::prof_end(cudaStream_t st, double bytes, double sync_bytes, int32_t shape) {
+void Engine::prof_end(cudaStream_t st, double bytes, double sync_bytes, int32_t shape,
+                      double link_bytes) {
   if (!prof_on_ || ev_.size() < ev_used_ + 2) return;
   cudaEventRecord(ev_[ev_used_ + 1], st);
   ev_used_ += 2;
@@ -587,6 +594,15 @@ void Engine::prof_end(cudaStream_t st, double bytes, double sync_bytes, int32_t 
   prof_launch_bytes_.push_back(bytes);
   prof_launch_sync_.push_back(sync_bytes);
   prof_launch_shape_.push_back(shape);
+  prof_launch_link_.push_back(link_bytes);
+}
+
+hp_status Engine::profile_link(int64_t max, double* link_bytes, int64_t* n) {
+  if (sticky_) return sticky_;
+  const int64_t cnt = std::min<int64_t>(max, (int64_t)prof_launch_link_.size());
+  for (int64_t i = 0; i < cnt && link_bytes; ++i) link_bytes[i] = prof_launch_link_[i];
+  if (n) *n = cnt;
+  return HP_OK;
 }
 
 // Append the segments of a source covering global range [a, a+len): the acc
@@ -1120,7 +1136,10 @@ hp_status Engine::flush_lockstep(int slot) {
     const double bytes = 4.0 * n * (2 + G_ + (pull ? G_ : 0));
     prof_begin(xs_);
     const int err = launch_nvls(d, xs_, xblocks_);
-    prof_end(xs_, bytes, bytes, (N_ << 8) | (pull ? (int)(1u << 31) : 0));
+    // per GPU and direction: its acc replica served to every owner's reduction
+    // (4P through the switch) + the multicast store (4n out / 4P in)
+    prof_end(xs_, bytes, bytes, (N_ << 8) | (pull ? (int)(1u << 31) : 0),
+             4.0 * P + (pull ? 4.0 * n : 0.0));
     if (pull) note_pulls(bpull_);
     launches_++;
     alg_bytes_ += bytes;
@@ -1134,7 +1153,7 @@ hp_status Engine::flush_lockstep(int slot) {
     prof_begin(xs_);
     if (int e = comm_->reduce_scatter_v(s.acc[slot], x, shard_b_.data(), xs_))
       return fail(HP_ERR_COMM, comm_->error());
-    prof_end(xs_, 4.0 * (P + n), 4.0 * (P + n), (1 << 8) | (127 << 24));
+    prof_end(xs_, 4.0 * (P + n), 4.0 * (P + n), (1 << 8) | (127 << 24), 4.0 * n * (G_ - 1));
     TickDesc d;
     memset(&d, 0, sizeof d);
     d.s[0].ptr = x;
@@ -1148,7 +1167,8 @@ hp_status Engine::flush_lockstep(int slot) {
       prof_begin(xs_);
       if (int e = comm_->all_gather_v(wg_, s.wl, shard_b_.data(), xs_))
         return fail(HP_ERR_COMM, comm_->error());
-      prof_end(xs_, 4.0 * (P + n), 4.0 * (P + n), (1 << 16) | (127 << 24) | (int)(1u << 31));
+      prof_end(xs_, 4.0 * (P + n), 4.0 * (P + n), (1 << 16) | (127 << 24) | (int)(1u << 31),
+               4.0 * (P - n));
       note_pulls(bpull_);
     }
     nvl_bytes_ += 4.0 * n * (G_ - 1) + (pull ? 4.0 * (P - n) : 0.0);
@@ -1383,6 +1403,7 @@ hp_status Engine::profile_enable(bool on) {
   prof_launches_ = 0;
   prof_launch_bytes_.clear();
   prof_launch_sync_.clear();
+  prof_launch_link_.clear();
   prof_launch_shape_.clear();
   push_launch_.assign(N_, -1);
   sync_recs_.clear();

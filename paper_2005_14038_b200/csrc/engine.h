@@ -106,6 +106,7 @@ class Engine {
   hp_status profile_sync(int64_t max, float* ms, int32_t* vw, int64_t* n);
   hp_status profile_launches(int64_t max, float* ms, double* bytes, int32_t* shape,
                              double* sync_bytes, float* start_ms, int64_t* n);
+  hp_status profile_link(int64_t max, double* link_bytes, int64_t* n);
   int64_t ticks = 0;
 
  private:
@@ -130,7 +131,8 @@ class Engine {
   hp_status flush_lockstep(int slot);        // its NCCL / NVLS exchange
   hp_status finish_connect(const void* comm_id);
   void prof_begin(cudaStream_t st);
-  void prof_end(cudaStream_t st, double bytes, double sync_bytes, int32_t shape);
+  void prof_end(cudaStream_t st, double bytes, double sync_bytes, int32_t shape,
+                double link_bytes = 0);
   hp_status emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st = nullptr,
                  int max_blocks = 0);
   void fork_streams();
@@ -211,6 +213,7 @@ class Engine {
   double prof_bytes_ = 0;
   std::vector<double> prof_launch_bytes_;
   std::vector<double> prof_launch_sync_;
+  std::vector<double> prof_launch_link_;   // NVLink bytes per direction (max of in, out)
   std::vector<int32_t> prof_launch_shape_;
   // wave-sync latency: profiled launch that carried VW v's wave-end COMPLETE
   // (its u~ final = the push) -> the launch that wrote its pulled w_local

@@ -100,6 +100,7 @@ EXPORTS = {
     "hp_profile_launches": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.POINTER(C.c_int64)]),
+    "hp_profile_link": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_int64)]),
     "hp_profile_sync_latency": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                           C.POINTER(C.c_int64)]),
     "hp_partition": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
@@ -351,6 +352,17 @@ def _profile_sync_latency(self, max_records: int = 1 << 16):
 
 
 Context.profile_sync_latency = _profile_sync_latency
+
+
+def _profile_link(self, max_records: int = 1 << 16):
+    out = np.zeros(max_records, dtype=np.float64)
+    n = C.c_int64()
+    self._chk(self.lib.hp_profile_link(self.h, max_records, out.ctypes.data_as(C.c_void_p),
+                                       C.byref(n)))
+    return out[:n.value]
+
+
+Context.profile_link = _profile_link
 
 
 def comm_unique_id(lib: Optional[C.CDLL] = None) -> bytes:
