@@ -55,7 +55,7 @@ typedef enum {
   HP_ERR_INVALID = -1,    /* bad argument */
   HP_ERR_PROTOCOL = -2,   /* out-of-order / duplicate / incomplete */
   HP_ERR_CUDA = -3,       /* sticky CUDA failure */
-  HP_ERR_COMM = -4,       /* reserved: inter-GPU transport failure */
+  HP_ERR_COMM = -4,       /* inter-GPU transport (NCCL) failure */
   HP_ERR_OOM = -5,        /* device allocation failed */
   HP_ERR_STATE = -6       /* call not valid in this context state */
 } hp_status;
@@ -139,6 +139,9 @@ typedef struct {
                               and multicast mappings go to hp_connect_symmetric);
                               NULL = the library allocates it */
 } hp_config;
+
+/* sizeof(hp_config) as compiled into the library (bindings check their layout). */
+size_t hp_config_size(void);
 
 /* Fill cfg with defaults (N=1, Nm=1, D=0, lr=0.01, FLOAT grads, PHILOX w0,
    EAGER, STRICT, deferred applies, R=2, merged ticks, device 0, library stream). */

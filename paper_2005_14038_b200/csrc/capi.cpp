@@ -131,6 +131,8 @@ hp_status guard_device(hp_ctx* ctx) {
 
 extern "C" {
 
+size_t hp_config_size(void) { return sizeof(hp_config); }
+
 void hp_config_default(hp_config* c) {
   if (!c) return;
   memset(c, 0, sizeof *c);

@@ -68,6 +68,7 @@ class HetPipeError(RuntimeError):
 _lib = None
 
 EXPORTS = {
+    "hp_config_size": (C.c_size_t, []),
     "hp_config_default": (None, [C.POINTER(hp_config)]),
     "hp_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32,
                           C.c_int64, C.c_float]),
@@ -135,7 +136,10 @@ def load() -> C.CDLL:
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2005_14038_b200.build`")
-        _lib = _bind(C.CDLL(LIB_PATH))
+        lib = _bind(C.CDLL(LIB_PATH))
+        if lib.hp_config_size() != C.sizeof(hp_config):
+            raise ImportError("hp_config layout of the binding does not match libhetpipe.so")
+        _lib = lib
     return _lib
 
 

@@ -78,3 +78,11 @@ def test_sources_share_nothing_with_oracle():
         if f.endswith(".py"):
             src = open(os.path.join(ROOT, "oracle", f)).read()
             assert not re.search(r"^\s*(from|import)\s+paper_2005_14038_b200", src, re.M), f
+
+
+def test_config_layout_matches_library():
+    import ctypes
+    from paper_2005_14038_b200 import hetpipe
+    lib = hetpipe.load()
+    assert lib.hp_config_size() == ctypes.sizeof(hetpipe.hp_config)
+    assert ctypes.sizeof(hetpipe.hp_stats) >= 8 * 4 + 8 * 16 + 8
