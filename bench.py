@@ -343,7 +343,8 @@ def main():
     # device time during which at least one tick kernel runs (union of the
     # launch intervals: the distributed placements launch on several streams)
     busy_ms, cur_a, cur_b = 0.0, None, None
-    for a, d in sorted(zip((float(x) for x in l_t0), (float(x) for x in l_ms))):
+    for a, d in sorted((float(t0), float(t)) for t0, t, by in zip(l_t0, l_ms, l_bytes)
+                       if by > 0):      # barriers (0 bytes) are not kernel time
         if cur_b is None or a > cur_b:
             if cur_b is not None:
                 busy_ms += cur_b - cur_a
@@ -377,6 +378,8 @@ def main():
                f"f{(sh >> 24) & 127}")
         if (sh >> 24) & 127 == 127:
             key = "nccl_reduce_scatter" if (sh >> 8) & 255 else "nccl_all_gather"
+        elif (sh >> 24) & 127 == 126:
+            key = "barrier"
         e = mix.setdefault(key, [0, 0.0, 0.0])
         e[0] += 1
         e[1] += float(t_ms)

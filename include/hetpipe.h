@@ -277,7 +277,8 @@ hp_status hp_profile_read(hp_ctx* ctx, double* kernel_ms, double* alg_bytes,
    algorithmic bytes, and shape = nc | ni<<4 | na<<8 | ng<<16 | nf<<24 | pull<<31
    (completes, inline folds, memory applies, w_local groups, group folds, and
    whether a pull is in the fused launch; nf = 127 marks an NCCL collective of
-   HP_XPORT_NCCL: na = 1 the reduce-scatter, ng = 1 the all-gather), and
+   HP_XPORT_NCCL: na = 1 the reduce-scatter, ng = 1 the all-gather; nf = 126
+   the 4-byte NCCL barrier of a distributed exchange), and
    sync_bytes = the part of
    alg_bytes that is synchronisation (w_global/m traffic, u~ reads of the
    applies, pull writes of w_local; the rest is wave accumulation and folds).

@@ -130,6 +130,7 @@ class Engine {
   int lockstep_slot() const;                 // acc slot of a lockstep batch, or -1
   hp_status flush_lockstep(int slot);        // its NCCL / NVLS exchange
   hp_status finish_connect(const void* comm_id);
+  hp_status xbarrier();
   void prof_begin(cudaStream_t st);
   void prof_end(cudaStream_t st, double bytes, double sync_bytes, int32_t shape,
                 double link_bytes = 0);
