@@ -17,7 +17,7 @@ import copy
 import numpy as np
 import pytest
 
-from oracle.wsp import WSPOracle, gradient, initial_weights, wave_range
+from oracle.wsp import WSPOracle, clock_range, gradient, initial_weights, wave_range
 from workloads import (GRAD_DYADIC, LOCAL_AT_LEAST, LOCAL_STRICT, PULL_EAGER,
                        PULL_LAZY, W0_PHILOX, WSPConfig)
 
@@ -31,8 +31,9 @@ def _key(sm):
 def explore(cfg):
     idx = np.arange(8)
     w0 = initial_weights(idx, cfg).astype(np.float64)
+    CU = cfg.F * cfg.Nm                    # minibatches per clock (F waves)
     U = {(v, p): -float(np.float32(cfg.lr)) * gradient(idx, v, p, cfg).astype(np.float64)
-         for v in range(cfg.num_vw) for p in range(1, cfg.waves * cfg.Nm + 1)}
+         for v in range(cfg.num_vw) for p in range(1, cfg.waves * CU + 1)}
 
     def version(v, a_v, prefix):
         tot = w0.copy()
@@ -40,7 +41,7 @@ def explore(cfg):
             tot += U[(v, q)]
         for (vv, c) in prefix:
             if vv != v:
-                lo, hi = wave_range(c, cfg.Nm)
+                lo, hi = clock_range(c, CU)
                 for q in range(lo, hi + 1):
                     tot += U[(vv, q)]
         return tot
@@ -67,7 +68,7 @@ def explore(cfg):
             p = sm.completed[v] + 1
             wave_end, start_next = sm.complete(0, v, p)
             if wave_end:
-                sm.push(0, v, (p - 1) // cfg.Nm)
+                sm.push(0, v, (p - 1) // CU)
             if start_next:
                 sm.start(0, v, p + cfg.Nm)
         else:
@@ -155,6 +156,37 @@ def test_bruteforce_nm3(D, expected):
     (22.4M / 56.4M / 57.1M)."""
     n, _ = explore(_cfg(3, D))
     assert n == expected
+
+
+@pytest.mark.parametrize("Nm,D,sem", [(1, 0, LOCAL_STRICT), (1, 1, LOCAL_STRICT),
+                                      (2, 0, LOCAL_STRICT), (2, 1, LOCAL_AT_LEAST)])
+def test_bruteforce_update_frequency(Nm, D, sem):
+    """NEXT-4 (F = 2 waves per clock): every admissible
+    interleaving of 2 VW x 2 clocks keeps START snapshots = version-set sums,
+    a_v = p - Nm (STRICT) and the clock bound; gates only at (c+2) F Nm."""
+    cfg = WSPConfig("bf", 2, Nm, D, 8, 2, (1, 1), lr=2.0 ** -6, grad_mode=GRAD_DYADIC,
+                    w0_mode=W0_PHILOX, local_semantics=sem, F=2)
+    n, stats = explore(cfg)
+    assert n > 0 and stats["starts"] > 0
+
+
+def test_bruteforce_update_frequency_counts():
+    """F = 2, Nm = 1, 2 clocks: each VW runs C1, C2 (push of clock 0), C3 (it
+    reaches the gate of minibatch (0+2)*F*Nm = 4), ADMIT, C4 (push of clock 1).
+    With D = 0 its ADMIT needs the other VW's clock-0 push (c_local - c_global
+    <= 0); with D = 1 nothing binds. Counted here directly over merges of
+    the two 5-step sequences (independent of the oracle) and compared with the
+    oracle's exhaustive exploration."""
+    import itertools
+    for D in (0, 1):
+        n = 0
+        for xs in itertools.combinations(range(10), 5):   # positions of VW 0's steps
+            ys = [i for i in range(10) if i not in xs]
+            ok = D >= 1 or (xs[3] > ys[1] and ys[3] > xs[1])
+            n += ok
+        cfg = WSPConfig("bf", 2, 1, D, 8, 2, (1, 1), lr=2.0 ** -6, grad_mode=GRAD_DYADIC,
+                        w0_mode=W0_PHILOX, F=2)
+        assert explore(cfg)[0] == n == {0: 200, 1: 252}[D]
 
 
 def test_pins_catch_plausible_mistakes(monkeypatch):
