@@ -465,7 +465,8 @@ hp_status Engine::tick_end(std::vector<std::pair<int, int64_t>>* ungated) {
 // Batch -> TickDesc(s). Algorithmic bytes are counted from the descriptor: each
 // buffer read or written once per launch = 4 bytes per param of the launch's
 // range [begin, begin+n); reads through peer segments are also NVLink bytes.
-hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, int max_blocks) {
+hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, int max_blocks,
+                       double link_bytes) {
   if (!st) st = stream_;
   d.n = n;
   d.blk_base = begin >> 2;
@@ -523,7 +524,7 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   prof_end(st, bytes, 4.0 * (double)n * tick_sync_streams(d) + pstore,
            d.nc | (inl << 4) | (d.na << 8) | (d.ng << 16) | (d.nf << 24) |
                (int)((unsigned)pulls << 31),
-           std::max(remote, rstore));
+           link_bytes >= 0 ? link_bytes : std::max(remote, rstore));
   note_sync(d);
   launches_++;
   alg_bytes_ += bytes;
@@ -920,6 +921,34 @@ hp_status Engine::flush_dist() {
   }
   const bool fuse_pull = push_pull_ && strict && !ba_.empty() && !bpull_.empty() &&
                          ptargets.size() <= (size_t)kMaxP;
+  // NVLink traffic of this rank's links while every owner runs its apply
+  // launch at once (the barrier aligns them): the ũ slices it loads from peers
+  // and the owner-side pull stores it receives (in), what peers load from it and
+  // the stores it sends (out); reported per direction as max(in, out)
+  double x_in = 0, x_out = 0;
+  auto flow = [&](int from, int to, double bytes) {
+    if (from == to) return;
+    if (to == rank_) x_in += bytes;
+    if (from == rank_) x_out += bytes;
+  };
+  for (int o = 0; o < G_ && !ba_.empty(); ++o) {
+    const int64_t s0 = shard_b_[o], s1 = shard_b_[o + 1];
+    for (const BApply& a : ba_)
+      for (int g = 0; g < G_; ++g) {
+        const RankLayout& L = lay_[g];
+        if (!L.has[a.v]) continue;
+        const int64_t x0 = std::max(L.a[a.v], s0), x1 = std::min(L.a[a.v] + L.len[a.v], s1);
+        if (x1 > x0) flow(g, o, 4.0 * (double)(x1 - x0));
+      }
+    if (fuse_pull)
+      for (const Prim& pr : prims) {
+        const int64_t x0 = std::max(pr.a, s0), x1 = std::min(pr.a + pr.len, s1);
+        if (x1 > x0) flow(o, pr.q, 4.0 * (double)(x1 - x0));
+      }
+  }
+  int n_apply_launches = 0;
+  for (size_t k2 = 0; k2 < ba_.size(); k2 += kMaxA) ++n_apply_launches;
+  const double x_link = n_apply_launches ? std::max(x_in, x_out) / n_apply_launches : 0.0;
   if (!ba_.empty()) {
     for (const BApply& a : ba_) xs_wait(a.v);
     for (int v : bpull_) {
@@ -941,7 +970,7 @@ hp_status Engine::flush_dist() {
       }
       if (fuse_pull && k == ba_.size())
         for (const DStore& t : ptargets) d.pd[d.np++] = t;
-      if (hp_status st = emit(d, begin_, n_, xs_, xblocks_)) return st;
+      if (hp_status st = emit(d, begin_, n_, xs_, xblocks_, x_link)) return st;
     }
     applied_ += (int64_t)ba_.size();
     if (hp_status st = xbarrier()) return st;
@@ -1026,6 +1055,32 @@ hp_status Engine::flush_dist() {
     }
     pranges.clear();
   }
+  // reader-side pull traffic of this rank's links while every rank pulls: the
+  // remote shards its stage ranges read (in) and what the other GPUs' ranges
+  // read from its shard (out)
+  double r_link = 0;
+  if (!pranges.empty()) {
+    double r_in = 0, r_out = 0;
+    for (int g = 0; g < G_; ++g) {
+      std::vector<std::pair<int64_t, int64_t>> rr;
+      for (int v : bpull_) {
+        const RankLayout& L = lay_[g];
+        if (!L.has[v]) continue;
+        auto key = std::make_pair(L.a[v], L.len[v]);
+        if (std::find(rr.begin(), rr.end(), key) == rr.end()) rr.push_back(key);
+      }
+      for (auto& r : rr)
+        for (int o = 0; o < G_; ++o) {
+          if (o == g) continue;
+          const int64_t x0 = std::max(r.first, shard_b_[o]);
+          const int64_t x1 = std::min(r.first + r.second, shard_b_[o + 1]);
+          if (x1 <= x0) continue;
+          if (g == rank_) r_in += 4.0 * (double)(x1 - x0);
+          if (o == rank_) r_out += 4.0 * (double)(x1 - x0);
+        }
+    }
+    r_link = std::max(r_in, r_out) / (double)pranges.size();
+  }
   for (auto& rg : pranges) {
     TickDesc d;
     auto fresh = [&]() {
@@ -1044,7 +1099,7 @@ hp_status Engine::flush_dist() {
       bool first_part = true;
       do {
         if (d.ng == kMaxG || d.nf == kMaxF) {
-          if (hp_status st = emit(d, rg.first, rg.second, xs_, xblocks_)) return st;
+          if (hp_status st = emit(d, rg.first, rg.second, xs_, xblocks_, r_link)) return st;
           fresh();
         }
         DGroup& g = d.g[d.ng++];
@@ -1063,7 +1118,7 @@ hp_status Engine::flush_dist() {
         g.f_end = d.nf;
       } while (fi < folds.size());
     }
-    if (hp_status st = emit(d, rg.first, rg.second, xs_, xblocks_)) return st;
+    if (hp_status st = emit(d, rg.first, rg.second, xs_, xblocks_, r_link)) return st;
   }
   if (!bpull_.empty()) {
     cudaEvent_t e = pool_event();       // w_local of the pulled VWs is written

@@ -135,7 +135,7 @@ class Engine {
   void prof_end(cudaStream_t st, double bytes, double sync_bytes, int32_t shape,
                 double link_bytes = 0);
   hp_status emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st = nullptr,
-                 int max_blocks = 0);
+                 int max_blocks = 0, double link_bytes = -1);
   void fork_streams();
   cudaEvent_t pool_event();
   hp_status join_exchange();          // compute stream waits for the exchange stream

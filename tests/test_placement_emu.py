@@ -157,3 +157,38 @@ def test_bad_ps_bounds(lib):
         with pytest.raises(hetpipe.HetPipeError):
             hetpipe.Context(hetpipe.config_from(cfg, world=2, rank=0, vw_span=1, ps_bounds=bad),
                             lib=lib)
+
+
+def test_exchange_link_bytes_lockstep_peer(lib):
+    """hp_profile_link: while every owner runs its apply launch of a lockstep
+    batch (4 VWs, one per GPU, k = 1, equal speeds), each GPU's links carry in
+    one direction the 3 remote u~ slices it loads plus the 3 owner-side pull
+    stores it receives (or, out, the same from the other side): 6 x 4n bytes;
+    the last round has no pull (Z16), so only the 3 loads."""
+    from paper_2005_14038_b200 import hetpipe
+    G, P = 4, 4096
+    cfg = WSPConfig("lk", G, 2, 0, P, 3, (5,) * G)
+    cid = hetpipe.comm_unique_id(lib)
+    ctxs = [hetpipe.Context(hetpipe.config_from(cfg, world=G, rank=r, vw_span=1), lib=lib)
+            for r in range(G)]
+    handles = [c.ipc_handle() for c in ctxs]
+    links = [None] * G
+
+    def work(r):
+        c = ctxs[r]
+        c.connect(handles, cid)
+        c.profile_enable(True)
+        c.run_schedule(cfg.tau, cfg.latency())
+        links[r] = [x for x in c.profile_link() if x > 0]
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(60)
+    n = P // G
+    for r in range(G):
+        assert links[r][:-1] == [6 * 4 * n] * (cfg.waves - 1), links[r]
+        assert links[r][-1] == 3 * 4 * n
+    for c in ctxs:
+        c.close()
