@@ -836,7 +836,7 @@ hp_status Engine::flush_dist() {
       // acc part now (its slot is free once the exchange that read it is done)
       if (d.nc) {
         for (int j = 0; j < d.nc; ++j) wait_clear(vs_[v], xacc_[v][cslot[j]]);
-        if (hp_status st = emit(d, s.a0, s.len, vs_[v])) return st;
+        if (hp_status st = emit(d, s.a0, s.len, vs_[v], ablocks_)) return st;
         lastc_[v] = pool_event();
         cudaEventRecord(lastc_[v], vs_[v]);
         memset(&d, 0, sizeof d);
@@ -858,7 +858,7 @@ hp_status Engine::flush_dist() {
     size_t fi = 0;
     while (fi < folds.size()) {
       if (d.ng == kMaxG || d.nf == kMaxF) {
-        if (hp_status st = emit(d, s.a0, s.len, fst)) return st;
+        if (hp_status st = emit(d, s.a0, s.len, fst, ablocks_)) return st;
         memset(&d, 0, sizeof d);
       }
       DGroup& g = d.g[d.ng++];
@@ -873,7 +873,7 @@ hp_status Engine::flush_dist() {
       }
       g.f_end = d.nf;
     }
-    if (hp_status st = emit(d, s.a0, s.len, fst)) return st;
+    if (hp_status st = emit(d, s.a0, s.len, fst, ablocks_)) return st;
     cudaEvent_t e = pool_event();
     cudaEventRecord(e, fst);
     if (d.nc || fst == vs_[v]) lastc_[v] = e;
@@ -1404,6 +1404,7 @@ hp_status Engine::finish_connect(const void* comm_id) {
         return check_cuda(e, "stream");
     }
   if (const char* xb = getenv("HP_XBLOCKS")) xblocks_ = atoi(xb);
+  if (const char* ab = getenv("HP_ABLOCKS")) ablocks_ = atoi(ab);
   // everyone's init writes are complete before anyone reads a peer
   if (int e = comm_->barrier(stream_)) return fail(HP_ERR_COMM, comm_->error());
   return check_cuda(cudaStreamSynchronize(stream_), "connect sync");

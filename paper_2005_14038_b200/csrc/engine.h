@@ -180,6 +180,7 @@ class Engine {
   bool push_pull_ = true;             // owner-side pull (HP_PULL_PUSH=0: reader-side)
   bool forked_ = false;               // side streams ordered after the context stream
   int xblocks_ = 0;                   // grid bound of exchange launches (HP_XBLOCKS)
+  int ablocks_ = 0;                   // grid bound of accumulation launches (HP_ABLOCKS)
   std::vector<cudaEvent_t> evpool_;
   size_t evnext_ = 0;
   double nvl_bytes_ = 0;
