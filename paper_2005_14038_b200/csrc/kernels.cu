@@ -61,9 +61,33 @@ __device__ __forceinline__ float4 f4scale(float s, float4 a) {
 
 // Chunk access: CNT == 4 is a full aligned float4; CNT < 4 the ragged tail
 // (element-wise, zero-filled), only ever executed by one thread.
+// HP_LD_VARIANT (compile time, tuning experiments): 0 = ld.global.cs (default),
+// 1 = ld.global.cs.L2::256B, 2 = ld.global.L1::no_allocate.L2::256B, 3 = ld.global
+#ifndef HP_LD_VARIANT
+#define HP_LD_VARIANT 0
+#endif
+__device__ __forceinline__ float4 ldv4(const float4* p) {
+#if HP_LD_VARIANT == 0
+  return __ldcs(p);
+#else
+  float4 r;
+#if HP_LD_VARIANT == 1
+  asm volatile("ld.global.cs.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+#elif HP_LD_VARIANT == 2
+  asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+#else
+  asm volatile("ld.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+#endif
+  return r;
+#endif
+}
+
 template <int CNT>
 __device__ __forceinline__ float4 ld4(const float* base, int64_t q) {
-  if (CNT == 4) return __ldcs(reinterpret_cast<const float4*>(base) + q);
+  if (CNT == 4) return ldv4(reinterpret_cast<const float4*>(base) + q);
   float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
   const float* p = base + 4 * q;
   r.x = p[0];

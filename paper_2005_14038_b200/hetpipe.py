@@ -12,7 +12,9 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhetpipe.so")
+# HP_LIB: another build of the same library (e.g. a tuning variant) -- still
+# the in-tree CUDA library; there is no CPU fallback
+LIB_PATH = os.environ.get("HP_LIB") or os.path.join(_HERE, "libhetpipe.so")
 
 HP_OK, HP_WOULD_BLOCK = 0, 1
 HP_ERR_INVALID, HP_ERR_PROTOCOL, HP_ERR_CUDA = -1, -2, -3
