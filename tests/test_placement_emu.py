@@ -166,6 +166,8 @@ def test_exchange_link_bytes_lockstep_peer(lib):
     stores it receives (or, out, the same from the other side): 6 x 4n bytes;
     the last round has no pull (Z16), so only the 3 loads."""
     from paper_2005_14038_b200 import hetpipe
+    if os.environ.get("HP_PULL_PUSH") == "0":
+        pytest.skip("reader-side pulls forced: other launch structure")
     G, P = 4, 4096
     cfg = WSPConfig("lk", G, 2, 0, P, 3, (5,) * G)
     cid = hetpipe.comm_unique_id(lib)
