@@ -266,15 +266,11 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
   const int slot = (int)(c % R_);
   const bool first = (p - 1) % U_ == 0;
   // F > 1, STRICT: the first completion joining a waiting VW's open clock
-  // snapshots that clock's aggregate for the pull (reading Z25)
-  if (s.at_gate && U_ > Nm_ && cfg_.local_semantics == HP_LOCAL_STRICT && s.backlog.empty() &&
-      s.acc_count > 0 && !first) {
-    if (hp_status st = flush()) return st;
-    if (hp_status st = check_cuda(cudaMemcpyAsync(s.snap, s.acc[slot], (size_t)s.len * 4,
-                                                  cudaMemcpyDeviceToDevice, stream_), "snapshot"))
-      return st;
-    s.snap_valid = true;
-  }
+  // snapshots that clock's aggregate for the pull (reading Z25): its launch
+  // copies the acc it loads, before adding u (kSnapAcc)
+  const bool snap = s.at_gate && U_ > Nm_ && cfg_.local_semantics == HP_LOCAL_STRICT &&
+                    s.backlog.empty() && s.acc_count > 0 && !first;
+  if (snap) s.snap_valid = true;
   if (first) {  // the slot must not hold a pushed wave that is not applied yet
     bool busy = false;
     for (auto& a : pending_applies_) busy |= (a.v == v && a.slot == slot);
@@ -305,7 +301,7 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
   const bool wave_end = p % U_ == 0;          // the clock's last minibatch: push
   // START(p+Nm) is the gated one iff p+Nm = (c+2)*U (with F)
   const bool gated_next = (p + Nm_) % U_ == 0 && p + Nm_ >= 2 * U_ && p + Nm_ <= last_p_;
-  bc_.push_back({v, p, slot, first, wave_end, g});
+  bc_.push_back({v, p, slot, first, wave_end, g, snap});
   s.completed = p;
   s.acc_count = first ? 1 : s.acc_count + 1;
   if (!s.at_gate) {
@@ -671,9 +667,10 @@ hp_status Engine::flush_local() {
     c.grad = b.grad;
     c.wl = nullptr;
     c.stash = convex_ ? vw_[b.v].stash[(b.p - 1) % Nm_] : nullptr;
+    c.snap = b.snap ? vw_[b.v].snap : nullptr;
     c.v = (uint32_t)b.v;
     c.p = (uint32_t)b.p;
-    c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc;
+    c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc | (b.snap ? kSnapAcc : 0u);
   }
   // 2. applies in commit order. The longest suffix whose waves were completed
   //    in this batch, in complete order, is applied straight from registers in

@@ -116,6 +116,7 @@ class Engine {
     int slot;
     bool first, wave_end;
     const float* grad;
+    bool snap = false;   // F > 1: snapshot the acc it loads (first backlog completion)
   };
   struct BApply {
     int v;

@@ -202,6 +202,7 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
       const float4 u = (GM == 2) ? f4scale(d.neg_lr, gin[x])
                        : (GM == 3) ? convex_u(d, c.v, c.p, blk, gin[x])
                                    : synth_u<GM>(d, c.v, c.p, blk);
+      if (fl & kSnapAcc) st4<CNT>(c.snap, q, ain[x]);          // F > 1: acc at the gate
       const float4 a = (fl & kFirst) ? u : f4add(ain[x], u);   // wave aggregate
       if (fl & kStoreAcc) st4<CNT>(c.acc, q, a);
       if (fl & kApplyNow) apply<MOM>(wg[x], mm[x], a, d.mu);

@@ -31,7 +31,8 @@ enum : uint32_t {
   kLoadAcc = 4u,     // read the acc slot (not first)
   kApplyNow = 8u,    // w_global += a right after this complete (commit order)
   kFoldInline = 16u, // w_local(v) += u right here (the VW's only due fold)
-  kStashAfter = 32u  // CONVEX: START(p+Nm) reads the folded w_local -> stash slot
+  kStashAfter = 32u, // CONVEX: START(p+Nm) reads the folded w_local -> stash slot
+  kSnapAcc = 64u     // F > 1: copy the loaded acc (before this u) to `snap`
 };
 
 struct DComplete {
@@ -39,6 +40,7 @@ struct DComplete {
   const float* grad;   // EXTERNAL gradient (local shard) or nullptr
   float* wl;           // w_local for kFoldInline, else nullptr
   float* stash;        // CONVEX: slot (p-1) mod Nm holding w_p (kStashAfter rewrites it)
+  float* snap;         // kSnapAcc: the waiting VW's open-clock aggregate (reading Z25)
   uint32_t v, p;
   uint32_t flags;
   uint32_t pad;
@@ -120,7 +122,8 @@ inline int tick_streams(const TickDesc& d) {
   for (int j = 0; j < d.nc; ++j) {
     const uint32_t f = d.c[j].flags;
     s += ((f & kLoadAcc) ? 1 : 0) + ((f & kStoreAcc) ? 1 : 0) + (d.c[j].grad ? 1 : 0) +
-         ((f & kFoldInline) ? 2 : 0) + (d.c[j].stash ? 1 : 0) + ((f & kStashAfter) ? 1 : 0);
+         ((f & kFoldInline) ? 2 : 0) + (d.c[j].stash ? 1 : 0) + ((f & kStashAfter) ? 1 : 0) +
+         ((f & kSnapAcc) ? 1 : 0);
   }
   for (int g = 0; g < d.ng; ++g) {
     s += 1 + (d.g[g].pull == 1 ? 0 : 1) + (d.g[g].partial ? 1 : 0);

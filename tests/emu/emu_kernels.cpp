@@ -69,6 +69,7 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
     for (int j = 0; j < d.nc; ++j) {
       const DComplete& c = d.c[j];
       const float u = draw_u(d, gm, c.v, c.p, i, c.grad, c.stash);
+      if (c.flags & kSnapAcc) c.snap[i] = c.acc[i];
       const float a = (c.flags & kFirst) ? u : c.acc[i] + u;
       if (c.flags & kStoreAcc) c.acc[i] = a;
       if (c.flags & kApplyNow) app(d, mom, wg, m, a);
