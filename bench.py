@@ -230,6 +230,8 @@ def main():
                     help="synthetic gradient: weight-independent Philox FLOAT draws, or the "
                          "weight-dependent CONVEX workload (NEXT-2: every gradient reads the "
                          "w_local its minibatch saw at START, kept in a stash ring)")
+    ap.add_argument("--D", type=int, default=-1,
+                    help="override the config's clock-distance threshold D (C5's sweep: 0, 4, 32)")
     ap.add_argument("--update-freq", type=int, default=1,
                     help="F (NEXT-4): one clock = F waves; a step is still one WSP round "
                          "(N pushes), each push carrying F*Nm minibatches")
@@ -247,6 +249,8 @@ def main():
         cfg = cfg.replace(num_vw=nvw, tau=tuple((list(cfg.tau) * 8)[:nvw]))
     if args.update_freq > 1:
         cfg = cfg.replace(F=args.update_freq)
+    if args.D >= 0:
+        cfg = cfg.replace(D=args.D)
     if args.grad == "convex":
         from workloads import GRAD_CONVEX
         cfg = cfg.replace(grad_mode=GRAD_CONVEX)
