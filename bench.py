@@ -230,6 +230,9 @@ def main():
                     help="synthetic gradient: weight-independent Philox FLOAT draws, or the "
                          "weight-dependent CONVEX workload (NEXT-2: every gradient reads the "
                          "w_local its minibatch saw at START, kept in a stash ring)")
+    ap.add_argument("--pull", default="eager", choices=["eager", "lazy"],
+                    help="pull policy (reading Z6): every gate pulls, or only when the held "
+                         "version is older than the bound needs (P:932)")
     ap.add_argument("--D", type=int, default=-1,
                     help="override the config's clock-distance threshold D (C5's sweep: 0, 4, 32)")
     ap.add_argument("--update-freq", type=int, default=1,
@@ -251,6 +254,8 @@ def main():
         cfg = cfg.replace(F=args.update_freq)
     if args.D >= 0:
         cfg = cfg.replace(D=args.D)
+    if args.pull == "lazy":
+        cfg = cfg.replace(pull_policy=1)
     if args.grad == "convex":
         from workloads import GRAD_CONVEX
         cfg = cfg.replace(grad_mode=GRAD_CONVEX)
@@ -473,7 +478,7 @@ def main():
                     else "ED-local shards" if ws > 1 else "single GPU"),
                    "grad": ("CONVEX a(w_p - b) + sigma xi, w_p from the START stash"
                             if args.grad == "convex" else "Philox FLOAT in-kernel"),
-                   "pull": "EAGER", "local": "STRICT",
+                   "pull": args.pull.upper(), "local": "STRICT",
                    "apply": "on arrival" if args.apply_mode else "deferred to the observing pull",
                    "transport": args.transport if placed else None,
                    "ps_shards": args.ps if placed else None,
