@@ -34,6 +34,11 @@ class Comm {
   // recv + b[q] on every rank. One ncclBroadcast per shard in one group.
   virtual int all_gather_v(const float* send, float* recv, const int64_t* b,
                            cudaStream_t stream) = 0;
+  // The equal-count forms (ncclReduceScatter / ncclAllGather): send / recv
+  // hold world x count floats (rank q's block at q x count).
+  virtual int reduce_scatter(const float* send, float* recv, int64_t count,
+                             cudaStream_t stream) = 0;
+  virtual int all_gather(const float* send, float* recv, int64_t count, cudaStream_t stream) = 0;
   virtual std::string error() const = 0;
 };
 

@@ -28,6 +28,8 @@ struct Api {
   ncclResult_t (*Reduce)(const void*, void*, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -61,8 +63,10 @@ Api* api(std::string* err) {
   a.Broadcast = (decltype(a.Broadcast))dlsym(a.h, "ncclBroadcast");
   a.GroupStart = (decltype(a.GroupStart))dlsym(a.h, "ncclGroupStart");
   a.GroupEnd = (decltype(a.GroupEnd))dlsym(a.h, "ncclGroupEnd");
+  a.ReduceScatter = (decltype(a.ReduceScatter))dlsym(a.h, "ncclReduceScatter");
+  a.AllGather = (decltype(a.AllGather))dlsym(a.h, "ncclAllGather");
   if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.CommDestroy || !a.Reduce ||
-      !a.Broadcast || !a.GroupStart || !a.GroupEnd) {
+      !a.Broadcast || !a.GroupStart || !a.GroupEnd || !a.ReduceScatter || !a.AllGather) {
     a.h = nullptr;
     if (err) *err = "libnccl.so.2 lacks required symbols";
     return nullptr;
@@ -99,6 +103,13 @@ class NcclComm : public Comm {
                         ncclFloat32, q, c_, s);
     const ncclResult_t r2 = a_->GroupEnd();
     return note(r ? r : r2, "ncclBroadcast (all-gather)");
+  }
+  int reduce_scatter(const float* send, float* recv, int64_t count, cudaStream_t s) override {
+    return note(a_->ReduceScatter(send, recv, (size_t)count, ncclFloat32, ncclSum, c_, s),
+                "ncclReduceScatter");
+  }
+  int all_gather(const float* send, float* recv, int64_t count, cudaStream_t s) override {
+    return note(a_->AllGather(send, recv, (size_t)count, ncclFloat32, c_, s), "ncclAllGather");
   }
   std::string error() const override { return err_; }
 

@@ -40,6 +40,15 @@ std::vector<int64_t> even_bounds(int64_t P, int n) {
   b[n] = P;
   return b;
 }
+// ceil split: the first n-1 parts ceil(P/n) rounded up to 32 floats, the last
+// the (smaller) rest -- equal blocks for NCCL's equal-count collectives
+std::vector<int64_t> ceil_bounds(int64_t P, int n) {
+  const int64_t per = ((P + n - 1) / n + 31) / 32 * 32;
+  std::vector<int64_t> b(n + 1);
+  for (int i = 0; i < n; ++i) b[i] = std::min<int64_t>(per * i, P);
+  b[n] = P;
+  return b;
+}
 size_t align256(int64_t nfloat) { return ((size_t)std::max<int64_t>(nfloat, 1) * 4 + 255) / 256 * 256; }
 }  // namespace
 
@@ -80,11 +89,16 @@ RankLayout Engine::layout_of(int q) const {
       L.a[v] = stage_b_[j];
       L.len[v] = stage_b_[j + 1] - stage_b_[j];
       L.has[v] = 1;
+      // NCCL transport with full replicas: w_local and the acc slots padded to
+      // G x the largest shard, so ncclReduceScatter / ncclAllGather (equal
+      // counts) work on them directly; the padding is never read back
+      const int64_t alen = (cfg_.transport == HP_XPORT_NCCL && G_ > 1 && span_ == 1)
+                               ? std::max<int64_t>(L.len[v], (int64_t)G_ * smax) : L.len[v];
       L.wl_off[v] = off;
-      off += align256(L.len[v]);
+      off += align256(alen);
       for (int r = 0; r < R_; ++r) {
         L.acc_off[v][r] = off;
-        off += align256(L.len[v]);
+        off += align256(alen);
       }
       for (auto& so : L.stash_off[v]) {
         so = off;
@@ -132,6 +146,7 @@ hp_status Engine::check_cuda(int err, const char* what) {
 void Engine::plan_layout() {
   if (dist_) {
     if (cfg_.ps_bounds) shard_b_.assign(cfg_.ps_bounds, cfg_.ps_bounds + G_ + 1);
+    else if (cfg_.transport == HP_XPORT_NCCL) shard_b_ = ceil_bounds(cfg_.nparams, G_);
     else shard_b_ = even_bounds(cfg_.nparams, G_);
     stage_b_ = even_bounds(cfg_.nparams, span_);
   } else {
@@ -1211,8 +1226,16 @@ hp_status Engine::flush_lockstep(int slot) {
     float* x = (float*)((char*)arena_ + L.x_off);
     // the collectives are profiled like launches: bytes = what they read and
     // write in this rank's HBM (send buffer + received data)
+    int64_t smax = 0;
+    for (int q = 0; q < G_; ++q) smax = std::max(smax, shard_b_[q + 1] - shard_b_[q]);
+    // the NCCL transport's default shards (ceil split) are smax long but the
+    // last: the equal-count collectives run on the padded buffers; other
+    // bounds (hp_config.ps_bounds) take the grouped per-shard form
+    bool equal = true;
+    for (int q = 0; q + 1 < G_; ++q) equal &= shard_b_[q + 1] - shard_b_[q] == smax;
     prof_begin(xs_);
-    if (int e = comm_->reduce_scatter_v(s.acc[slot], x, shard_b_.data(), xs_))
+    if (int e = equal ? comm_->reduce_scatter(s.acc[slot], x, smax, xs_)
+                      : comm_->reduce_scatter_v(s.acc[slot], x, shard_b_.data(), xs_))
       return fail(HP_ERR_COMM, comm_->error());
     prof_end(xs_, 4.0 * (P + n), 4.0 * (P + n), (1 << 8) | (127 << 24), 4.0 * n * (G_ - 1));
     TickDesc d;
@@ -1226,7 +1249,8 @@ hp_status Engine::flush_lockstep(int slot) {
     if (hp_status st = emit(d, begin_, n_, xs_)) return st;
     if (pull) {
       prof_begin(xs_);
-      if (int e = comm_->all_gather_v(wg_, s.wl, shard_b_.data(), xs_))
+      if (int e = equal ? comm_->all_gather(wg_, s.wl, smax, xs_)
+                        : comm_->all_gather_v(wg_, s.wl, shard_b_.data(), xs_))
         return fail(HP_ERR_COMM, comm_->error());
       prof_end(xs_, 4.0 * (P + n), 4.0 * (P + n), (1 << 16) | (127 << 24) | (int)(1u << 31),
                4.0 * (P - n));

@@ -283,7 +283,9 @@ class Context:
         if c.world <= 1:
             return c.param_count
         if which < 0:
-            b = getattr(c, "_ps_list", None) or even_shards(c.nparams, c.world)
+            from workloads import ceil_shards
+            b = (getattr(c, "_ps_list", None)
+                 or (ceil_shards if c.transport == XPORT_NCCL else even_shards)(c.nparams, c.world))
             return b[c.rank + 1] - b[c.rank]
         for j in range(c.vw_span):
             if (which * c.vw_span + j) % c.world == c.rank:

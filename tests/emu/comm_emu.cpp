@@ -67,6 +67,26 @@ class EmuComm : public Comm {
     b_->wait();
     return 0;
   }
+  int reduce_scatter(const float* send, float* recv, int64_t count, cudaStream_t) override {
+    b_->posted[rank_] = send;
+    b_->wait();
+    for (int64_t i = 0; i < count; ++i) {
+      const int64_t j = (int64_t)rank_ * count + i;
+      float s = b_->posted[0][j];
+      for (int q = 1; q < b_->world; ++q) s = s + b_->posted[q][j];
+      recv[i] = s;
+    }
+    b_->wait();
+    return 0;
+  }
+  int all_gather(const float* send, float* recv, int64_t count, cudaStream_t) override {
+    b_->posted[rank_] = send;
+    b_->wait();
+    for (int q = 0; q < b_->world; ++q)
+      for (int64_t i = 0; i < count; ++i) recv[(int64_t)q * count + i] = b_->posted[q][i];
+    b_->wait();
+    return 0;
+  }
   std::string error() const override { return ""; }
 
  private:

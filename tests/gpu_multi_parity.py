@@ -17,7 +17,8 @@ sys.path.insert(0, ROOT)
 
 from oracle import run_schedule  # noqa: E402
 from paper_2005_14038_b200 import dist as hdist  # noqa: E402
-from workloads import C3, C4, C5, C5E, GRAD_DYADIC, WSPConfig, sample_indices, even_shards  # noqa: E402
+from workloads import (C3, C4, C5, C5E, GRAD_DYADIC, WSPConfig, ceil_shards,  # noqa: E402
+                       sample_indices, even_shards)
 
 from workloads import models as M  # noqa: E402
 
@@ -156,7 +157,8 @@ def main():
         cfg, k, mode, xport, exact, want_lock = case[:6]
         if cfg is None:
             continue
-        bounds = (M.layer_rr_bounds(M.vgg19(), G) if len(case) > 6 else None)
+        bounds = (M.layer_rr_bounds(M.vgg19(), G) if len(case) > 6 else
+                  ceil_shards(cfg.nparams, G) if xport == "nccl" else None)
         sampled = (sample_indices(cfg.nparams, 104729, bounds or even_shards(cfg.nparams, G))
                    if mode else None)
         objs = run(cfg, G, k, rank, local, sampled, xport, bounds)

@@ -125,6 +125,13 @@ def even_shards(nparams: int, nshards: int, align: int = 32) -> Sequence[int]:
     return bounds
 
 
+def ceil_shards(nparams: int, nshards: int, align: int = 32) -> Sequence[int]:
+    """The NCCL transport's default shards: the first G-1 equal (ceil, rounded
+    up to `align`), the last the rest."""
+    per = (-(-nparams // nshards) + align - 1) // align * align
+    return [min(s * per, nparams) for s in range(nshards)] + [nparams]
+
+
 def sample_indices(nparams: int, stride: int = 4099, extra: Sequence[int] = ()) -> list:
     """A deterministic index sample for full-size parity: every `stride`-th param,
     the first 8 and last 8 params, and any extra indices (e.g. shard boundaries)."""
