@@ -129,8 +129,9 @@ typedef struct {
   const int64_t* ps_bounds;/* optional PS shard boundaries (world > 1): world+1 values,
                               0 = b[0] < b[1] < ... < b[world] = nparams, inner ones
                               multiples of 32; shard q = [b[q], b[q+1]) on GPU q.
-                              NULL = even split (reading Z12; HP_XPORT_NCCL: ceil
-                              split, equal blocks but the last). Read during
+                              NULL = even split (reading Z12; HP_XPORT_NCCL with
+                              vw_span 1: ceil split, equal blocks but the last, for
+                              the equal-count collectives). Read during
                               hp_init_ex / hp_arena_bytes only (copied). Uneven
                               bounds express e.g. the paper's layer round-robin
                               placement on a permuted parameter order */

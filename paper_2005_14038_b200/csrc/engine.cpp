@@ -146,7 +146,7 @@ hp_status Engine::check_cuda(int err, const char* what) {
 void Engine::plan_layout() {
   if (dist_) {
     if (cfg_.ps_bounds) shard_b_.assign(cfg_.ps_bounds, cfg_.ps_bounds + G_ + 1);
-    else if (cfg_.transport == HP_XPORT_NCCL) shard_b_ = ceil_bounds(cfg_.nparams, G_);
+    else if (cfg_.transport == HP_XPORT_NCCL && span_ == 1) shard_b_ = ceil_bounds(cfg_.nparams, G_);
     else shard_b_ = even_bounds(cfg_.nparams, G_);
     stage_b_ = even_bounds(cfg_.nparams, span_);
   } else {

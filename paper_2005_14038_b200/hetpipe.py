@@ -285,7 +285,8 @@ class Context:
         if which < 0:
             from workloads import ceil_shards
             b = (getattr(c, "_ps_list", None)
-                 or (ceil_shards if c.transport == XPORT_NCCL else even_shards)(c.nparams, c.world))
+                 or (ceil_shards if c.transport == XPORT_NCCL and c.vw_span == 1
+                     else even_shards)(c.nparams, c.world))
             return b[c.rank + 1] - b[c.rank]
         for j in range(c.vw_span):
             if (which * c.vw_span + j) % c.world == c.rank:

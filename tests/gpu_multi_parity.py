@@ -158,7 +158,7 @@ def main():
         if cfg is None:
             continue
         bounds = (M.layer_rr_bounds(M.vgg19(), G) if len(case) > 6 else
-                  ceil_shards(cfg.nparams, G) if xport == "nccl" else None)
+                  ceil_shards(cfg.nparams, G) if xport == "nccl" and k == 1 else None)
         sampled = (sample_indices(cfg.nparams, 104729, bounds or even_shards(cfg.nparams, G))
                    if mode else None)
         objs = run(cfg, G, k, rank, local, sampled, xport, bounds)
