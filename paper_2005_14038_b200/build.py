@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhetpipe.so")
-SOURCES = ["kernels.cu", "engine.cpp", "capi.cpp", "comm_nccl.cpp", "pipeline.cpp"]
+SOURCES = ["kernels.cu", "engine.cpp", "engine_dist.cpp", "capi.cpp", "comm_nccl.cpp", "pipeline.cpp"]
 HEADERS = ["tick_desc.h", "engine.h", "comm.h", os.path.join("..", "..", "include", "hetpipe.h")]
 
 NVCC_FLAGS = [

@@ -128,6 +128,16 @@ class Engine {
   hp_status flush();
   hp_status flush_local();
   hp_status flush_dist();
+  // one target of an owner-side pull: the first pulled VW (its w_local) of a
+  // (GPU, stage range); the other pulled VWs of that range copy it
+  struct Prim {
+    int q;
+    int64_t a, len;
+    int v;
+  };
+  hp_status dist_accumulate(const std::vector<bool>& pulled);
+  hp_status dist_apply(std::vector<Prim>* prims, bool* fuse_pull);
+  hp_status dist_pull(const std::vector<Prim>& prims, bool fuse_pull);
   int lockstep_slot() const;                 // acc slot of a lockstep batch, or -1
   hp_status flush_lockstep(int slot);        // its NCCL / NVLS exchange
   hp_status finish_connect(const void* comm_id);

@@ -8,7 +8,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 CSRC = os.path.join(ROOT, "paper_2005_14038_b200", "csrc")
 LIB = os.path.join(HERE, "libhetpipe_emu.so")
-SRCS = [os.path.join(CSRC, "engine.cpp"), os.path.join(CSRC, "capi.cpp"),
+SRCS = [os.path.join(CSRC, "engine.cpp"), os.path.join(CSRC, "engine_dist.cpp"),
+        os.path.join(CSRC, "capi.cpp"),
         os.path.join(HERE, "emu_kernels.cpp"), os.path.join(HERE, "comm_emu.cpp"),
         os.path.join(CSRC, "pipeline.cpp")]
 DEPS = SRCS + [os.path.join(CSRC, "engine.h"), os.path.join(CSRC, "tick_desc.h"),
