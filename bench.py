@@ -367,7 +367,7 @@ def main():
     # pull ops are fused with accumulation, so they have no launch of their own)
     sync_ms = float(sum(float(t) * float(sy) / float(by)
                         for t, by, sy in zip(l_ms, l_bytes, l_sync) if by > 0))
-    s_ms, s_vw = ctx.profile_sync_latency()
+    s_ms, s_vw, s_waited = ctx.profile_sync_latency()
     l_link = ctx.profile_link()
     xl = [(float(t), float(b)) for t, b in zip(l_ms, l_link) if b > 0]
     xch = None
@@ -380,6 +380,7 @@ def main():
                       "collectives): algorithmic NVLink bytes per direction / their device "
                       "time, rank 0; peak = guide-measured peer copy per direction"}
     sync_us = [1e3 * float(x) for x in s_ms]
+    sync_unblocked = [1e3 * float(x) for x, w in zip(s_ms, s_waited) if not w]
     mix = {}
     for t_ms, by, sh in zip(l_ms, l_bytes, l_shape):
         sh = int(sh) & 0xFFFFFFFF
@@ -503,9 +504,13 @@ def main():
         "wave_sync_latency_us": (
             {"p50": float(np.percentile(sync_us, 50)), "p99": float(np.percentile(sync_us, 99)),
              "max": float(np.max(sync_us)), "n": len(sync_us),
+             "unblocked": ({"p50": float(np.percentile(sync_unblocked, 50)),
+                            "p99": float(np.percentile(sync_unblocked, 99)),
+                            "n": len(sync_unblocked)} if sync_unblocked else None),
              "def": "per (VW, wave), rank 0: device time from the start of the launch carrying "
                     "the VW's wave-end COMPLETE (u~ final = push) to the end of the launch that "
-                    "wrote its pulled w_local (hp_profile_sync_latency); includes gate waits"}
+                    "wrote its pulled w_local (hp_profile_sync_latency); all records include gate "
+                    "waits, `unblocked` only those whose VW did not wait"}
             if sync_us else None),
         "kernel_share_of_step": busy_ms / ms if ms > 0 else None,
         "launch_mix": launch_mix,

@@ -302,8 +302,11 @@ hp_status hp_profile_link(hp_ctx* ctx, int64_t max, double* link_bytes, int64_t*
    of the launch that carried the VW's wave-end COMPLETE (its u~ final: the
    push) to the end of the launch (or NCCL collective) that wrote its pulled
    w_local (a LAZY admission without a pull ends no record; a VW that waited at
-   its gate includes the wait). ms[i], vw[i]; *n = records written. */
-hp_status hp_profile_sync_latency(hp_ctx* ctx, int64_t max, float* ms, int32_t* vw, int64_t* n);
+   its gate includes the wait and is flagged waited[i] = 1; SURVEY.md 8(d)
+   reports the unblocked case). ms[i], vw[i], waited[i] (any may be NULL);
+   *n = records written. */
+hp_status hp_profile_sync_latency(hp_ctx* ctx, int64_t max, float* ms, int32_t* vw,
+                                  int32_t* waited, int64_t* n);
 
 /* ---- Intra-VW pipeline schedule (section 4; no context).
    The upstream generator of the controller's per-VW timing (tau_v, L_v of

@@ -448,9 +448,10 @@ hp_status hp_profile_link(hp_ctx* ctx, int64_t max, double* link_bytes, int64_t*
   HP_EXIT(ctx)
 }
 
-hp_status hp_profile_sync_latency(hp_ctx* ctx, int64_t max, float* ms, int32_t* vw, int64_t* n) {
+hp_status hp_profile_sync_latency(hp_ctx* ctx, int64_t max, float* ms, int32_t* vw,
+                                  int32_t* waited, int64_t* n) {
   HP_ENTRY(ctx)
-  return ctx->eng->profile_sync(max, ms, vw, n);
+  return ctx->eng->profile_sync(max, ms, vw, waited, n);
   HP_EXIT(ctx)
 }
 

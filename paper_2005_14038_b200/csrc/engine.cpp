@@ -392,6 +392,7 @@ hp_status Engine::admit(int v, std::vector<int64_t>* started) {
     return HP_WOULD_BLOCK;
   }
   phase_ = kPhPull;
+  s.waited_last = s.blocked;
   if (s.blocked) {
     s.wait += tick_ - s.t_block;
     s.blocked = false;
@@ -564,12 +565,13 @@ void Engine::note_pulls(const std::vector<int>& vws) {
   const int64_t idx = prof_launches_ - 1;
   for (int v : vws)
     if (push_launch_[v] >= 0) {
-      sync_recs_.push_back({v, push_launch_[v], idx});
+      sync_recs_.push_back({v, push_launch_[v], idx, vw_[v].waited_last ? 1 : 0});
       push_launch_[v] = -1;
     }
 }
 
-hp_status Engine::profile_sync(int64_t max, float* ms, int32_t* vw, int64_t* n) {
+hp_status Engine::profile_sync(int64_t max, float* ms, int32_t* vw, int32_t* waited,
+                               int64_t* n) {
   if (sticky_) return sticky_;
   if (hp_status st = join_exchange()) return st;
   if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "profile sync")) return st;
@@ -580,6 +582,7 @@ hp_status Engine::profile_sync(int64_t max, float* ms, int32_t* vw, int64_t* n) 
     if (int e = cudaEventElapsedTime(&t, ev_[2 * r.from], ev_[2 * r.to + 1])) return check_cuda(e, "elapsed");
     if (ms) ms[i] = t;
     if (vw) vw[i] = r.v;
+    if (waited) waited[i] = r.waited;
   }
   if (n) *n = cnt;
   return HP_OK;

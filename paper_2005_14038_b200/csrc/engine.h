@@ -43,6 +43,7 @@ struct VW {
   int64_t held_g = 0, held_K = 0;
   bool at_gate = false, blocked = false;
   int64_t t_block = 0, wait = 0, pulls = 0;
+  bool waited_last = false;      // its latest admission followed a BLOCK
   int64_t acc_count = 0;         // completions in the open wave
   std::vector<int64_t> backlog;  // completions while waiting at the gate (Z17)
   // Ops on w_local not yet on the device, in order: p > 0 = FOLD u_p; p < 0 =
@@ -103,7 +104,7 @@ class Engine {
   void stats(hp_stats* out) const;
   hp_status profile_enable(bool on);
   hp_status profile_read(double* ms, double* bytes, int64_t* launches);
-  hp_status profile_sync(int64_t max, float* ms, int32_t* vw, int64_t* n);
+  hp_status profile_sync(int64_t max, float* ms, int32_t* vw, int32_t* waited, int64_t* n);
   hp_status profile_launches(int64_t max, float* ms, double* bytes, int32_t* shape,
                              double* sync_bytes, float* start_ms, int64_t* n);
   hp_status profile_link(int64_t max, double* link_bytes, int64_t* n);
@@ -234,6 +235,7 @@ class Engine {
   struct SyncRec {
     int32_t v;
     int64_t from, to;
+    int32_t waited;      // the VW waited at its gate before this pull
   };
   std::vector<SyncRec> sync_recs_;
   void note_sync(const TickDesc& d);

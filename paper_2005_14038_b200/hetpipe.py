@@ -105,7 +105,7 @@ EXPORTS = {
                                       C.POINTER(C.c_int64)]),
     "hp_profile_link": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_int64)]),
     "hp_profile_sync_latency": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
-                                          C.POINTER(C.c_int64)]),
+                                          C.c_void_p, C.POINTER(C.c_int64)]),
     "hp_partition": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
                                C.c_int32, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_void_p]),
@@ -354,10 +354,12 @@ Context.profile_launches = _profile_launches
 def _profile_sync_latency(self, max_records: int = 1 << 16):
     ms = np.zeros(max_records, dtype=np.float32)
     vw = np.zeros(max_records, dtype=np.int32)
+    waited = np.zeros(max_records, dtype=np.int32)
     n = C.c_int64()
     self._chk(self.lib.hp_profile_sync_latency(self.h, max_records, ms.ctypes.data_as(C.c_void_p),
-                                               vw.ctypes.data_as(C.c_void_p), C.byref(n)))
-    return ms[:n.value], vw[:n.value]
+                                               vw.ctypes.data_as(C.c_void_p),
+                                               waited.ctypes.data_as(C.c_void_p), C.byref(n)))
+    return ms[:n.value], vw[:n.value], waited[:n.value]
 
 
 Context.profile_sync_latency = _profile_sync_latency

@@ -98,12 +98,16 @@ def test_sync_latency_records(hp, cfg):
     ctx = hetpipe.Context(hetpipe.config_from(cfg), lib=hp.lib)
     ctx.profile_enable(True)
     ctx.run_schedule(cfg.tau, cfg.latency())
-    ms, vw = ctx.profile_sync_latency()
+    ms, vw, waited = ctx.profile_sync_latency()
     st = ctx.stats()
     assert len(ms) == sum(st.pulls[:cfg.num_vw])
     for v in range(cfg.num_vw):
         assert int((vw == v).sum()) == st.pulls[v]
     assert np.all(ms >= 0)
+    # waited flags: C1's equal speeds never block; the skewed C1 blocks its fast VW
+    assert int(waited.sum()) == (0 if cfg is C1 else int(waited.sum()))
+    if cfg is C1_SKEW:
+        assert waited.any() and not waited[vw == 1].any()
     ctx.close()
 
 
