@@ -376,6 +376,7 @@ def main():
         xch = {"launches": len(xl), "ms": xt, "link_bytes": xb,
                "achieved_GBps": xb / (xt / 1e3) / 1e9, "peak_GBps": 770.0,
                "frac": xb / (xt / 1e3) / 1e9 / 770.0, "bound": "nvlink",
+               "frac_vs_nominal_900": xb / (xt / 1e3) / 1e9 / 900.0,
                "def": "exchange launches only (peer loads/stores, NVLS multimem, NCCL "
                       "collectives): algorithmic NVLink bytes per direction / their device "
                       "time, rank 0; peak = guide-measured peer copy per direction"}
@@ -494,6 +495,7 @@ def main():
                       if sync_ms_max > 0 else None),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _ncu_traffic(cfg.name),
+                     "frac_vs_nominal_8000": achieved / 8000.0,
                      "peak_kind": peak_kind, "kernel": "hp::tick_kernel (all launches)",
                      "kernel_ms": kern_ms, "busy_ms": busy_ms, "launches": kern_launches,
                      "alg_bytes_per_launch": kern_bytes / max(kern_launches, 1)},
