@@ -188,6 +188,7 @@ const char* validate(hp_config& cfg) {
   else if (cfg.apply_mode < 0 || cfg.apply_mode > 1) bad = "bad apply_mode";
   else if (cfg.merge_ticks < 0 || cfg.merge_ticks > 1) bad = "bad merge_ticks";
   else if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world) bad = "bad world/rank";
+  else if (cfg.world > 8) bad = "world must be <= 8 (one NVLink domain of B200s)";
   else if (cfg.world > 1 && (cfg.vw_span < 1 || cfg.vw_span > cfg.world)) bad = "vw_span must be 1..world";
   else if (cfg.world > 1 && (cfg.param_begin != 0 || cfg.param_count != cfg.nparams))
     bad = "world > 1 places the whole model: param_begin 0, param_count -1";

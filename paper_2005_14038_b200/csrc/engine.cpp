@@ -110,12 +110,17 @@ RankLayout Engine::layout_of(int q) const {
       }
     }
   }
+  if (G_ > 1) {                       // K7 flags: one uint64 per source rank
+    L.flag_off = off;
+    off += align256(2 * G_);
+  }
   L.bytes = off;
   return L;
 }
 
 Engine::~Engine() {
   delete comm_;
+  if (flag_err_) cudaFree(flag_err_);
   for (auto e : evpool_) cudaEventDestroy(e);
   if (xs_) cudaStreamDestroy(xs_);
   for (auto v : vs_)
@@ -209,6 +214,8 @@ hp_status Engine::init() {
       st = check_cuda(launch_init(v.wl, v.len, v.a0, cfg_.w0_mode, cfg_.grad_mode, k0, k1, stream_),
                       "init");
   if (st == HP_OK && m_) st = check_cuda(cudaMemsetAsync(m_, 0, (size_t)n_ * 4, stream_), "memset");
+  if (st == HP_OK && G_ > 1)            // K7 flags start at epoch 0 (before hp_connect's barrier)
+    st = check_cuda(cudaMemsetAsync(base + L.flag_off, 0, (size_t)G_ * 8, stream_), "flags");
   for (auto& v : vw_)                 // CONVEX: minibatches 1..Nm read w0
     for (float* sl : v.stash)
       if (st == HP_OK)
@@ -590,9 +597,29 @@ hp_status Engine::profile_sync(int64_t max, float* ms, int32_t* vw, int32_t* wai
 
 // The stream-ordered barrier of the exchange stream, profiled like a launch
 // (shape nf = 126) so its cost shows in the launch mix.
+// The stream-ordered barrier of the exchange stream:
+// every rank stores the barrier's epoch into its slot of every peer's flag
+// array (NVLink stores, release) and waits until its own array holds the
+// epoch from every rank (acquire) -- one tiny kernel, no NCCL call. A wait
+// that exceeds its deadline sets a device error flag, reported as
+// HP_ERR_COMM at the next synchronising call. HP_FLAG_BARRIER=0 uses a
+// 4-byte NCCL all-reduce instead. Profiled like a launch (shape nf = 126).
 hp_status Engine::xbarrier() {
   prof_begin(xs_);
-  if (comm_->barrier(xs_) != 0) return fail(HP_ERR_COMM, comm_->error());
+  if (flag_barrier_) {
+    ++epoch_;
+    FlagBarrier fb;
+    memset(&fb, 0, sizeof fb);
+    fb.G = G_;
+    fb.me = rank_;
+    fb.epoch = epoch_;
+    fb.err = flag_err_;
+    for (int q = 0; q < G_; ++q)
+      fb.flags[q] = (unsigned long long*)(peer_[q] + lay_[q].flag_off);
+    if (int e = launch_flag_barrier(fb, xs_)) return check_cuda(e, "flag barrier");
+  } else if (comm_->barrier(xs_) != 0) {
+    return fail(HP_ERR_COMM, comm_->error());
+  }
   prof_end(xs_, 0.0, 0.0, 126 << 24);
   return HP_OK;
 }
@@ -831,7 +858,18 @@ hp_status Engine::sync() {
   ungated_.clear();
   if (hp_status st = flush_applies()) return st;
   if (hp_status st = join_exchange()) return st;
-  return check_cuda(cudaStreamSynchronize(stream_), "sync");
+  if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "sync")) return st;
+  if (flag_err_) {                     // a K7 flag wait ran past its deadline
+    int bad = 0;
+    if (hp_status st = check_cuda(cudaMemcpy(&bad, flag_err_, sizeof bad, cudaMemcpyDeviceToHost),
+                                  "flag error"))
+      return st;
+    if (bad) {
+      sticky_ = HP_ERR_COMM;
+      return fail(HP_ERR_COMM, "K7 readiness flag wait timed out (a rank stopped issuing barriers)");
+    }
+  }
+  return HP_OK;
 }
 
 hp_status Engine::read(int which, int64_t off, int64_t cnt, float* dst) {

@@ -29,6 +29,7 @@ namespace hp {
 struct RankLayout {
   int64_t s0 = 0, s1 = 0;             // PS shard [s0, s1) (global params)
   size_t wg_off = 0, m_off = 0, x_off = 0, bytes = 0;   // x: NCCL staging (shard)
+  size_t flag_off = 0;                // K7 readiness flags: uint64 per source rank
   std::vector<int64_t> a, len;        // per VW: local stage [a, a+len)
   std::vector<char> has;              // per VW: a stage lives on this rank
   std::vector<size_t> wl_off;
@@ -193,6 +194,9 @@ class Engine {
   bool forked_ = false;               // side streams ordered after the context stream
   int xblocks_ = 0;                   // grid bound of exchange launches (HP_XBLOCKS)
   int ablocks_ = 0;                   // grid bound of accumulation launches (HP_ABLOCKS)
+  bool flag_barrier_ = true;          // K7 device flags (HP_FLAG_BARRIER=0: NCCL barrier)
+  uint64_t epoch_ = 0;                // barriers issued (identical on every rank)
+  int* flag_err_ = nullptr;           // device: set if a flag wait timed out
   std::vector<cudaEvent_t> evpool_;
   size_t evnext_ = 0;
   double nvl_bytes_ = 0;

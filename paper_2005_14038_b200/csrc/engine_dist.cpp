@@ -624,6 +624,11 @@ hp_status Engine::finish_connect(const void* comm_id) {
   std::string err;
   comm_ = comm_create(comm_id, G_, rank_, &err);
   if (!comm_) return fail(HP_ERR_COMM, err);
+  if (const char* fb = getenv("HP_FLAG_BARRIER")) flag_barrier_ = atoi(fb) != 0;
+  if (flag_barrier_) {
+    if (int e = cudaMalloc((void**)&flag_err_, sizeof(int))) return check_cuda(e, "flag error");
+    if (int e = cudaMemset(flag_err_, 0, sizeof(int))) return check_cuda(e, "flag error");
+  }
   // Stream priorities (HP_PRIO, default on): the exchange and the folds that
   // wait for it are the round's critical path; the accumulation of the next
   // wave has slack (the acc ring), so its CTAs yield to them.

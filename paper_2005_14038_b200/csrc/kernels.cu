@@ -358,6 +358,33 @@ __global__ void __launch_bounds__(256) nvls_kernel(const __grid_constant__ NvlsD
   __threadfence_system();
 }
 
+// K7 barrier: lane q stores the epoch into rank q's flag slot of this rank
+// (release, system scope: the writes of the kernels before it on this GPU are
+// visible to any peer that sees the flag), then waits (acquire) until this
+// rank's array holds the epoch from rank q. 10 s deadline (%globaltimer).
+__global__ void flag_barrier_kernel(const __grid_constant__ FlagBarrier fb) {
+  const int q = threadIdx.x;
+  if (q < fb.G) {
+    __threadfence_system();
+    unsigned long long* dst = fb.flags[q] + fb.me;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(fb.epoch) : "memory");
+    const unsigned long long* src = fb.flags[fb.me] + q;
+    unsigned long long t0, t, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(src) : "memory");
+      if (v >= fb.epoch) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) {
+        if (fb.err) atomicExch(fb.err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
 // w0 (Z8): zero or Philox stream 1, counter (i>>2, 0, 0, 1).
 __global__ void init_kernel(float* out, int64_t n, int64_t param_begin, int w0_mode,
                             int grad_mode, uint32_t k0, uint32_t k1) {
@@ -470,6 +497,11 @@ int launch_nvls(const NvlsDesc& d, void* stream, int max_blocks) {
   if (u >= 8) return launch_nvls_u<8>(d, s, max_blocks);
   if (u <= 2) return launch_nvls_u<2>(d, s, max_blocks);
   return launch_nvls_u<4>(d, s, max_blocks);
+}
+
+int launch_flag_barrier(const FlagBarrier& fb, void* stream) {
+  flag_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(fb);
+  return (int)cudaGetLastError();
 }
 
 int launch_init(float* out, int64_t n, int64_t param_begin, int w0_mode, int grad_mode,

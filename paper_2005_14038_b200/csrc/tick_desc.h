@@ -163,6 +163,16 @@ struct NvlsDesc {
 };
 int launch_nvls(const NvlsDesc& d, void* stream, int max_blocks = 0);
 
+// K7 readiness barrier among G ranks (engine.cpp xbarrier): flags[q] is rank
+// q's flag array (one uint64 per source rank), mapped into this process.
+struct FlagBarrier {
+  unsigned long long* flags[8];
+  int* err;                    // device int set to 1 if a wait timed out
+  unsigned long long epoch;
+  int32_t G, me;
+};
+int launch_flag_barrier(const FlagBarrier& fb, void* stream);
+
 // Launch the fused tick kernel (kernels.cu). grad_mode: HP_GRAD_*.
 // Returns a cudaError_t as int.
 // max_blocks > 0 bounds the grid (exchange launches that share the GPU with

@@ -113,6 +113,15 @@ int launch_nvls(const NvlsDesc& d, void*, int) {
   return 0;
 }
 
+// K7 flag barrier on host threads (ranks are threads of one process here)
+int launch_flag_barrier(const FlagBarrier& fb, void*) {
+  for (int q = 0; q < fb.G; ++q) __atomic_store_n(fb.flags[q] + fb.me, fb.epoch, __ATOMIC_RELEASE);
+  for (int q = 0; q < fb.G; ++q)
+    while (__atomic_load_n(fb.flags[fb.me] + q, __ATOMIC_ACQUIRE) < fb.epoch) {
+    }
+  return 0;
+}
+
 int launch_init(float* out, int64_t n, int64_t begin, int w0_mode, int gm, uint32_t k0,
                 uint32_t k1, void*) {
   for (int64_t i = 0; i < n; ++i) {
