@@ -155,9 +155,12 @@ void hp_config_default(hp_config* cfg);
    hp_connect(handles = world*64 bytes in rank order, comm_id). After that the
    ranks must issue the same protocol calls in the same order (the replicated
    controller does); pushes are applied by each PS shard owner reading the
-   pushed u~ slices from the GPU that holds them, and pulls read w_global
-   shards from their owners -- NVLink loads inside the tick kernels, ordered by
-   a stream-ordered barrier (a 4-byte NCCL all-reduce). */
+   pushed u~ slices from the GPU that holds them and storing the new w_global
+   into the pullers' w_local (or pulls read w_global shards from their owners)
+   -- NVLink loads and stores inside the tick kernels, ordered by a
+   stream-ordered barrier: device readiness flags in every arena (release /
+   acquire over NVLink; HP_FLAG_BARRIER=0: a 4-byte NCCL
+   all-reduce). */
 hp_status hp_comm_unique_id(void* out128);
 hp_status hp_ipc_handle(hp_ctx* ctx, void* out64);
 hp_status hp_connect(hp_ctx* ctx, const void* handles, const void* comm_id);
@@ -280,7 +283,7 @@ hp_status hp_profile_read(hp_ctx* ctx, double* kernel_ms, double* alg_bytes,
    (completes, inline folds, memory applies, w_local groups, group folds, and
    whether a pull is in the fused launch; nf = 127 marks an NCCL collective of
    HP_XPORT_NCCL: na = 1 the reduce-scatter, ng = 1 the all-gather; nf = 126
-   the 4-byte NCCL barrier of a distributed exchange), and
+   the barrier of a distributed exchange), and
    sync_bytes = the part of
    alg_bytes that is synchronisation (w_global/m traffic, u~ reads of the
    applies, pull writes of w_local; the rest is wave accumulation and folds).

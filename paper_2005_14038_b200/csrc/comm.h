@@ -1,7 +1,8 @@
 // comm.h -- inter-GPU plumbing of libhetpipe for the distributed placements:
-// a stream-ordered barrier among the ranks (NCCL all-reduce of one int, loaded
-// with dlopen so the library uses the NCCL the process already has) and CUDA
-// IPC for mapping every peer's arena (one process per GPU).
+// the NCCL communicator (dlopen'd, so the library uses the NCCL the process
+// already has): the set-up barrier, the fallback exchange barrier (an
+// all-reduce of one int; the default is the device flag barrier of
+// engine.cpp xbarrier, K7) and the NCCL transport's collectives.
 //
 // Under HP_XPORT_PEER / NVLS the data never goes through NCCL: the tick
 // kernels read remote acc slices (push) and remote w_global shards (pull)
