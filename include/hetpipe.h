@@ -91,7 +91,7 @@ enum { HP_XPORT_PEER = 0, HP_XPORT_NCCL = 1, HP_XPORT_NVLS = 2 };
 
 typedef struct {
   int32_t num_vw;          /* N virtual workers, 1..8 */
-  int32_t Nm;              /* minibatches per wave, s_local = Nm-1, 1..64 */
+  int32_t Nm;              /* minibatches per wave, s_local = Nm-1, 1..32 */
   int32_t D;               /* clock-distance threshold, >= 0 */
   int32_t waves;           /* W: minibatches > W*Nm never start (Z16); default 2^30 */
   int64_t nparams;         /* P, global model size */
@@ -108,7 +108,7 @@ typedef struct {
   int32_t acc_slots;       /* acc ring depth R per VW, 2..8 (default 2) */
   int32_t merge_ticks;     /* 1 (default): ops of consecutive ticks on disjoint VW
                               state may share one launch; 0: one launch per tick */
-  int32_t world;           /* G ranks (one process per GPU); 1 = single context */
+  int32_t world;           /* G ranks (one process per GPU), 1..8; 1 = single context */
   int32_t rank;            /* this rank, 0..G-1 */
   int32_t vw_span;         /* k GPUs per VW (1..G): VW v's stage j (even split of P
                               over k) lives on GPU (v*k+j) mod G; PS shard q (even
