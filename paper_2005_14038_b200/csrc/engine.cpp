@@ -123,6 +123,7 @@ Engine::~Engine() {
   if (flag_err_) cudaFree(flag_err_);
   for (auto e : evpool_) cudaEventDestroy(e);
   if (xs_) cudaStreamDestroy(xs_);
+  if (xs2_) cudaStreamDestroy(xs2_);
   for (auto v : vs_)
     if (v) cudaStreamDestroy(v);
   for (auto v : fs_)
@@ -489,8 +490,11 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   if (!st) st = stream_;
   d.n = n;
   d.blk_base = begin >> 2;
-  d.wg = wg_;
-  d.m = m_;
+  // an apply launch over a sub-range of this rank's shard addresses w_global
+  // (and m) from the sub-range's start
+  const int64_t woff = (d.na > 0 && begin > begin_ && begin < begin_ + n_) ? begin - begin_ : 0;
+  d.wg = wg_ + woff;
+  d.m = m_ ? m_ + woff : nullptr;
   d.neg_lr = -cfg_.lr;
   d.mu = cfg_.momentum;
   d.conv_a = cfg_.conv_a;

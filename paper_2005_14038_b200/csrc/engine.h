@@ -179,6 +179,8 @@ class Engine {
   // stream; a compute-stream launch waits only for the exchange events of the
   // VWs whose buffers it touches.
   cudaStream_t xs_ = nullptr;
+  cudaStream_t xs2_ = nullptr;        // second exchange stream (NVLS / peer split)
+  int nvls_split_ = 100;              // % of a shard through NVLS (HP_NVLS_SPLIT)
   // Per local VW: accumulation (acc ring) runs on vs_, folds into w_local on
   // fs_ (split_folds_), so the next wave's accumulation does not wait for the
   // pull that rewrites w_local (row a9); exchange ops wait for exactly the

@@ -436,9 +436,35 @@ hp_status Engine::flush_lockstep(int slot) {
   const double P = (double)cfg_.nparams, n = (double)n_;
   if (cfg_.transport == HP_XPORT_NVLS) {
     if (hp_status st = xbarrier()) return st;
+    // HP_NVLS_SPLIT < 100: the tail of the shard goes through the peer path
+    // (NVLink loads of the u~ slices + owner-side stores into every w_local)
+    // on a second exchange stream, concurrently with the multicast kernel
+    const int64_t n1 = nvls_split_ >= 100 ? n_ : (n_ * nvls_split_ / 100) / 32 * 32;
+    cudaEvent_t peer_done = nullptr;
+    if (n1 < n_) {
+      cudaEvent_t e0 = pool_event();
+      cudaEventRecord(e0, xs_);
+      cudaStreamWaitEvent(xs2_, e0, 0);
+      TickDesc t;
+      memset(&t, 0, sizeof t);
+      for (const BApply& a : ba_) {
+        const int b = t.ns;
+        add_segs(t, begin_ + n1, n_ - n1, true, a.v, a.slot);
+        t.a[t.na].seg_begin = b;
+        t.a[t.na].seg_end = t.ns;
+        t.na++;
+      }
+      if (pull)
+        for (int q = 0; q < G_; ++q)
+          t.pd[t.np++] = {(float*)(peer_[q] + lay_[q].wl_off[q]) + begin_ + n1, 0, n_ - n1};
+      const double tl = 4.0 * (double)(n_ - n1) * (G_ - 1) * (pull ? 2.0 : 1.0);
+      if (hp_status st = emit(t, begin_ + n1, n_ - n1, xs2_, xblocks_, tl)) return st;
+      peer_done = pool_event();
+      cudaEventRecord(peer_done, xs2_);
+    }
     NvlsDesc d;
     memset(&d, 0, sizeof d);
-    d.n = n_;
+    d.n = n1;
     d.wg = wg_;
     d.mc_acc = (const float*)(mc_ + L.acc_off[me][slot]) + begin_;
     d.mc_wl = pull ? (float*)(mc_ + L.wl_off[me]) + begin_ : nullptr;
@@ -447,18 +473,20 @@ hp_status Engine::flush_lockstep(int slot) {
       d.src[q] = (const float*)(peer_[q] + lay_[q].acc_off[q][slot]) + begin_;
       d.dst[q] = (float*)(peer_[q] + lay_[q].wl_off[q]) + begin_;
     }
-    const double bytes = 4.0 * n * (2 + G_ + (pull ? G_ : 0));
+    const double fr = n_ > 0 ? (double)n1 / (double)n_ : 0.0;   // multicast share
+    const double bytes = 4.0 * (double)n1 * (2 + G_ + (pull ? G_ : 0));
     prof_begin(xs_);
     const int err = launch_nvls(d, xs_, xblocks_);
     // per GPU and direction: its acc replica served to every owner's reduction
     // (4P through the switch) + the multicast store (4n out / 4P in)
     prof_end(xs_, bytes, bytes, (N_ << 8) | (pull ? (int)(1u << 31) : 0),
-             4.0 * P + (pull ? 4.0 * n : 0.0));
+             (4.0 * P + (pull ? 4.0 * n : 0.0)) * fr);
     if (pull) note_pulls(bpull_);
-    launches_++;
+    if (n1 > 0) launches_++;
     alg_bytes_ += bytes;
-    nvl_bytes_ += 4.0 * n + (pull ? 4.0 * (P - n) : 0.0);
+    nvl_bytes_ += (4.0 * n + (pull ? 4.0 * (P - n) : 0.0)) * fr;
     if (hp_status st = check_cuda(err, "nvls kernel")) return st;
+    if (peer_done) cudaStreamWaitEvent(xs_, peer_done, 0);
     if (hp_status st = xbarrier()) return st;
   } else {
     float* x = (float*)((char*)arena_ + L.x_off);
@@ -638,6 +666,9 @@ hp_status Engine::finish_connect(const void* comm_id) {
     if (atoi(pr) == 0) prio_lo = prio_hi = 0;
   if (int e = cudaStreamCreateWithPriority(&xs_, cudaStreamNonBlocking, prio_hi))
     return check_cuda(e, "stream");
+  if (int e = cudaStreamCreateWithPriority(&xs2_, cudaStreamNonBlocking, prio_hi))
+    return check_cuda(e, "stream");
+  if (const char* ns = getenv("HP_NVLS_SPLIT")) nvls_split_ = std::max(0, std::min(100, atoi(ns)));
   xacc_.assign(N_, std::vector<cudaEvent_t>(R_, nullptr));
   xwl_.assign(N_, nullptr);
   lastc_.assign(N_, nullptr);
