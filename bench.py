@@ -315,6 +315,8 @@ def main():
         ctx = hdist.rank_context(run_cfg, rank, ws, device=local, stream=stream.cuda_stream,
                                  merge_ticks=args.merge_ticks, apply_mode=args.apply_mode)
     ctx.trace_enable(False)
+    from paper_2005_14038_b200 import hetpipe as _hp
+    arena = _hp.arena_bytes(ctx.cfg)       # device bytes this rank's context holds
     ctx.schedule_begin(run_cfg.tau, run_cfg.latency())
     sampler = ClockSampler(local)
     ctx.schedule_advance(N * args.warmup)
@@ -485,7 +487,8 @@ def main():
                    "transport": args.transport if placed else None,
                    "ps_shards": args.ps if placed else None,
                    "lockstep_batches": lock_batches if placed else None,
-                   "l2": "inputs larger than L2 (>= 13 x 230 MiB buffers per GPU)"},
+                   "l2": "inputs larger than L2 (>= 13 x 230 MiB buffers per GPU)",
+                   "arena_GiB_per_rank": arena / 2 ** 30},
         "images_per_sec_equiv": commits * 32 * cfg.Nm * cfg.F / (ms_max / 1e3),
         "sync_only": ({"value": commits * cfg.nparams / (sync_ms_max / 1e3), "unit": UNIT,
                        "ms_per_step": sync_ms_max / args.steps,
