@@ -327,3 +327,22 @@ def test_gradient_modes():
     assert set(np.unique(gd).tolist()) <= set(range(-8, 8))
     w0 = initial_weights(idx, C2)
     assert w0.min() >= -1 and w0.max() < 1
+
+
+def test_spec_timeline_examples():
+    """SPEC.md's timeline examples, in the tick model (Nm = 1, so a
+    wave is one minibatch and L = tau): homogeneous speeds never wait; wave
+    durations {1, 2} at D = 0 make the fast VW wait one unit per clock --
+    it pushes at t = c*100 + 100 and is admitted when the slow VW's push of the
+    same clock arrives, 100 ticks later, for every clock but the last (no gated
+    START remains, Z16) -- and D = 4 waits strictly less."""
+    for tau in ((100, 100), (50, 50, 50)):
+        r = run_schedule(WSPConfig("h", len(tau), 1, 0, 8, 8, tau, lr=2.0 ** -6,
+                                   grad_mode=GRAD_DYADIC))
+        assert r.wait == [0] * len(tau)
+    W = 8
+    base = WSPConfig("t", 2, 1, 0, 8, W, (100, 200), lr=2.0 ** -6, grad_mode=GRAD_DYADIC)
+    r0 = run_schedule(base)
+    assert r0.wait == [(W - 1) * 100, 0]
+    r4 = run_schedule(base.replace(D=4))
+    assert r4.wait[0] < r0.wait[0] and r4.wait[1] == 0
