@@ -17,14 +17,21 @@ DEPS = SRCS + [os.path.join(CSRC, "engine.h"), os.path.join(CSRC, "tick_desc.h")
                os.path.join(HERE, "cuda_runtime.h"), os.path.join(ROOT, "include", "hetpipe.h")]
 
 
-def build():
-    if os.path.exists(LIB) and all(os.path.getmtime(d) <= os.path.getmtime(LIB) for d in DEPS):
-        return LIB
-    cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-pthread",
-           "-I", HERE, "-o", LIB + ".tmp", *SRCS]
+ASAN_LIB = os.path.join(HERE, "libhetpipe_emu_asan.so")
+
+
+def build(asan: bool = False):
+    """The emulation library; asan=True: the same sources under AddressSanitizer
+    (tests/test_asan_emu.py loads it into a subprocess with libasan preloaded)."""
+    lib = ASAN_LIB if asan else LIB
+    if os.path.exists(lib) and all(os.path.getmtime(d) <= os.path.getmtime(lib) for d in DEPS):
+        return lib
+    flags = (["-O1", "-g", "-fsanitize=address", "-fno-omit-frame-pointer"] if asan else ["-O2"])
+    cmd = ["g++", "-std=c++17", *flags, "-fPIC", "-shared", "-ffp-contract=off", "-pthread",
+           "-I", HERE, "-o", lib + ".tmp", *SRCS]
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
