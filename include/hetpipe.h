@@ -64,7 +64,7 @@ typedef enum {
    g = a (w_p - b) + sigma xi, the gradient of a/2 ||w - b||^2 plus noise at the
    weights w_p = w_local minibatch p read at its START (kept in a ring of N_m
    per-VW stash slots: the "forward pass" of minibatch p); b = Philox stream 2,
-   xi = the FLOAT draw; every op one fp32 rounding. world = 1 contexts only. */
+   xi = the FLOAT draw; every op one fp32 rounding. */
 enum { HP_GRAD_FLOAT = 0, HP_GRAD_DYADIC = 1, HP_GRAD_EXTERNAL = 2, HP_GRAD_CONVEX = 3 };
 enum { HP_W0_ZERO = 0, HP_W0_PHILOX = 1 };
 enum { HP_PULL_EAGER = 0, HP_PULL_LAZY = 1 };
@@ -122,7 +122,7 @@ typedef struct {
                               frequency factor): one clock = F waves; a VW
                               aggregates and pushes F*Nm minibatches per clock, its gated
                               STARTs are (c+2)*F*Nm, s_global = F(D+2)Nm - 2; `waves`
-                              counts clocks. F > 1 needs world = 1. Default 1 */
+                              counts clocks. Default 1 */
   int32_t reserved2;
   float conv_a;            /* HP_GRAD_CONVEX curvature a (default 0.5) */
   float conv_sigma;        /* HP_GRAD_CONVEX noise scale sigma (default 1.0) */

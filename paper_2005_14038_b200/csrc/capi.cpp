@@ -181,7 +181,7 @@ const char* validate(hp_config& cfg) {
   else if (cfg.param_count < 0 || cfg.param_begin + cfg.param_count > cfg.nparams) bad = "bad shard";
   else if (cfg.acc_slots < 2 || cfg.acc_slots > 8) bad = "acc_slots must be 2..8";
   else if (cfg.grad_mode < 0 || cfg.grad_mode > 3) bad = "bad grad_mode";
-  else if (cfg.world > 1 && cfg.grad_mode == HP_GRAD_CONVEX) bad = "CONVEX gradients need world 1";
+
   else if (cfg.w0_mode < 0 || cfg.w0_mode > 1) bad = "bad w0_mode";
   else if (cfg.pull_policy < 0 || cfg.pull_policy > 1) bad = "bad pull_policy";
   else if (cfg.local_semantics < 0 || cfg.local_semantics > 1) bad = "bad local_semantics";
@@ -195,7 +195,7 @@ const char* validate(hp_config& cfg) {
   else if (cfg.world > 1 && cfg.grad_mode == HP_GRAD_EXTERNAL) bad = "EXTERNAL gradients need world 1";
   else if (cfg.transport < 0 || cfg.transport > 2) bad = "bad transport";
   else if (cfg.update_freq < 1 || cfg.update_freq > 64) bad = "update_freq must be 1..64";
-  else if (cfg.update_freq > 1 && cfg.world > 1) bad = "update_freq > 1 needs world 1";
+
   if (!bad && cfg.world > 1 && cfg.ps_bounds) {
     const int64_t* b = cfg.ps_bounds;
     if (b[0] != 0 || b[cfg.world] != cfg.nparams) bad = "ps_bounds must span [0, nparams]";

@@ -258,6 +258,15 @@ bool Engine::done() const {
   return true;
 }
 
+void Engine::fill_fold(DFold& f, int v, int64_t x) const {
+  const int64_t q = x > 0 ? x : -x;
+  f.v = (uint32_t)v;
+  f.p = (uint32_t)q;
+  f.op = x > 0 ? 0u : 1u;
+  f.grad = x > 0 ? fold_grad(v, q) : nullptr;
+  f.stash = convex_ ? vw_[v].stash[(q - 1) % Nm_] : nullptr;
+}
+
 const float* Engine::fold_grad(int v, int64_t p) const {
   if (cfg_.grad_mode != HP_GRAD_EXTERNAL) return nullptr;
   return vw_[v].grad_of_slot[(p - 1) % Nm_];
@@ -809,15 +818,7 @@ hp_status Engine::flush_local() {
       // stored in phase B if completed now
       g.partial = g.pull ? s.pull_partial : nullptr;
       g.f_begin = d.nf;
-      for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
-        DFold& f = d.f[d.nf++];
-        const int64_t q = folds[fi] > 0 ? folds[fi] : -folds[fi];
-        f.v = (uint32_t)v;
-        f.p = (uint32_t)q;
-        f.op = folds[fi] > 0 ? 0u : 1u;
-        f.grad = folds[fi] > 0 ? fold_grad(v, q) : nullptr;
-        f.stash = convex_ ? s.stash[(q - 1) % Nm_] : nullptr;
-      }
+      for (; fi < folds.size() && d.nf < kMaxF; ++fi) fill_fold(d.f[d.nf++], v, folds[fi]);
       g.f_end = d.nf;
     } while (fi < folds.size());
   }

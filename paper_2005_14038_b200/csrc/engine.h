@@ -158,6 +158,9 @@ class Engine {
   void rec(char phase, int v, const char* kind, int64_t p, int64_t c);
   std::pair<bool, bool> gate_open(int v) const;
   const float* fold_grad(int v, int64_t p) const;
+  // one w_local op of VW v from its pending list: x > 0 FOLD u_x, x < 0 STASH
+  // for START(-x) (CONVEX); sets the stash slot / EXTERNAL gradient it reads
+  void fill_fold(DFold& f, int v, int64_t x) const;
   bool has_due_folds() const {
     for (const auto& s : vw_)
       if (!s.pending_folds.empty() && !(cfg_.local_semantics == HP_LOCAL_STRICT && s.at_gate)) return true;

@@ -65,9 +65,11 @@ hp_status Engine::dist_accumulate(const std::vector<bool>& pulled) {
       c.acc = s.acc[b.slot];
       c.grad = nullptr;
       c.wl = nullptr;
+      c.stash = convex_ ? s.stash[(b.p - 1) % Nm_] : nullptr;
+      c.snap = b.snap ? s.snap : nullptr;
       c.v = (uint32_t)b.v;
       c.p = (uint32_t)b.p;
-      c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc;
+      c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc | (b.snap ? kSnapAcc : 0u);
     }
     const bool hold = strict && s.at_gate;
     std::vector<int64_t> folds;
@@ -78,7 +80,9 @@ hp_status Engine::dist_accumulate(const std::vector<bool>& pulled) {
       e = nullptr;
     };
     cudaStream_t fst = vs_[v];          // stream of the w_local folds
-    if (split_folds_) {
+    // (CONVEX: a complete reads the stash slot the folds' STASH ops write, so
+    // acc and folds stay in one launch)
+    if (split_folds_ && !convex_) {
       // acc part now (its slot is free once the exchange that read it is done)
       if (d.nc) {
         for (int j = 0; j < d.nc; ++j) wait_clear(vs_[v], xacc_[v][cslot[j]]);
@@ -95,8 +99,9 @@ hp_status Engine::dist_accumulate(const std::vector<bool>& pulled) {
       for (int j = 0; j < d.nc; ++j) wait_clear(vs_[v], xacc_[v][cslot[j]]);
       wait_clear(vs_[v], xwl_[v]);
       if (lastw_[v]) cudaStreamWaitEvent(vs_[v], lastw_[v], 0);
-      if (folds.size() == 1 && d.nc == 1 && (int64_t)d.c[0].p == folds[0]) {
-        d.c[0].flags |= kFoldInline;
+      const bool tail_stash = folds.size() == 2 && folds[1] == -(folds[0] + Nm_);
+      if ((folds.size() == 1 || tail_stash) && d.nc == 1 && (int64_t)d.c[0].p == folds[0]) {
+        d.c[0].flags |= kFoldInline | (tail_stash ? kStashAfter : 0u);
         d.c[0].wl = s.wl;
         folds.clear();
       }
@@ -112,10 +117,7 @@ hp_status Engine::dist_accumulate(const std::vector<bool>& pulled) {
       g.pull = 0;
       g.f_begin = d.nf;
       for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
-        DFold& f = d.f[d.nf++];
-        f.v = (uint32_t)v;
-        f.p = (uint32_t)folds[fi];
-        f.grad = nullptr;
+        fill_fold(d.f[d.nf++], v, folds[fi]);
       }
       g.f_end = d.nf;
     }
@@ -166,7 +168,8 @@ hp_status Engine::dist_apply(std::vector<Prim>* prims_out, bool* fuse_out) {
     float* base = (float*)(peer_[pr.q] + L.wl_off[pr.v]);
     ptargets.push_back({base + (begin_ - pr.a), x0 - begin_, x1 - begin_});   // i -> [begin_+i-a]
   }
-  const bool fuse_pull = *fuse_out = push_pull_ && strict && !ba_.empty() && !bpull_.empty() &&
+  const bool fuse_pull = *fuse_out = push_pull_ && strict && U_ == Nm_ && !ba_.empty() &&
+                                     !bpull_.empty() &&
                          ptargets.size() <= (size_t)kMaxP;
   // NVLink traffic of this rank's links while every owner runs its apply
   // launch at once (the barrier aligns them): the ũ slices it loads from peers
@@ -296,10 +299,7 @@ hp_status Engine::dist_pull(const std::vector<Prim>& prims, bool fuse_pull) {
           first_part = false;
           g.f_begin = d.nf;
           for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
-            DFold& f = d.f[d.nf++];
-            f.v = (uint32_t)v;
-            f.p = (uint32_t)folds[fi];
-            f.grad = nullptr;
+            fill_fold(d.f[d.nf++], v, folds[fi]);
           }
           g.f_end = d.nf;
         } while (fi < folds.size());
@@ -364,10 +364,7 @@ hp_status Engine::dist_pull(const std::vector<Prim>& prims, bool fuse_pull) {
         first_part = false;
         g.f_begin = d.nf;
         for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
-          DFold& f = d.f[d.nf++];
-          f.v = (uint32_t)v;
-          f.p = (uint32_t)folds[fi];
-          f.grad = nullptr;
+          fill_fold(d.f[d.nf++], v, folds[fi]);
         }
         g.f_end = d.nf;
       } while (fi < folds.size());
@@ -393,7 +390,10 @@ hp_status Engine::dist_pull(const std::vector<Prim>& prims, bool fuse_pull) {
 // (STRICT: the pull is the copy w_local = w_global). Returns the acc slot of
 // wave c, or -1 (the batch takes the PEER path).
 int Engine::lockstep_slot() const {
-  if (cfg_.transport == HP_XPORT_PEER || !dist_ || G_ != N_ || span_ != 1 || m_) return -1;
+  // (F > 1: a STRICT pull adds the open clock's aggregate, which the
+  // collective copy w_local = w_global does not)
+  if (cfg_.transport == HP_XPORT_PEER || !dist_ || G_ != N_ || span_ != 1 || m_ || U_ != Nm_)
+    return -1;
   if (cfg_.transport == HP_XPORT_NVLS && !mc_) return -1;
   if ((int)ba_.size() != N_) return -1;
   std::vector<char> seen(N_, 0);
@@ -541,10 +541,7 @@ hp_status Engine::flush_lockstep(int slot) {
         g.pull = 0;
         g.f_begin = d.nf;
         for (; fi < folds.size() && d.nf < kMaxF; ++fi) {
-          DFold& f = d.f[d.nf++];
-          f.v = (uint32_t)v;
-          f.p = (uint32_t)folds[fi];
-          f.grad = nullptr;
+          fill_fold(d.f[d.nf++], v, folds[fi]);
         }
         g.f_end = d.nf;
       }

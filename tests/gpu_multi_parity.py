@@ -147,10 +147,13 @@ def main():
         Nm = rng.randint(1, 4)
         tau = tuple(rng.randint(1, 9) for _ in range(N))
         k = rng.randint(1, G)
+        convex = rng.random() < 0.3
         cfg = WSPConfig("rnd", N, Nm, rng.randint(0, 3), rng.choice([4099, 20_000, 33_333]),
                         rng.randint(2, 6), tau, momentum=rng.choice([0.0, 0.9]),
                         pull_policy=rng.choice([0, 1]), local_semantics=rng.choice([0, 1]),
-                        lat=tuple(t * rng.randint(1, Nm + 1) for t in tau))
+                        lat=tuple(t * rng.randint(1, Nm + 1) for t in tau),
+                        grad_mode=3 if convex else 0, lr=0.05 if convex else 0.01,
+                        F=rng.choice([1, 1, 2]))
         cases.append((cfg, k, None, rng.choice(["peer", "peer", "nccl"]), None, None))
     ok = True
     for case in cases:

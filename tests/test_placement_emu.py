@@ -194,3 +194,28 @@ def test_exchange_link_bytes_lockstep_peer(lib):
         assert links[r][-1] == 3 * 4 * n
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_placement_convex_and_update_frequency(lib, seed):
+    """The weight-dependent CONVEX workload (NEXT-2) and F > 1 (NEXT-4) in the
+    distributed placements: stash rings per VW stage, STASH ops after pulls and
+    folds on every path (reader- and owner-side pulls), the F > 1 STRICT pull
+    with its partial aggregate (reader-side), bit-exact against the oracle."""
+    rng = random.Random(900 + seed)
+    G = rng.choice([2, 3, 4])
+    k = rng.randint(1, G)
+    N = rng.randint(1, 4)
+    Nm = rng.randint(1, 3)
+    tau = tuple(rng.randint(1, 9) for _ in range(N))
+    convex = seed % 2 == 0
+    F = rng.choice([1, 2, 3]) if seed % 3 else 1
+    cfg = WSPConfig("cf", N, Nm, rng.randint(0, 2), rng.choice([333, 1030, 4099]),
+                    rng.randint(2, 4), tau, lr=0.05 if convex else 0.01,
+                    momentum=rng.choice([0.0, 0.9]), grad_mode=3 if convex else GRAD_FLOAT,
+                    pull_policy=rng.choice([PULL_EAGER, PULL_LAZY]),
+                    local_semantics=rng.choice([LOCAL_STRICT, LOCAL_AT_LEAST]),
+                    lat=tuple(t * rng.randint(1, Nm + 1) for t in tau), F=F)
+    out = run_placement(lib, cfg, G, k, merge_ticks=rng.randint(0, 1),
+                        apply_mode=rng.randint(0, 1))
+    check(cfg, G, k, out)

@@ -185,3 +185,22 @@ def test_nvls_requires_symmetric_connect(lib):
         ctx.connect([ctx.ipc_handle()] * 2, cid)
     assert e.value.status == hetpipe.HP_ERR_STATE
     ctx.close()
+
+
+@pytest.mark.parametrize("transport", [NCCL, NVLS], ids=["nccl", "nvls"])
+def test_lockstep_convex(lib, transport):
+    # weight-dependent gradients through the collective exchange: the STASH of
+    # the gated START follows the collective pull (normwise: one-sum applies)
+    cfg = lockstep_cfg(3, 2, 0, 1030, 4, GRAD_FLOAT).replace(grad_mode=3, lr=0.05)
+    out = run_transport(lib, cfg, 3, transport)
+    check(cfg, 3, out, exact=False)
+    assert out[0][3].lockstep_batches == cfg.waves
+
+
+@pytest.mark.parametrize("transport", [NCCL, NVLS], ids=["nccl", "nvls"])
+def test_update_frequency_never_lockstep(lib, transport):
+    # F > 1: a STRICT pull adds the open clock's aggregate -> never a collective
+    cfg = lockstep_cfg(2, 2, 0, 1030, 3, GRAD_FLOAT).replace(F=2)
+    out = run_transport(lib, cfg, 2, transport)
+    check(cfg, 2, out, exact=True)
+    assert out[0][3].lockstep_batches == 0
