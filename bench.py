@@ -422,17 +422,29 @@ def main():
 
     # ---------------- e2e: host gradients in, w_global out, through the C-ABI
     e2e = None
-    if not args.no_e2e and not placed:
+    if not args.no_e2e and cfg.grad_mode != 3:
         e_steps = max(1, args.e2e_steps)
         ecfg = cfg.replace(waves=3 + e_steps + 1)
-        nloc = hi - lo
+        # host gradients: single-rank contexts take their shard, the distributed
+        # placements each VW's whole gradient (every rank copies its stages)
+        nloc = cfg.nparams if placed else hi - lo
         host = [torch.empty(nloc, dtype=torch.float32, pin_memory=True) for _ in range(4)]
         rng = np.random.default_rng(cfg.seed)
         for h in host:
             h.numpy()[:] = (rng.random(nloc, dtype=np.float32) - np.float32(0.5))
-        out = torch.empty(nloc, dtype=torch.float32, pin_memory=True)
-        ectx = hdist.rank_context(ecfg, rank, ws, device=local, stream=stream.cuda_stream,
-                                  grad_mode=GRAD_EXTERNAL)
+        ekeep = None
+        if placed and args.transport == "nvls":
+            ectx, ekeep = hdist.symmetric_context(ecfg, rank, ws, args.span, device=local,
+                                                  stream=stream.cuda_stream, transport=xport,
+                                                  grad_mode=GRAD_EXTERNAL, **extra)
+        elif placed:
+            ectx = hdist.placed_context(ecfg, rank, ws, args.span, device=local,
+                                        stream=stream.cuda_stream, transport=xport,
+                                        grad_mode=GRAD_EXTERNAL, **extra)
+        else:
+            ectx = hdist.rank_context(ecfg, rank, ws, device=local, stream=stream.cuda_stream,
+                                      grad_mode=GRAD_EXTERNAL)
+        out = torch.empty(max(1, ectx.local_len(-1)), dtype=torch.float32, pin_memory=True)
         ectx.trace_enable(False)
         ectx.schedule_set_host_grads([h.numpy() for h in host])
         ectx.schedule_begin(ecfg.tau, ecfg.latency())
@@ -454,12 +466,15 @@ def main():
         dt = float(tt.item())
         ecommits = s1.commits - s0.commits
         completes_per_step = N * cfg.Nm
+        # every minibatch's gradient crosses PCIe once in total (a rank copies its
+        # shard / its stages of it); w_global is read back once across the ranks
         e2e = {"value": ecommits * cfg.nparams / dt, "unit": UNIT,
-               "h2d_bytes_per_step": completes_per_step * nloc * 4 * ws,
-               "d2h_bytes_per_step": nloc * 4 * ws,
+               "h2d_bytes_per_step": completes_per_step * cfg.nparams * 4,
+               "d2h_bytes_per_step": cfg.nparams * 4,
                "steps": e_steps, "ms_per_step": 1e3 * dt / e_steps,
                "path": "hp_schedule_set_host_grads + hp_schedule_advance + hp_read_weights(-1)"}
         ectx.close()
+        del ekeep
 
     if rank != 0:
         if ws > 1:

@@ -186,14 +186,18 @@ hp_status hp_init_ex(hp_ctx** out, const hp_config* cfg);
 
 /* COMPLETE(vw, p). Requires p == completed(vw)+1 and p
    already started, else HP_ERR_PROTOCOL. grad: HP_GRAD_EXTERNAL only -- device
-   fp32[param_count] for this rank's shard, BORROWED until vw's next admission
+   fp32[param_count] for this rank's shard (distributed placements: this rank's
+   stage of vw, or any non-NULL pointer if vw has no stage here), BORROWED until
+   vw's next admission
    (a deferred STRICT fold may re-read it); must be NULL otherwise. If p ends a
    wave the caller must push that wave next (hp_push_wave). The START of
    p+N_m (when not gated) is implicit in this call. */
 hp_status hp_accumulate_minibatch(hp_ctx* ctx, int32_t vw, int64_t p, const float* grad);
 
 /* As above with a HOST gradient buffer (pinned for overlap): copied into a
-   library-owned device slot on the context stream before the kernel reads it. */
+   library-owned device slot on the context stream before the kernel reads it.
+   Single-rank contexts: fp32[param_count] (the shard); distributed placements:
+   fp32[nparams], the VW's whole gradient, of which this rank copies its stage. */
 hp_status hp_accumulate_minibatch_host(hp_ctx* ctx, int32_t vw, int64_t p,
                                        const float* host_grad);
 

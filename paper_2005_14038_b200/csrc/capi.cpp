@@ -192,7 +192,7 @@ const char* validate(hp_config& cfg) {
   else if (cfg.world > 1 && (cfg.vw_span < 1 || cfg.vw_span > cfg.world)) bad = "vw_span must be 1..world";
   else if (cfg.world > 1 && (cfg.param_begin != 0 || cfg.param_count != cfg.nparams))
     bad = "world > 1 places the whole model: param_begin 0, param_count -1";
-  else if (cfg.world > 1 && cfg.grad_mode == HP_GRAD_EXTERNAL) bad = "EXTERNAL gradients need world 1";
+
   else if (cfg.transport < 0 || cfg.transport > 2) bad = "bad transport";
   else if (cfg.update_freq < 1 || cfg.update_freq > 64) bad = "update_freq must be 1..64";
 

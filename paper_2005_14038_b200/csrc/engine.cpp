@@ -313,6 +313,10 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
     }
   }
   const float* g = grad_dev;
+  if (grad_host && dist_ && !s.here) {   // the VW has no stage on this rank
+    grad_host = nullptr;
+    g = nullptr;
+  }
   if (grad_host) {  // library-owned device copy of a host gradient
     if (s.grad_ring.empty()) {
       s.grad_ring.assign(Nm_, nullptr);
@@ -323,7 +327,10 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
       dst = nullptr;
       return fail(HP_ERR_OOM, "gradient staging allocation failed");
     }
-    if (hp_status st = check_cuda(cudaMemcpyAsync(dst, grad_host, (size_t)s.len * 4,
+    // a distributed placement's host gradient is the VW's whole model: copy
+    // this rank's stage of it (single-rank contexts: their shard, a0 = begin)
+    const float* src = dist_ ? grad_host + s.a0 : grad_host;
+    if (hp_status st = check_cuda(cudaMemcpyAsync(dst, src, (size_t)s.len * 4,
                                                   cudaMemcpyHostToDevice, stream_), "H2D grad"))
       return st;
     g = dst;

@@ -63,7 +63,7 @@ hp_status Engine::dist_accumulate(const std::vector<bool>& pulled) {
       cslot[d.nc] = b.slot;
       DComplete& c = d.c[d.nc++];
       c.acc = s.acc[b.slot];
-      c.grad = nullptr;
+      c.grad = b.grad;                  // EXTERNAL: this rank's stage of u's gradient
       c.wl = nullptr;
       c.stash = convex_ ? s.stash[(b.p - 1) % Nm_] : nullptr;
       c.snap = b.snap ? s.snap : nullptr;

@@ -25,10 +25,26 @@ from workloads import models as M  # noqa: E402
 XPORT = {"peer": 0, "nccl": 1, "nvls": 2}
 
 
-def run(cfg, G, k, rank, local, sampled, transport="peer", bounds=None):
+def host_gradients(cfg):
+    """EXTERNAL mode: the VWs' whole gradients as host buffers, filled with the
+    same Philox values the synthetic mode draws (oracle.gradient)."""
+    from oracle import gradient
+    idx = np.arange(cfg.nparams)
+    last_p = cfg.waves * cfg.Nm
+    n = cfg.num_vw * last_p + 1
+    bufs = [np.zeros(cfg.nparams, dtype=np.float32) for _ in range(n)]
+    for v in range(cfg.num_vw):
+        for p in range(1, last_p + 1):
+            bufs[(v * last_p + p) % n][:] = gradient(idx, v, p, cfg)
+    return bufs
+
+
+def run(cfg, G, k, rank, local, sampled, transport="peer", bounds=None, external=False):
     stream = torch.cuda.Stream(local)
     keep = None
     extra = {"ps_bounds": bounds} if bounds else {}
+    if external:
+        extra["grad_mode"] = 2
     if transport == "nvls":
         ctx, keep = hdist.symmetric_context(cfg, rank, G, k, device=local,
                                             stream=stream.cuda_stream, transport=XPORT["nvls"],
@@ -36,6 +52,9 @@ def run(cfg, G, k, rank, local, sampled, transport="peer", bounds=None):
     else:
         ctx = hdist.placed_context(cfg, rank, G, k, device=local, stream=stream.cuda_stream,
                                    transport=XPORT[transport], **extra)
+    if external:
+        bufs = host_gradients(cfg)
+        ctx.schedule_set_host_grads(bufs)
     ctx.run_schedule(cfg.tau, cfg.latency())
     with tempfile.NamedTemporaryFile(suffix=".trace") as f:
         tr = ctx.trace_lines(f.name)
@@ -128,6 +147,9 @@ def main():
         (c5e, 1, "sample", "nccl", False, True),
         (c5e, 1, "sample", "nvls", False, True),
         (c5e, 1, "sample", "peer", True, False),
+        # EXTERNAL host gradients (the VWs' whole gradients, each rank copies its stages)
+        (C3.replace(nparams=20_000, waves=4, D=1), 1, None, "peer", True, False, "external"),
+        (C3.replace(nparams=20_000, waves=4), max(1, G // 2), None, "peer", True, False, "external"),
         # the paper's default layer round-robin PS placement: uneven shards
         (c5e, 1, "sample", "nvls", False, True, "layer_rr"),
         (C5.replace(waves=2, D=4, num_vw=G, tau=C5.tau[:G]), 1, "sample", "peer", True, False,
@@ -160,11 +182,12 @@ def main():
         cfg, k, mode, xport, exact, want_lock = case[:6]
         if cfg is None:
             continue
-        bounds = (M.layer_rr_bounds(M.vgg19(), G) if len(case) > 6 else
+        external = len(case) > 6 and case[6] == "external"
+        bounds = (M.layer_rr_bounds(M.vgg19(), G) if len(case) > 6 and case[6] == "layer_rr" else
                   ceil_shards(cfg.nparams, G) if xport == "nccl" and k == 1 else None)
         sampled = (sample_indices(cfg.nparams, 104729, bounds or even_shards(cfg.nparams, G))
                    if mode else None)
-        objs = run(cfg, G, k, rank, local, sampled, xport, bounds)
+        objs = run(cfg, G, k, rank, local, sampled, xport, bounds, external)
         if rank == 0:
             try:
                 nlock = objs[0][5]

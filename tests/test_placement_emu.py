@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 from oracle import run_schedule
-from workloads import (C3, C5, GRAD_DYADIC, GRAD_FLOAT, LOCAL_AT_LEAST,
+from workloads import (C3, C5, GRAD_DYADIC, GRAD_EXTERNAL, GRAD_FLOAT, LOCAL_AT_LEAST,
                        LOCAL_STRICT, PULL_EAGER, PULL_LAZY, WSPConfig, even_shards)
 
 
@@ -25,7 +25,7 @@ def lib():
     return hetpipe.load_test_library(build_emu.build())
 
 
-def run_placement(lib, cfg, G, k, **over):
+def run_placement(lib, cfg, G, k, host_grads=None, **over):
     from paper_2005_14038_b200 import hetpipe
     cid = hetpipe.comm_unique_id(lib)
     ctxs = [hetpipe.Context(hetpipe.config_from(cfg, world=G, rank=r, vw_span=k, **over), lib=lib)
@@ -37,6 +37,8 @@ def run_placement(lib, cfg, G, k, **over):
         try:
             c = ctxs[r]
             c.connect(handles, cid)
+            if host_grads is not None:
+                c.schedule_set_host_grads(host_grads)
             c.run_schedule(cfg.tau, cfg.latency())
             with tempfile.NamedTemporaryFile(suffix=".trace") as f:
                 tr = c.trace_lines(f.name)
@@ -218,4 +220,22 @@ def test_placement_convex_and_update_frequency(lib, seed):
                     lat=tuple(t * rng.randint(1, Nm + 1) for t in tau), F=F)
     out = run_placement(lib, cfg, G, k, merge_ticks=rng.randint(0, 1),
                         apply_mode=rng.randint(0, 1))
+    check(cfg, G, k, out)
+
+
+@pytest.mark.parametrize("G,k", [(2, 1), (3, 2), (4, 1), (4, 4)])
+def test_placement_external_host_gradients(lib, G, k):
+    """EXTERNAL gradients in the distributed placements: every rank gets the
+    VWs' whole host gradients and copies the stages it holds; the same Philox
+    values as the synthetic mode give the oracle's arrays exactly."""
+    from oracle import gradient
+    cfg = C3.replace(nparams=2053, waves=3, D=1, tau=(3, 4, 6, 7))
+    idx = np.arange(cfg.nparams)
+    last_p = cfg.waves * cfg.Nm
+    n = cfg.num_vw * last_p + 1
+    bufs = [np.zeros(cfg.nparams, dtype=np.float32) for _ in range(n)]
+    for v in range(cfg.num_vw):
+        for p in range(1, last_p + 1):
+            bufs[(v * last_p + p) % n][:] = gradient(idx, v, p, cfg)
+    out = run_placement(lib, cfg, G, k, host_grads=bufs, grad_mode=GRAD_EXTERNAL)
     check(cfg, G, k, out)
