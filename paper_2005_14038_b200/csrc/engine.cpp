@@ -328,10 +328,30 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
       return fail(HP_ERR_OOM, "gradient staging allocation failed");
     }
     // a distributed placement's host gradient is the VW's whole model: copy
-    // this rank's stage of it (single-rank contexts: their shard, a0 = begin)
+    // this rank's stage of it (single-rank contexts: their shard, a0 = begin).
+    // Distributed: the copy runs on the VW's accumulation stream (the complete
+    // that reads it follows in stream order) after every exchange-stream and
+    // fold-stream op issued so far (a deferred fold may still read the slot)
     const float* src = dist_ ? grad_host + s.a0 : grad_host;
+    // the slot's previous minibatch (p - Nm) may still have its fold queued on
+    // the host (e.g. replayed at an admission in this batch): launch it first,
+    // it reads the gradient this copy replaces
+    bool reader_queued = false;
+    for (int64_t x : s.pending_folds) reader_queued |= x > 0 && (x - 1) % Nm_ == (p - 1) % Nm_;
+    if (reader_queued)
+      if (hp_status st = flush()) return st;
+    cudaStream_t cst = stream_;
+    if (dist_) {
+      fork_streams();
+      cst = vs_[v];
+      for (cudaStream_t o : {xs_, fs_[v]}) {
+        cudaEvent_t e = pool_event();
+        cudaEventRecord(e, o);
+        cudaStreamWaitEvent(cst, e, 0);
+      }
+    }
     if (hp_status st = check_cuda(cudaMemcpyAsync(dst, src, (size_t)s.len * 4,
-                                                  cudaMemcpyHostToDevice, stream_), "H2D grad"))
+                                                  cudaMemcpyHostToDevice, cst), "H2D grad"))
       return st;
     g = dst;
   }

@@ -146,3 +146,8 @@ def test_update_frequency_random(hp, seed):
                                              (3, 2, 1, (2, 11), 3), (2, 4, 0, (5, 6, 13), 3)])
 def test_update_frequency_blocked_strict(hp, F, Nm, D, tau, mode):
     G.test_update_frequency_blocked_strict(hp, F, Nm, D, tau, mode)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_external_gradients_random(hp, seed):
+    G.test_external_gradients_random(hp, seed)

@@ -392,3 +392,30 @@ def test_update_frequency_blocked_strict(hp, F, Nm, D, tau, mode):
     for merge in (0, 1):
         trace, wg, wl, _, _ = run_device(hp, cfg, merge_ticks=merge)
         assert_same(o, trace, wg, wl)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_external_gradients_random(hp, seed):
+    """EXTERNAL host gradients (the library's ring of Nm device slots per VW)
+    on random configs with gate waits: a deferred STRICT fold re-reads the
+    slot of its minibatch, which the copy for minibatch p + Nm replaces --
+    the queued fold must reach the device first."""
+    base = _rand_cfg(4000 + seed)
+    cfg = base.replace(grad_mode=GRAD_FLOAT, lr=0.01)
+    o = run_schedule(cfg)
+    idx = np.arange(cfg.nparams)
+    last_p = cfg.waves * cfg.Nm
+    n = cfg.num_vw * last_p + 1
+    bufs = [np.zeros(cfg.nparams, dtype=np.float32) for _ in range(n)]
+    for v in range(cfg.num_vw):
+        for p in range(1, last_p + 1):
+            bufs[(v * last_p + p) % n][:] = gradient(idx, v, p, cfg)
+    rng = random.Random(seed)
+    ctx = hp.Context(hp.config_from(cfg, grad_mode=GRAD_EXTERNAL,
+                                    merge_ticks=rng.randint(0, 1), apply_mode=rng.randint(0, 1)))
+    ctx.schedule_set_host_grads(bufs)
+    ctx.run_schedule(cfg.tau, cfg.latency())
+    assert np.array_equal(ctx.read_weights(-1), o.wg)
+    for v in range(cfg.num_vw):
+        assert np.array_equal(ctx.read_weights(v), o.wl[v]), f"w_local({v})"
+    ctx.close()
