@@ -4,6 +4,7 @@
 """
 from __future__ import annotations
 
+import fcntl
 import os
 import subprocess
 import sys
@@ -32,6 +33,13 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    # one builder at a time (parallel test workers share the tree)
+    with open(LIB + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        return _build_locked(force, verbose)
+
+
+def _build_locked(force: bool, verbose: bool) -> str:
     if not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")

@@ -574,6 +574,10 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
         const char* p = (const char*)(d.s[t].ptr + b);
         if (p < lo || p >= hi) remote += 4.0 * (double)(d.s[t].end - b);
       }
+  // L2 prefetch of later chunk rounds (HP_PREFETCH = distance in rounds, 0 off):
+  // only for launches whose loads are all local (a hint; never a peer address)
+  static const int pf_env = getenv("HP_PREFETCH") ? atoi(getenv("HP_PREFETCH")) : 0;
+  d.pf = remote == 0 ? pf_env : 0;
   prof_begin(st);
   int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, st, max_blocks);
   int inl = 0;

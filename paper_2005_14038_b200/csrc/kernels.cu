@@ -269,8 +269,49 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
   }
 }
 
+// L2 prefetch (TickDesc::pf) of this CTA's tile of a later round: every buffer
+// the round loads, one 4 KB contiguous bulk prefetch per (buffer, chunk x),
+// spread over the CTA's threads. It costs no registers, so the bytes in flight
+// per SM are no longer capped by the U loads each thread holds (launches with
+// one or two load streams are latency-bound otherwise). Multi-segment sources
+// are skipped (a hint only).
+__device__ __forceinline__ void bulk_prefetch(const float* p) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(4096u) : "memory");
+}
 template <int GM, bool MOM, int U>
-__global__ void __launch_bounds__(256) tick_kernel(const __grid_constant__ TickDesc d) {
+__device__ __forceinline__ void prefetch_round(const TickDesc& d, int64_t qb, int64_t S) {
+  int slot = 0;
+  const int me = threadIdx.x;
+  auto pf = [&](const float* base) {
+#pragma unroll
+    for (int x = 0; x < U; ++x, ++slot)
+      if ((slot & 255) == me) bulk_prefetch(base + 4 * (qb + x * S));
+  };
+  if (d.wg_load && d.wgs_end <= d.wgs_begin) pf(d.wg);
+  if (MOM && d.wg_store) pf(d.m);
+  for (int k = 0; k < d.na; ++k)
+    if (d.a[k].seg_end - d.a[k].seg_begin == 1) pf(d.s[d.a[k].seg_begin].ptr);
+  for (int j = 0; j < d.nc; ++j) {
+    const DComplete& c = d.c[j];
+    if (c.flags & kLoadAcc) pf(c.acc);
+    if (c.flags & kFoldInline) pf(c.wl);
+    if (GM == 2) pf(c.grad);
+    if (GM == 3) pf(c.stash);
+  }
+  for (int gi = 0; gi < d.ng; ++gi) {
+    const DGroup& g = d.g[gi];
+    if (g.pull == 0) pf(g.wl);
+    else if (g.pull == 2 && g.seg_end - g.seg_begin == 1) pf(d.s[g.seg_begin].ptr);
+    if (g.pull && g.partial) pf(g.partial);
+    for (int fi = g.f_begin; fi < g.f_end; ++fi) {
+      if (GM == 2) pf(d.f[fi].grad);
+      if (GM == 3 && d.f[fi].op != 1) pf(d.f[fi].stash);
+    }
+  }
+}
+
+template <int GM, bool MOM, int U>
+__global__ void __launch_bounds__(256, (U == 2 && GM != 3) ? 4 : 2) tick_kernel(const __grid_constant__ TickDesc d) {
   // Programmatic dependent launch: this grid may start while the previous tick
   // kernel drains; it touches no global memory before the previous grid has
   // completed and flushed its writes.
@@ -280,7 +321,13 @@ __global__ void __launch_bounds__(256) tick_kernel(const __grid_constant__ TickD
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t groups = nfull / (S * U);          // rounds where every thread has U chunks
   int64_t q = t0;
-  for (int64_t r = 0; r < groups; ++r, q += S * U) tick_chunks<GM, MOM, U, 4>(d, q, S);
+  const int64_t cta0 = (int64_t)blockIdx.x * blockDim.x;   // this CTA's first chunk, round 0
+  if (d.pf > 0)
+    for (int64_t r = 1; r < d.pf && r < groups; ++r) prefetch_round<GM, MOM, U>(d, cta0 + r * S * U, S);
+  for (int64_t r = 0; r < groups; ++r, q += S * U) {
+    if (d.pf > 0 && r + d.pf < groups) prefetch_round<GM, MOM, U>(d, cta0 + (r + d.pf) * S * U, S);
+    tick_chunks<GM, MOM, U, 4>(d, q, S);
+  }
   for (; q < nfull; q += S) tick_chunks<GM, MOM, 1, 4>(d, q, S);
   if (t0 == 0) {
     switch (d.n & 3) {

@@ -108,6 +108,8 @@ struct TickDesc {
   int32_t wgs_begin, wgs_end;   // if non-empty: w_global registers are loaded from
                                 // these segments (remote shards) instead of wg
   int32_t np;                   // store targets of the owner-side pull
+  int32_t pf;                   // L2 prefetch distance in chunk rounds (0 = off;
+                                // only when every load of the launch is local)
   DStore pd[kMaxP];
 };
 

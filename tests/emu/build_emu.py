@@ -1,6 +1,7 @@
 """Build tests/emu/libhetpipe_emu.so: the REAL engine.cpp + capi.cpp host code
 linked against a host emulation of the device kernels (TEST-ONLY; the product
 library libhetpipe.so is built by paper_2005_14038_b200/build.py with nvcc)."""
+import fcntl
 import os
 import subprocess
 
@@ -24,6 +25,13 @@ def build(asan: bool = False):
     """The emulation library; asan=True: the same sources under AddressSanitizer
     (tests/test_asan_emu.py loads it into a subprocess with libasan preloaded)."""
     lib = ASAN_LIB if asan else LIB
+    # one builder at a time (pytest-xdist workers share the tree)
+    with open(lib + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        return _build_locked(lib, asan)
+
+
+def _build_locked(lib, asan):
     if os.path.exists(lib) and all(os.path.getmtime(d) <= os.path.getmtime(lib) for d in DEPS):
         return lib
     flags = (["-O1", "-g", "-fsanitize=address", "-fno-omit-frame-pointer"] if asan else ["-O2"])
