@@ -574,10 +574,23 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
         const char* p = (const char*)(d.s[t].ptr + b);
         if (p < lo || p >= hi) remote += 4.0 * (double)(d.s[t].end - b);
       }
-  // L2 prefetch of later chunk rounds (HP_PREFETCH = distance in rounds, 0 off):
+  // L2 prefetch one chunk round ahead (HP_PREFETCH = distance in rounds, 0 off):
   // only for launches whose loads are all local (a hint; never a peer address)
-  static const int pf_env = getenv("HP_PREFETCH") ? atoi(getenv("HP_PREFETCH")) : 0;
-  d.pf = remote == 0 ? pf_env : 0;
+  // and that have at most HP_PREFETCH_MAXLOADS load streams per chunk. Measured
+  // on B200 (profiles/r01_prefetch_ab.txt): +3-7% on C2's 1-3 stream launches,
+  // -1 to -7% on 4-6 stream ones, whose own loads already fill the memory system.
+  static const int pf_env = getenv("HP_PREFETCH") ? atoi(getenv("HP_PREFETCH")) : 1;
+  static const int pf_max = getenv("HP_PREFETCH_MAXLOADS") ? atoi(getenv("HP_PREFETCH_MAXLOADS")) : 3;
+  int loads = d.wg_load + ((d.m && d.wg_store) ? 1 : 0) + d.na;
+  for (int j = 0; j < d.nc; ++j)
+    loads += ((d.c[j].flags & kLoadAcc) ? 1 : 0) + ((d.c[j].flags & kFoldInline) ? 1 : 0) +
+             (d.c[j].grad ? 1 : 0) + (d.c[j].stash ? 1 : 0);
+  for (int g = 0; g < d.ng; ++g) {
+    loads += (d.g[g].pull != 1 ? 1 : 0) + ((d.g[g].pull && d.g[g].partial) ? 1 : 0);
+    for (int k = d.g[g].f_begin; k < d.g[g].f_end; ++k)
+      loads += (d.f[k].grad ? 1 : 0) + ((d.f[k].stash && d.f[k].op != 1) ? 1 : 0);
+  }
+  d.pf = (remote == 0 && loads <= pf_max) ? pf_env : 0;
   prof_begin(st);
   int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, st, max_blocks);
   int inl = 0;

@@ -310,8 +310,8 @@ __device__ __forceinline__ void prefetch_round(const TickDesc& d, int64_t qb, in
   }
 }
 
-template <int GM, bool MOM, int U>
-__global__ void __launch_bounds__(256, (U == 2 && GM != 3) ? 4 : 2) tick_kernel(const __grid_constant__ TickDesc d) {
+template <int GM, bool MOM, int U, bool PF>
+__global__ void __launch_bounds__(256) tick_kernel(const __grid_constant__ TickDesc d) {
   // Programmatic dependent launch: this grid may start while the previous tick
   // kernel drains; it touches no global memory before the previous grid has
   // completed and flushed its writes.
@@ -322,11 +322,14 @@ __global__ void __launch_bounds__(256, (U == 2 && GM != 3) ? 4 : 2) tick_kernel(
   const int64_t groups = nfull / (S * U);          // rounds where every thread has U chunks
   int64_t q = t0;
   const int64_t cta0 = (int64_t)blockIdx.x * blockDim.x;   // this CTA's first chunk, round 0
-  if (d.pf > 0)
+  if (PF) {
     for (int64_t r = 1; r < d.pf && r < groups; ++r) prefetch_round<GM, MOM, U>(d, cta0 + r * S * U, S);
-  for (int64_t r = 0; r < groups; ++r, q += S * U) {
-    if (d.pf > 0 && r + d.pf < groups) prefetch_round<GM, MOM, U>(d, cta0 + (r + d.pf) * S * U, S);
-    tick_chunks<GM, MOM, U, 4>(d, q, S);
+    for (int64_t r = 0; r < groups; ++r, q += S * U) {
+      if (r + d.pf < groups) prefetch_round<GM, MOM, U>(d, cta0 + (r + d.pf) * S * U, S);
+      tick_chunks<GM, MOM, U, 4>(d, q, S);
+    }
+  } else {
+    for (int64_t r = 0; r < groups; ++r, q += S * U) tick_chunks<GM, MOM, U, 4>(d, q, S);
   }
   for (; q < nfull; q += S) tick_chunks<GM, MOM, 1, 4>(d, q, S);
   if (t0 == 0) {
@@ -454,14 +457,14 @@ int g_u_override = -1;   // HP_TICK_U: tuning override of chunks per thread
 int g_pdl = 1;           // HP_PDL=0 disables programmatic dependent launch
 int g_grid = 0;          // HP_GRID=1: one round of U chunks per thread (non-persistent)
 
-template <int GM, bool MOM, int U>
+template <int GM, bool MOM, int U, bool PF>
 int launch_u(const TickDesc& d, cudaStream_t s, int max_blocks) {
   static int grid_max = 0;
   if (grid_max == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tick_kernel<GM, MOM, U>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tick_kernel<GM, MOM, U, PF>, 256, 0);
     grid_max = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int64_t chunks = (d.n + 3) >> 2;
@@ -480,7 +483,7 @@ int launch_u(const TickDesc& d, cudaStream_t s, int max_blocks) {
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, tick_kernel<GM, MOM, U>, d);
+  return (int)cudaLaunchKernelEx(&cfg, tick_kernel<GM, MOM, U, PF>, d);
 }
 
 template <int GM, bool MOM>
@@ -490,8 +493,11 @@ int launch_gm(const TickDesc& d, cudaStream_t s, int mb) {
   // folds) with 2, which keeps 3 CTAs/SM resident.
   int u = d.ng > 0 ? 2 : 4;
   if (g_u_override > 0) u = g_u_override;
-  if (u >= 4) return launch_u<GM, MOM, 4>(d, s, mb);
-  return launch_u<GM, MOM, 2>(d, s, mb);
+  // the L2 prefetch (d.pf > 0) is a separate instance, so the plain kernels keep
+  // their code; the engine asks for it only on launches with few load streams
+  // (complete-only, hence U = 4)
+  if (u >= 4) return d.pf > 0 ? launch_u<GM, MOM, 4, true>(d, s, mb) : launch_u<GM, MOM, 4, false>(d, s, mb);
+  return launch_u<GM, MOM, 2, false>(d, s, mb);
 }
 
 }  // namespace
