@@ -121,6 +121,7 @@ RankLayout Engine::layout_of(int q) const {
 Engine::~Engine() {
   delete comm_;
   if (flag_err_) cudaFree(flag_err_);
+  if (tiles_) cudaFree(tiles_);
   for (auto e : evpool_) cudaEventDestroy(e);
   if (xs_) cudaStreamDestroy(xs_);
   if (xs2_) cudaStreamDestroy(xs2_);
@@ -215,6 +216,14 @@ hp_status Engine::init() {
       st = check_cuda(launch_init(v.wl, v.len, v.a0, cfg_.w0_mode, cfg_.grad_mode, k0, k1, stream_),
                       "init");
   if (st == HP_OK && m_) st = check_cuda(cudaMemsetAsync(m_, 0, (size_t)n_ * 4, stream_), "memset");
+  if (st == HP_OK) {
+    if (cudaMalloc((void**)&tiles_, kTileSlots * 128) != cudaSuccess) {
+      cudaGetLastError();
+      tiles_ = nullptr;
+      return fail(HP_ERR_OOM, "tile counter allocation failed");
+    }
+    st = check_cuda(cudaMemsetAsync(tiles_, 0, kTileSlots * 128, stream_), "tile counters");
+  }
   if (st == HP_OK && G_ > 1)            // K7 flags start at epoch 0 (before hp_connect's barrier)
     st = check_cuda(cudaMemsetAsync(base + L.flag_off, 0, (size_t)G_ * 8, stream_), "flags");
   for (auto& v : vw_)                 // CONVEX: minibatches 1..Nm read w0
@@ -591,6 +600,17 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
       loads += (d.f[k].grad ? 1 : 0) + ((d.f[k].stash && d.f[k].op != 1) ? 1 : 0);
   }
   d.pf = (remote == 0 && loads <= pf_max) ? pf_env : 0;
+  // dynamic tile scheduling (HP_DYN, default on) for launches with at least
+  // HP_DYN_MINLOADS load streams (HP_DYN_PULLS: also launches with pull groups):
+  // counters of this launch stream
+  static const int dyn_env = getenv("HP_DYN") ? atoi(getenv("HP_DYN")) : 1;
+  static const int dyn_min = getenv("HP_DYN_MINLOADS") ? atoi(getenv("HP_DYN_MINLOADS")) : 2;
+  static const int dyn_pulls = getenv("HP_DYN_PULLS") ? atoi(getenv("HP_DYN_PULLS")) : 1;
+  static const int64_t dyn_n = getenv("HP_DYN_MIN_N") ? atoll(getenv("HP_DYN_MIN_N")) : 0;
+  d.ctr = nullptr;
+  d.done = nullptr;
+  if (dyn_env && loads >= dyn_min && n >= dyn_n && (dyn_pulls || d.ng == 0))
+    tile_slot(st, &d.ctr, &d.done);
   prof_begin(st);
   int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, st, max_blocks);
   int inl = 0;
@@ -606,6 +626,18 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   alg_bytes_ += bytes;
   nvl_bytes_ += remote;
   return check_cuda(err, "tick kernel");
+}
+
+bool Engine::tile_slot(cudaStream_t st, unsigned long long** ctr, unsigned int** done) {
+  size_t i = 0;
+  while (i < tile_streams_.size() && tile_streams_[i] != st) ++i;
+  if (i == tile_streams_.size()) {
+    if (!tiles_ || i >= (size_t)kTileSlots) return false;   // static grid stride instead
+    tile_streams_.push_back(st);
+  }
+  *ctr = (unsigned long long*)(tiles_ + 128 * i);
+  *done = (unsigned int*)(tiles_ + 128 * i + 64);
+  return true;
 }
 
 // Wave-sync latency bookkeeping (profile window only): a launch with VW v's

@@ -202,6 +202,11 @@ class Engine {
   bool flag_barrier_ = true;          // K7 device flags (HP_FLAG_BARRIER=0: NCCL barrier)
   uint64_t epoch_ = 0;                // barriers issued (identical on every rank)
   int* flag_err_ = nullptr;           // device: set if a flag wait timed out
+  // dynamic tile scheduling of the tick kernel: one (counter, done) pair per
+  // launch stream, 128 bytes apart, zero between launches (TickDesc::ctr)
+  char* tiles_ = nullptr;
+  std::vector<cudaStream_t> tile_streams_;
+  bool tile_slot(cudaStream_t st, unsigned long long** ctr, unsigned int** done);
   std::vector<cudaEvent_t> evpool_;
   size_t evnext_ = 0;
   double nvl_bytes_ = 0;

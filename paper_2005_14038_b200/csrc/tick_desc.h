@@ -24,6 +24,7 @@ constexpr int kMaxG = 8;    // w_local groups per launch (one per VW)
 constexpr int kMaxF = 40;   // folds per launch
 constexpr int kMaxS = 32;   // source segments per launch
 constexpr int kMaxP = 16;   // pushed-pull store targets per launch
+constexpr int kTileSlots = 64;   // launch streams with dynamic tile counters per context
 
 enum : uint32_t {
   kFirst = 1u,       // first minibatch of its wave: a = u
@@ -110,6 +111,9 @@ struct TickDesc {
   int32_t np;                   // store targets of the owner-side pull
   int32_t pf;                   // L2 prefetch distance in chunk rounds (0 = off;
                                 // only when every load of the launch is local)
+  unsigned long long* ctr;      // dynamic tile scheduling (nullptr = static grid
+  unsigned int* done;           // stride): tile counter and finished-CTA count of
+                                // the launch stream, both 0 between launches
   DStore pd[kMaxP];
 };
 
