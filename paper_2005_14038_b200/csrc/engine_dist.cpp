@@ -473,6 +473,8 @@ hp_status Engine::flush_lockstep(int slot) {
       d.src[q] = (const float*)(peer_[q] + lay_[q].acc_off[q][slot]) + begin_;
       d.dst[q] = (float*)(peer_[q] + lay_[q].wl_off[q]) + begin_;
     }
+    static const int nvls_dyn = getenv("HP_NVLS_DYN") ? atoi(getenv("HP_NVLS_DYN")) : 1;
+    if (nvls_dyn) tile_slot(xs_, &d.ctr, &d.done);
     const double fr = n_ > 0 ? (double)n1 / (double)n_ : 0.0;   // multicast share
     const double bytes = 4.0 * (double)n1 * (2 + G_ + (pull ? G_ : 0));
     prof_begin(xs_);

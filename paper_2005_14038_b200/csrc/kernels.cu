@@ -420,32 +420,52 @@ __device__ __forceinline__ void mc_st1(float* mc, float v) {
   asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
 }
 
+// U chunks at q + x*stride: sum the shard's pushes in the switch, apply, and
+// multicast the new w_global into every w_local.
 template <int U>
+__device__ __forceinline__ void nvls_chunks(const NvlsDesc& d, int64_t q, int64_t stride) {
+  float4* wg4 = reinterpret_cast<float4*>(d.wg);
+  float4 s[U], w[U];
+#pragma unroll
+  for (int x = 0; x < U; ++x) {
+    s[x] = mc_ld_reduce4(d.mc_acc + 4 * (q + x * stride));
+    w[x] = __ldcs(wg4 + q + x * stride);
+  }
+#pragma unroll
+  for (int x = 0; x < U; ++x) {
+    w[x] = f4add(w[x], s[x]);
+    __stcs(wg4 + q + x * stride, w[x]);
+    if (d.mc_wl) mc_st4(d.mc_wl + 4 * (q + x * stride), w[x]);
+  }
+}
+
+template <int U, bool DYN>
 __global__ void __launch_bounds__(256) nvls_kernel(const __grid_constant__ NvlsDesc d) {
   const int64_t nfull = d.n >> 2;
   const int64_t S = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  float4* wg4 = reinterpret_cast<float4*>(d.wg);
   int64_t q = t0;
-  for (; q + (U - 1) * S < nfull; q += U * S) {
-    float4 s[U], w[U];
-#pragma unroll
-    for (int x = 0; x < U; ++x) {
-      s[x] = mc_ld_reduce4(d.mc_acc + 4 * (q + x * S));
-      w[x] = __ldcs(wg4 + q + x * S);
+  if (DYN) {
+    // dynamic tiles of 256U chunks claimed two ahead, as in tick_body
+    __shared__ long long nxt[3];
+    const int64_t T = nfull / (256 * U);
+    if (threadIdx.x == 0) {
+      nxt[0] = (long long)atomicAdd(d.ctr, 1ull);
+      nxt[1] = (long long)atomicAdd(d.ctr, 1ull);
     }
-#pragma unroll
-    for (int x = 0; x < U; ++x) {
-      w[x] = f4add(w[x], s[x]);
-      __stcs(wg4 + q + x * S, w[x]);
-      if (d.mc_wl) mc_st4(d.mc_wl + 4 * (q + x * S), w[x]);
+    __syncthreads();
+    for (int j = 0;; j = j == 2 ? 0 : j + 1) {
+      const int64_t k = nxt[j];
+      if (k >= T) break;
+      if (threadIdx.x == 0) nxt[j == 0 ? 2 : j - 1] = (long long)atomicAdd(d.ctr, 1ull);
+      nvls_chunks<U>(d, k * 256 * U + threadIdx.x, 256);
+      __syncthreads();
     }
+    q = T * 256 * U + t0;
+  } else {
+    for (; q + (U - 1) * S < nfull; q += U * S) nvls_chunks<U>(d, q, S);
   }
-  for (; q < nfull; q += S) {
-    float4 w = f4add(__ldcs(wg4 + q), mc_ld_reduce4(d.mc_acc + 4 * q));
-    __stcs(wg4 + q, w);
-    if (d.mc_wl) mc_st4(d.mc_wl + 4 * q, w);
-  }
+  for (; q < nfull; q += S) nvls_chunks<1>(d, q, 0);
   if (t0 == 0)
     for (int64_t i = nfull * 4; i < d.n; ++i) {
       const float w = __fadd_rn(d.wg[i], mc_ld_reduce1(d.mc_acc + i));
@@ -455,6 +475,10 @@ __global__ void __launch_bounds__(256) nvls_kernel(const __grid_constant__ NvlsD
   // the multicast stores must be visible system-wide before the barrier that
   // follows this kernel releases the other ranks to read their w_local
   __threadfence_system();
+  if (DYN && threadIdx.x == 0 && atomicAdd(d.done, 1u) == gridDim.x - 1) {
+    atomicExch(d.ctr, 0ull);
+    atomicExch(d.done, 0u);
+  }
 }
 
 // K7 barrier: lane q stores the epoch into rank q's flag slot of this rank
@@ -577,21 +601,21 @@ int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream, i
   }
 }
 
-template <int U>
+template <int U, bool DYN>
 int launch_nvls_u(const NvlsDesc& d, cudaStream_t s, int max_blocks) {
   static int grid_max = 0;
   if (grid_max == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nvls_kernel<U>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nvls_kernel<U, DYN>, 256, 0);
     grid_max = sms * (per_sm > 0 ? per_sm : 1);
   }
   int64_t blocks = ((d.n >> 2) + 255) / 256;
   if (blocks > grid_max) blocks = grid_max;
   if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  nvls_kernel<U><<<(unsigned)blocks, 256, 0, s>>>(d);
+  nvls_kernel<U, DYN><<<(unsigned)blocks, 256, 0, s>>>(d);
   return (int)cudaGetLastError();
 }
 
@@ -603,9 +627,10 @@ int launch_nvls(const NvlsDesc& d, void* stream, int max_blocks) {
     u = e ? atoi(e) : 4;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  if (u >= 8) return launch_nvls_u<8>(d, s, max_blocks);
-  if (u <= 2) return launch_nvls_u<2>(d, s, max_blocks);
-  return launch_nvls_u<4>(d, s, max_blocks);
+  const bool dyn = d.ctr != nullptr;
+  if (u >= 8) return dyn ? launch_nvls_u<8, true>(d, s, max_blocks) : launch_nvls_u<8, false>(d, s, max_blocks);
+  if (u <= 2) return dyn ? launch_nvls_u<2, true>(d, s, max_blocks) : launch_nvls_u<2, false>(d, s, max_blocks);
+  return dyn ? launch_nvls_u<4, true>(d, s, max_blocks) : launch_nvls_u<4, false>(d, s, max_blocks);
 }
 
 int launch_flag_barrier(const FlagBarrier& fb, void* stream) {

@@ -164,6 +164,8 @@ struct NvlsDesc {
   float* mc_wl;          // multicast address of w_local at the shard's first param, or nullptr
   int32_t G;
   int32_t pad;
+  unsigned long long* ctr;   // dynamic tiles (nullptr = static grid stride), as TickDesc
+  unsigned int* done;
   const float* src[8];   // per rank: acc slot at the shard's first param (unicast)
   float* dst[8];         // per rank: w_local at the shard's first param (unicast)
 };
