@@ -267,6 +267,38 @@ def test_full_size_sampled(hp, cfg):
         assert np.array_equal(m[idx], o.m)
 
 
+def test_beyond_int32_indices_sampled(hp):
+    """2^31 + 37 params (8.6 GB per fp32 buffer, ~60 GB of arena): every index,
+    chunk and tile computation is 64-bit. Sampled params around 2^31, 2^30, the
+    ends and every 2^24-th, read back one by one, against the oracle on the
+    same sample (FLOAT gradients, momentum: every path of the fused kernel)."""
+    torch = pytest.importorskip("torch")
+    free, _ = torch.cuda.mem_get_info()
+    if free < 80 * 2 ** 30:
+        pytest.skip("needs ~64 GB of free device memory")
+    P = 2 ** 31 + 37
+    cfg = C1.replace(name="big", nparams=P, Nm=2, D=1, waves=3, tau=(5, 7), lr=0.01,
+                     momentum=0.9, grad_mode=0)
+    idx = set(range(0, P, 2 ** 24))
+    for c in (0, 2 ** 30, 2 ** 31, P - 1):
+        idx.update(i for i in range(c - 9, c + 10) if 0 <= i < P)
+    idx = np.array(sorted(idx), dtype=np.int64)
+    o = run_schedule(cfg, idx=idx)
+    ctx = hp.Context(hp.config_from(cfg))
+    ctx.run_schedule(cfg.tau, cfg.latency())
+    with tempfile.NamedTemporaryFile(suffix=".trace") as f:
+        assert ctx.trace_lines(f.name) == o.trace
+    one = np.empty(1, dtype=np.float32)
+
+    def sampled(which):
+        return np.array([ctx.read_weights(which, int(i), 1, out=one)[0] for i in idx], np.float32)
+    assert np.array_equal(sampled(-1), o.wg)
+    assert np.array_equal(sampled(-2), o.m)
+    for v in range(cfg.num_vw):
+        assert np.array_equal(sampled(v), o.wl[v]), f"w_local({v})"
+    ctx.close()
+
+
 def test_c4_sharded_ranks_sampled(hp):
     """ED-local placement: two rank-shards of C4 run as separate
     contexts on one GPU reproduce the oracle at sampled params of each shard."""
