@@ -151,6 +151,46 @@ __device__ __forceinline__ void apply(float4& wg, float4& m, float4 ut, float mu
   }
 }
 
+// Phase B of one complete: its loads (acc, inline-fold w_local, EXTERNAL
+// gradient / CONVEX stash) ...
+template <int GM, int U, int CNT>
+__device__ __forceinline__ void complete_load(const DComplete& c, int64_t q0, int64_t qs,
+                                              float4* ain, float4* win, float4* gin) {
+  const uint32_t fl = c.flags;
+#pragma unroll
+  for (int x = 0; x < U; ++x) {
+    const int64_t q = q0 + x * qs;
+    if (fl & kLoadAcc) ain[x] = ld4<CNT>(c.acc, q);
+    if (fl & kFoldInline) win[x] = ld4<CNT>(c.wl, q);
+    if (GM == 2) gin[x] = ld4<CNT>(c.grad, q);
+    if (GM == 3) gin[x] = ld4<CNT>(c.stash, q);             // w_p
+  }
+}
+// ... and the rest: u, the wave aggregate, apply-now, inline fold.
+template <int GM, bool MOM, int U, int CNT>
+__device__ __forceinline__ void complete_finish(const TickDesc& d, const DComplete& c, int64_t q0,
+                                                int64_t qs, const float4* ain, const float4* win,
+                                                const float4* gin, float4* wg, float4* mm) {
+  const uint32_t fl = c.flags;
+#pragma unroll
+  for (int x = 0; x < U; ++x) {
+    const int64_t q = q0 + x * qs;
+    const uint64_t blk = (uint64_t)(d.blk_base + q);
+    const float4 u = (GM == 2) ? f4scale(d.neg_lr, gin[x])
+                     : (GM == 3) ? convex_u(d, c.v, c.p, blk, gin[x])
+                                 : synth_u<GM>(d, c.v, c.p, blk);
+    if (fl & kSnapAcc) st4<CNT>(c.snap, q, ain[x]);          // F > 1: acc at the gate
+    const float4 a = (fl & kFirst) ? u : f4add(ain[x], u);   // wave aggregate
+    if (fl & kStoreAcc) st4<CNT>(c.acc, q, a);
+    if (fl & kApplyNow) apply<MOM>(wg[x], mm[x], a, d.mu);
+    if (fl & kFoldInline) {
+      const float4 w = f4add(win[x], u);
+      st4<CNT>(c.wl, q, w);
+      if (GM == 3 && (fl & kStashAfter)) st4<CNT>(c.stash, q, w);   // START(p+Nm)
+    }
+  }
+}
+
 // U chunks (4 params each), chunk x at q0 + x*qs, through phases A-D of
 // tick_desc.h. Inside each op the loads of all U chunks are issued together,
 // so a thread keeps U (or 2U-3U) 16-byte requests in flight per op while its
@@ -175,7 +215,27 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
     for (int x = 0; x < U; ++x) mm[x] = ld4<CNT>(d.m, q0 + x * qs);
   }
   // ---- A. memory-sourced applies, commit order ------------------------------
-  for (int k = 0; k < d.na; ++k) {
+  int k0 = 0;
+  if (U <= 2) {
+    // two sources per step: twice the loads in flight per thread (the U = 2
+    // launches carry the pulls and most applies); per element the applies
+    // still run in commit order
+    for (; k0 + 1 < d.na; k0 += 2) {
+      float4 s0[U], s1[U];
+#pragma unroll
+      for (int x = 0; x < U; ++x) {
+        const int64_t q = q0 + x * qs;
+        s0[x] = ld4<CNT>(seg_ptr(d, d.a[k0].seg_begin, d.a[k0].seg_end, q), q);
+        s1[x] = ld4<CNT>(seg_ptr(d, d.a[k0 + 1].seg_begin, d.a[k0 + 1].seg_end, q), q);
+      }
+#pragma unroll
+      for (int x = 0; x < U; ++x) {
+        apply<MOM>(wg[x], mm[x], s0[x], d.mu);
+        apply<MOM>(wg[x], mm[x], s1[x], d.mu);
+      }
+    }
+  }
+  for (int k = k0; k < d.na; ++k) {
     float4 s[U];
 #pragma unroll
     for (int x = 0; x < U; ++x) s[x] = ld4<CNT>(seg_ptr(d, d.a[k].seg_begin, d.a[k].seg_end, q0 + x * qs), q0 + x * qs);
@@ -183,35 +243,12 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
     for (int x = 0; x < U; ++x) apply<MOM>(wg[x], mm[x], s[x], d.mu);
   }
   // ---- B. completes --------------------------------------------------------
+  // (pairing two completes' loads as in phase A needs ~45 more registers at
+  // U = 2: it spills under the 4-CTA cap, so the completes stay sequential)
   for (int j = 0; j < d.nc; ++j) {
-    const DComplete& c = d.c[j];
-    const uint32_t fl = c.flags;
     float4 ain[U], win[U], gin[U];
-#pragma unroll
-    for (int x = 0; x < U; ++x) {
-      const int64_t q = q0 + x * qs;
-      if (fl & kLoadAcc) ain[x] = ld4<CNT>(c.acc, q);
-      if (fl & kFoldInline) win[x] = ld4<CNT>(c.wl, q);
-      if (GM == 2) gin[x] = ld4<CNT>(c.grad, q);
-      if (GM == 3) gin[x] = ld4<CNT>(c.stash, q);             // w_p
-    }
-#pragma unroll
-    for (int x = 0; x < U; ++x) {
-      const int64_t q = q0 + x * qs;
-      const uint64_t blk = (uint64_t)(d.blk_base + q);
-      const float4 u = (GM == 2) ? f4scale(d.neg_lr, gin[x])
-                       : (GM == 3) ? convex_u(d, c.v, c.p, blk, gin[x])
-                                   : synth_u<GM>(d, c.v, c.p, blk);
-      if (fl & kSnapAcc) st4<CNT>(c.snap, q, ain[x]);          // F > 1: acc at the gate
-      const float4 a = (fl & kFirst) ? u : f4add(ain[x], u);   // wave aggregate
-      if (fl & kStoreAcc) st4<CNT>(c.acc, q, a);
-      if (fl & kApplyNow) apply<MOM>(wg[x], mm[x], a, d.mu);
-      if (fl & kFoldInline) {
-        const float4 w = f4add(win[x], u);
-        st4<CNT>(c.wl, q, w);
-        if (GM == 3 && (fl & kStashAfter)) st4<CNT>(c.stash, q, w);   // START(p+Nm)
-      }
-    }
+    complete_load<GM, U, CNT>(d.c[j], q0, qs, ain, win, gin);
+    complete_finish<GM, MOM, U, CNT>(d, d.c[j], q0, qs, ain, win, gin, wg, mm);
   }
   // ---- C. store w_global / m ------------------------------------------------
   if (d.wg_store) {
