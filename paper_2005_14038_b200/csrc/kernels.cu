@@ -220,6 +220,22 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
     // two sources per step: twice the loads in flight per thread (the U = 2
     // launches carry the pulls and most applies); per element the applies
     // still run in commit order
+    for (; k0 + 2 < d.na; k0 += 3) {
+      float4 s0[U], s1[U], s2[U];
+#pragma unroll
+      for (int x = 0; x < U; ++x) {
+        const int64_t q = q0 + x * qs;
+        s0[x] = ld4<CNT>(seg_ptr(d, d.a[k0].seg_begin, d.a[k0].seg_end, q), q);
+        s1[x] = ld4<CNT>(seg_ptr(d, d.a[k0 + 1].seg_begin, d.a[k0 + 1].seg_end, q), q);
+        s2[x] = ld4<CNT>(seg_ptr(d, d.a[k0 + 2].seg_begin, d.a[k0 + 2].seg_end, q), q);
+      }
+#pragma unroll
+      for (int x = 0; x < U; ++x) {
+        apply<MOM>(wg[x], mm[x], s0[x], d.mu);
+        apply<MOM>(wg[x], mm[x], s1[x], d.mu);
+        apply<MOM>(wg[x], mm[x], s2[x], d.mu);
+      }
+    }
     for (; k0 + 1 < d.na; k0 += 2) {
       float4 s0[U], s1[U];
 #pragma unroll
