@@ -21,7 +21,8 @@ decomposition and Lemma 1 (tests/test_oracle_convex.py); s_global with F
 (tests/test_oracle_update_freq.py); the pipeline partitioner / simulator
 oracle (oracle/pipeline.py, tests/test_pipeline_schedule.py). Parity
 unpinned: the exact bits of FLOAT-mode intermediate w_local snapshots with
-D>0 and heterogeneous speeds (their version sets are pinned).
+D>0 and heterogeneous speeds (their version sets are pinned exactly, their
+values to within Higham's summation bound).
 """
 from .philox import philox4x32_10, philox_words
 from .wsp import (OracleRun, WSPOracle, convex_target, gradient, initial_weights,

@@ -230,6 +230,70 @@ def test_random_configs_invariants(seed):
         assert np.array_equal(r.wl[v].astype(np.float64), expect)
 
 
+def _abs_sum_u(idx, cfg, pairs):
+    tot = np.zeros(idx.size, dtype=np.float64)
+    for v, p in pairs:
+        tot += np.abs(float(np.float32(cfg.lr)) * gradient(idx, v, p, cfg).astype(np.float64))
+    return tot
+
+
+def _version_pairs(cfg, v, a_v, commit_prefix):
+    pairs = [(v, q) for q in range(1, a_v + 1)]
+    for (vv, c) in commit_prefix:
+        if vv != v:
+            lo, hi = wave_range(c, cfg.Nm)
+            pairs += [(vv, q) for q in range(lo, hi + 1)]
+    return pairs
+
+
+def _within_summation_bound(got, w0, idx, cfg, pairs):
+    """|fl32 result - exact| <= gamma_n * (|w0| + sum|u|) + per-term rounding:
+    Higham, Accuracy and Stability, eq. 4.4 (any summation order, n terms,
+    gamma_n = n u / (1 - n u), u = 2^-24), plus u |term| for fl(-lr * g)."""
+    exact = w0 + _exact_sum_u(idx, cfg, pairs)
+    absum = np.abs(w0) + _abs_sum_u(idx, cfg, pairs)
+    n = len(pairs) + 1
+    u = 2.0 ** -24
+    bound = (n * u / (1 - n * u) + u) * absum
+    return bool(np.all(np.abs(got.astype(np.float64) - exact) <= bound))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_float_snapshots_within_summation_bound(seed):
+    """FLOAT mode, D > 0, heterogeneous speeds (the case whose exact bits only
+    the oracle fixes): every START snapshot, the final
+    w_global and every final w_local hold the values of their version
+    set (the same sets the DYADIC pins fix exactly) to within the recursive
+    summation bound of Higham eq. 4.4; a snapshot with one update dropped or
+    with one extra update does not."""
+    rng = random.Random(1000 + seed)
+    cfg = _rand_cfg(rng, grad_mode=GRAD_FLOAT, lr=0.01, D=rng.randint(1, 4),
+                    nparams=64)
+    idx = np.arange(cfg.nparams)
+    w0 = initial_weights(idx, cfg).astype(np.float64)
+    r = run_schedule(cfg, record_snapshots=True)
+    allp = [(v, p) for v in range(cfg.num_vw) for p in range(1, cfg.waves * cfg.Nm + 1)]
+    assert _within_summation_bound(r.wg, w0, idx, cfg, allp)
+    checked_neg = 0
+    for (t, v, p, snap), (v2, p2, a_v, held_K) in zip(r.snapshots, r.start_versions):
+        assert (v, p) == (v2, p2)
+        pairs = _version_pairs(cfg, v, a_v, r.commit[:held_K])
+        assert _within_summation_bound(snap, w0, idx, cfg, pairs), (v, p)
+        if pairs:                                   # a dropped update is caught
+            assert not _within_summation_bound(snap, w0, idx, cfg, pairs[1:])
+            checked_neg += 1
+        missing = [q for q in allp if q not in pairs]
+        if missing:                                 # so is an extra one
+            assert not _within_summation_bound(snap, w0, idx, cfg, pairs + missing[:1])
+    for v in range(cfg.num_vw):
+        last_pull = [ln.split() for ln in r.trace
+                     if ln.split()[2] == str(v) and ln.split()[3] == "PULL"]
+        held_K = int(last_pull[-1][10]) if last_pull else 0
+        pairs = _version_pairs(cfg, v, cfg.waves * cfg.Nm, r.commit[:held_K])
+        assert _within_summation_bound(r.wl[v], w0, idx, cfg, pairs)
+    assert checked_neg > 0 or cfg.waves * cfg.Nm <= cfg.Nm
+
+
 def test_d0_lockstep():
     """P6: with D=0 every admission sees all local clocks equal."""
     for tau in (TAU_NP, (100, 173, 260), (5, 7)):
