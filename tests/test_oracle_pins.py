@@ -368,6 +368,75 @@ def test_momentum_heavy_ball_closed_form():
     assert np.all(np.abs(r.wg.astype(np.float64) - w) <= 4 * K * 2.0 ** -24 * mag + 1e-12)
 
 
+def _heavy_ball_snapshot(idx, cfg, v, a_v, prefix, w0, mu):
+    """w0 + sum_j u~_(j) (1 - mu^(K-j+1)) / (1 - mu) over the commit prefix
+    (K = its length; Z11 heavy ball applied in commit order) + the
+    VW's own updates not in a pushed wave of the prefix, up to a_v (P:838-839,
+    "w_local = w_global + not-yet-pushed local updates"); fp64 from the fp32
+    terms u_p. Returns (value, magnitude for the rounding bound)."""
+    K = len(prefix)
+    w = w0.copy()
+    mag = np.abs(w0).copy()
+    own_pushed = set()
+    for j, (vv, c) in enumerate(prefix, start=1):
+        lo, hi = wave_range(c, cfg.Nm)
+        ut = np.zeros_like(w0)
+        for q in range(lo, hi + 1):
+            ut += update(idx, vv, q, cfg).astype(np.float64)
+        w += ut * (1 - mu ** (K - j + 1)) / (1 - mu)
+        mag += np.abs(ut) / (1 - mu)
+        if vv == v:
+            own_pushed.update(range(lo, hi + 1))
+    for q in range(1, a_v + 1):
+        if q not in own_pushed:
+            u = update(idx, v, q, cfg).astype(np.float64)
+            w += u
+            mag += np.abs(u)
+    return w, mag
+
+
+@pytest.mark.parametrize("seed", list(range(16)) + ["np"])
+def test_momentum_snapshots_heavy_ball_closed_form(seed):
+    """P15 with several VWs, D > 0 and heterogeneous speeds: every START
+    snapshot and the final w_global equal the heavy-ball closed form over the
+    commit order (Z11) plus the VW's own unpushed updates, in fp64 within a
+    rounding bound; the same snapshot with plain-SGD weights (mu dropped) or
+    with one pushed wave missing does not."""
+    mu = 0.9
+    if seed == "np":                     # C2's NP speeds, EAGER / STRICT, D = 1
+        cfg = C2.replace(nparams=64, waves=5, D=1, lr=0.01, momentum=mu,
+                         grad_mode=GRAD_FLOAT, w0_mode=W0_PHILOX)
+    else:
+        rng = random.Random(2000 + seed)
+        cfg = _rand_cfg(rng, grad_mode=GRAD_FLOAT, lr=0.01, momentum=mu,
+                        D=rng.randint(1, 3), nparams=64)
+    idx = np.arange(cfg.nparams)
+    w0 = initial_weights(idx, cfg).astype(np.float64)
+    r = run_schedule(cfg, record_snapshots=True)
+    n = cfg.num_vw * cfg.waves * cfg.Nm + cfg.num_vw * cfg.waves + 2
+    tol = lambda mag: 4 * n * 2.0 ** -24 * mag
+    w, mag = _heavy_ball_snapshot(idx, cfg, -1, 0, r.commit, w0, mu)
+    assert np.all(np.abs(r.wg.astype(np.float64) - w) <= tol(mag))
+    negatives = 0
+    for (t, v, p, snap), (v2, p2, a_v, held_K) in zip(r.snapshots, r.start_versions):
+        assert (v, p) == (v2, p2)
+        prefix = r.commit[:held_K]
+        w, mag = _heavy_ball_snapshot(idx, cfg, v, a_v, prefix, w0, mu)
+        err = np.abs(snap.astype(np.float64) - w)
+        assert np.all(err <= tol(mag)), (v, p)
+        if any(vv != v for vv, _ in prefix):
+            sgd = _version_sum(idx, cfg, v, a_v, prefix, w0)
+            if held_K >= 2:                      # mu matters once two pushes stack
+                assert not np.all(np.abs(snap.astype(np.float64) - sgd) <= tol(mag))
+            k = next(j for j, (vv, _) in enumerate(prefix) if vv != v)
+            w_drop, _ = _heavy_ball_snapshot(idx, cfg, v, a_v,
+                                             prefix[:k] + prefix[k + 1:], w0, mu)
+            assert not np.all(np.abs(snap.astype(np.float64) - w_drop) <= tol(mag))
+            negatives += 1
+    if seed == "np":
+        assert negatives > 0
+
+
 # ----------------------------------------------------------------------------- P16
 def test_determinism_and_sampling():
     cfg = C2.replace(nparams=3000, waves=4, D=1)
