@@ -35,7 +35,11 @@ def explore(cfg):
     U = {(v, p): -float(np.float32(cfg.lr)) * gradient(idx, v, p, cfg).astype(np.float64)
          for v in range(cfg.num_vw) for p in range(1, cfg.waves * CU + 1)}
 
+    mu = cfg.momentum
+
     def version(v, a_v, prefix):
+        if mu:
+            return heavy_ball(v, a_v, prefix)
         tot = w0.copy()
         for q in range(1, a_v + 1):
             tot += U[(v, q)]
@@ -44,6 +48,24 @@ def explore(cfg):
                 lo, hi = clock_range(c, CU)
                 for q in range(lo, hi + 1):
                     tot += U[(vv, q)]
+        return tot
+
+    def heavy_ball(v, a_v, prefix):
+        """Z11 in closed form over the commit order: w0 + sum_j u~_(j)
+        (1 - mu^(K-j+1)) / (1 - mu), + own updates not in a pushed clock of the
+        prefix, up to a_v (exact for mu = 1/2 and DYADIC terms)."""
+        K = len(prefix)
+        tot = w0.copy()
+        own = set()
+        for j, (vv, c) in enumerate(prefix, start=1):
+            lo, hi = clock_range(c, CU)
+            for q in range(lo, hi + 1):
+                tot += U[(vv, q)] * (1 - mu ** (K - j + 1)) / (1 - mu)
+            if vv == v:
+                own.update(range(lo, hi + 1))
+        for q in range(1, a_v + 1):
+            if q not in own:
+                tot += U[(v, q)]
         return tot
 
     root = WSPOracle(cfg, idx, record_snapshots=True)
@@ -97,6 +119,8 @@ def explore(cfg):
             tot = w0.copy()
             for vq in allp:
                 tot += U[vq]
+            if mu:
+                tot = heavy_ball(-1, 0, sm.commit)
             assert np.array_equal(sm.wg.astype(np.float64), tot)
             memo[k] = 1
             return 1
@@ -116,10 +140,10 @@ def explore(cfg):
     return n, stats
 
 
-def _cfg(Nm, D, policy=PULL_EAGER, sem=LOCAL_STRICT):
+def _cfg(Nm, D, policy=PULL_EAGER, sem=LOCAL_STRICT, momentum=0.0):
     return WSPConfig("bf", 2, Nm, D, 8, 3, (1, 1), lr=2.0 ** -6,
                      grad_mode=GRAD_DYADIC, w0_mode=W0_PHILOX,
-                     pull_policy=policy, local_semantics=sem)
+                     pull_policy=policy, local_semantics=sem, momentum=momentum)
 
 
 @pytest.mark.parametrize("D,expected", [(0, 72), (1, 240), (2, 252), (3, 252)])
@@ -148,6 +172,19 @@ def test_bruteforce_policies(policy, sem, D):
     pull when the held version suffices, so the path set is the same."""
     n, _ = explore(_cfg(2, D, policy, sem))
     assert n == {0: 70400, 1: 200704}[D]
+
+
+@pytest.mark.parametrize("Nm,D,expected", [(1, 0, 72), (1, 1, 240), (2, 0, 70400),
+                                           (2, 1, 200704)])
+@pytest.mark.parametrize("policy,sem", [(PULL_EAGER, LOCAL_STRICT),
+                                        (PULL_LAZY, LOCAL_AT_LEAST)])
+def test_bruteforce_momentum(Nm, D, expected, policy, sem):
+    """P15 on every interleaving: with heavy-ball momentum mu = 1/2 (Z11; exact
+    in fp32 on DYADIC terms) every START snapshot and the final w_global equal
+    the heavy-ball closed form over that interleaving's commit order (+ own
+    unpushed updates); the path set is the one of plain SGD."""
+    n, stats = explore(_cfg(Nm, D, policy, sem, momentum=0.5))
+    assert n == expected and stats["starts"] > 0
 
 
 @pytest.mark.parametrize("D,expected", [(0, 22415400), (1, 56362878), (2, 57139992)])
@@ -215,3 +252,22 @@ def test_pins_catch_plausible_mistakes(monkeypatch):
     monkeypatch.setattr(WSPOracle, "complete", dropping_complete)
     with pytest.raises(AssertionError):
         explore(_cfg(2, 1))
+
+
+def test_momentum_pin_catches_plausible_mistake(monkeypatch):
+    """The momentum brute force fails when the PS applies the previous m
+    before updating it (w += m; m = mu m + u~), a plausible heavy-ball slip."""
+    from oracle.wsp import F32
+
+    def stale_push(self, t, v, c):
+        ut = self.acc[v]
+        self.wg = self.wg + self.m
+        self.m = (F32(self.cfg.momentum) * self.m) + ut
+        self.commit.append((v, c))
+        self.c_local[v] = c + 1
+        self.c_global = min(self.c_local)
+        self.acc_count[v] = 0
+
+    monkeypatch.setattr(WSPOracle, "push", stale_push)
+    with pytest.raises(AssertionError):
+        explore(_cfg(1, 0, momentum=0.5))
