@@ -254,6 +254,16 @@ def test_pins_catch_plausible_mistakes(monkeypatch):
         explore(_cfg(2, 1))
 
 
+@pytest.mark.parametrize("D,expected", [(0, 200), (1, 252)])
+def test_bruteforce_momentum_update_frequency(D, expected):
+    """The momentum brute force with F = 2 (NEXT-4: one push per two waves,
+    P:1086-1087): 2 VW x 2 clocks x 8 params, N_m = 1."""
+    cfg = WSPConfig("bf", 2, 1, D, 8, 2, (1, 1), lr=2.0 ** -6, grad_mode=GRAD_DYADIC,
+                    w0_mode=W0_PHILOX, F=2, momentum=0.5)
+    n, stats = explore(cfg)
+    assert n == expected and stats["starts"] > 0
+
+
 def test_momentum_pin_catches_plausible_mistake(monkeypatch):
     """The momentum brute force fails when the PS applies the previous m
     before updating it (w += m; m = mu m + u~), a plausible heavy-ball slip."""
