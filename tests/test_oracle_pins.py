@@ -9,7 +9,7 @@ import pytest
 from oracle import (gradient, initial_weights, philox4x32_10, run_schedule,
                     s_global, version_floor, wave_range)
 from oracle.wsp import WSPOracle, update, wave_of
-from workloads import (C1, C1_SKEW, C2, GRAD_DYADIC, GRAD_FLOAT, LOCAL_AT_LEAST,
+from workloads import (C1, C1_SKEW, C2, C3, GRAD_DYADIC, GRAD_FLOAT, LOCAL_AT_LEAST,
                        LOCAL_STRICT, PULL_EAGER, PULL_LAZY, TAU_NP, W0_PHILOX,
                        W0_ZERO, WSPConfig)
 
@@ -258,7 +258,7 @@ def _within_summation_bound(got, w0, idx, cfg, pairs):
     return bool(np.all(np.abs(got.astype(np.float64) - exact) <= bound))
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", list(range(24)) + ["np", "hd"])
 def test_float_snapshots_within_summation_bound(seed):
     """FLOAT mode, D > 0, heterogeneous speeds (the case whose exact bits only
     the oracle fixes): every START snapshot, the final
@@ -266,9 +266,13 @@ def test_float_snapshots_within_summation_bound(seed):
     set (the same sets the DYADIC pins fix exactly) to within the recursive
     summation bound of Higham eq. 4.4; a snapshot with one update dropped or
     with one extra update does not."""
-    rng = random.Random(1000 + seed)
-    cfg = _rand_cfg(rng, grad_mode=GRAD_FLOAT, lr=0.01, D=rng.randint(1, 4),
-                    nparams=64)
+    if seed in ("np", "hd"):             # C2's NP speeds at D = 1; C3's HD speeds, D = 4
+        cfg = (C2.replace(D=1) if seed == "np" else C3).replace(
+            nparams=64, waves=6, lr=0.01, grad_mode=GRAD_FLOAT, w0_mode=W0_PHILOX)
+    else:
+        rng = random.Random(1000 + seed)
+        cfg = _rand_cfg(rng, grad_mode=GRAD_FLOAT, lr=0.01, D=rng.randint(1, 4),
+                        nparams=64)
     idx = np.arange(cfg.nparams)
     w0 = initial_weights(idx, cfg).astype(np.float64)
     r = run_schedule(cfg, record_snapshots=True)
