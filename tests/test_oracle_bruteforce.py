@@ -28,7 +28,7 @@ def _key(sm):
             tuple(tuple(b) for b in sm.backlog), tuple(sm.commit))
 
 
-def explore(cfg):
+def explore(cfg, seen=None):
     idx = np.arange(8)
     w0 = initial_weights(idx, cfg).astype(np.float64)
     CU = cfg.F * cfg.Nm                    # minibatches per clock (F waves)
@@ -105,6 +105,11 @@ def explore(cfg):
             assert np.array_equal(snap.astype(np.float64),
                                   version(v, a_v, sm.commit[:held_K]))
             stats["starts"] += 1
+            if seen is not None:      # newest other-VW minibatch this START holds
+                top = min(max([clock_range(c, CU)[1] for vv, c in sm.commit[:held_K]
+                               if vv == o], default=0)
+                          for o in range(cfg.num_vw) if o != v)
+                seen[(v, p)] = min(seen.get((v, p), top), top)
         assert max(sm.c_local) - min(sm.c_local) <= cfg.D + 1
 
     def count(sm):
@@ -281,3 +286,25 @@ def test_momentum_pin_catches_plausible_mistake(monkeypatch):
     monkeypatch.setattr(WSPOracle, "push", stale_push)
     with pytest.raises(AssertionError):
         explore(_cfg(1, 0, momentum=0.5))
+
+
+@pytest.mark.parametrize("Nm,D,W", [(1, 0, 3), (1, 1, 3), (2, 0, 3), (2, 1, 4), (3, 0, 3)])
+def test_global_staleness_bound_is_tight(Nm, D, W):
+    """P4: minibatch p is guaranteed every global update of
+    minibatches 1..p-(s_global+1), s_global = (D+2) N_m - 2. Over every
+    interleaving, the oldest other-VW state any START(p) can hold never goes
+    below that floor, and the floor is attained: some START reads exactly it
+    (the paper's example, minibatch 11 needs only 1..4 at N_m = 4, D = 0)."""
+    from oracle import version_floor
+    seen = {}
+    cfg = WSPConfig("bf", 2, Nm, D, 8, W, (1, 1), lr=2.0 ** -6,
+                    grad_mode=GRAD_DYADIC, w0_mode=W0_PHILOX)
+    explore(cfg, seen)
+    attained = 0
+    for (v, p), top in seen.items():
+        fl = max(0, version_floor(p, Nm, D))
+        assert top >= fl, (v, p, top, fl)
+        if fl > 0 and fl % Nm == 0:          # the floor ends a wave: reached exactly
+            assert top == fl, (v, p, top, fl)
+            attained += 1
+    assert attained > 0
