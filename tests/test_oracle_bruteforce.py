@@ -73,7 +73,7 @@ def explore(cfg, seen=None):
         for p in range(1, min(cfg.Nm, root.last_p) + 1):
             root.start(0, v, p)
     memo = {}
-    stats = {"states": 0, "starts": 0}
+    stats = {"states": 0, "starts": 0, "max_gap": 0}
 
     def enabled(sm):
         steps = []
@@ -110,7 +110,9 @@ def explore(cfg, seen=None):
                                if vv == o], default=0)
                           for o in range(cfg.num_vw) if o != v)
                 seen[(v, p)] = min(seen.get((v, p), top), top)
-        assert max(sm.c_local) - min(sm.c_local) <= cfg.D + 1
+        gap = max(sm.c_local) - min(sm.c_local)
+        assert gap <= cfg.D + 1
+        stats["max_gap"] = max(stats["max_gap"], gap)
 
     def count(sm):
         k = _key(sm)
@@ -308,3 +310,15 @@ def test_global_staleness_bound_is_tight(Nm, D, W):
             assert top == fl, (v, p, top, fl)
             attained += 1
     assert attained > 0
+
+
+@pytest.mark.parametrize("Nm,D,W", [(1, 0, 3), (1, 1, 3), (2, 0, 3), (2, 1, 4), (1, 2, 5)])
+def test_clock_distance_bound_is_tight(Nm, D, W):
+    """P11 (north_star "no VW's clock runs more than D+1 waves past the
+    slowest"): over every interleaving the clock distance never exceeds D+1,
+    and some interleaving reaches D+1 (a fast VW that has pushed its gated
+    wave while the slow one has pushed none beyond c_global)."""
+    cfg = WSPConfig("bf", 2, Nm, D, 8, W, (1, 1), lr=2.0 ** -6,
+                    grad_mode=GRAD_DYADIC, w0_mode=W0_PHILOX)
+    _, stats = explore(cfg)
+    assert stats["max_gap"] == D + 1
