@@ -15,7 +15,8 @@ Pins (tests/test_oracle_*.py): Philox known-answer vectors, the paper's worked
 examples, closed forms (BSP limit P:960 / P:819,
 conservation P:928-929), invariants (D+1 clock bound P:942, p-Nm read bound
 P:846-847, lockstep at D=0), brute force over every interleaving of
-2 VW x 3 waves x 8 params (also with F = 2); the weight-dependent CONVEX
+2 VW x 3 waves x 8 params (also with F = 2 and with heavy-ball momentum;
+the s_global floor and the D+1 clock distance shown tight); the weight-dependent CONVEX
 workload's BSP closed form and delayed recurrence, the section-6
 decomposition and Lemma 1 (tests/test_oracle_convex.py); s_global with F
 (tests/test_oracle_update_freq.py); the pipeline partitioner / simulator
