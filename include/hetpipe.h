@@ -171,8 +171,18 @@ int64_t hp_arena_bytes(const hp_config* cfg);
 /* As hp_connect, for a context whose cfg.arena is a symmetric allocation:
    peer_bases[q] (world entries, q = rank is this arena) is rank q's arena mapped
    into this process, mc_base the multicast mapping of the arenas (NULL if none;
-   HP_XPORT_NVLS needs it). No CUDA IPC is used. Errors: HP_ERR_STATE (not
-   world > 1, no external arena, or already connected), HP_ERR_COMM. */
+   HP_XPORT_NVLS needs it). No CUDA IPC is used.
+   comm_id may be NULL: co-located ranks connected WITHOUT an NCCL communicator
+   (e.g. G threads of one process driving G contexts on one GPU, peer_bases =
+   the other contexts' arenas). Every barrier is then the K7 device flag
+   barrier (HP_FLAG_BARRIER=0 is refused) and the exchange is HP_XPORT_PEER
+   (HP_XPORT_NCCL is refused; NVLS without mc_base never runs). The caller
+   must let every rank's hp_init_ex return before any rank connects (init
+   zeroes the flag arrays); the first flag barrier then orders every rank's
+   initialisation before any peer access. Collective: every rank calls it.
+   Errors: HP_ERR_STATE (not world > 1, no external arena, already connected,
+   or a refused combination above), HP_ERR_COMM (a rank never arrived: the
+   flag wait's 10 s deadline). */
 hp_status hp_connect_symmetric(hp_ctx* ctx, const void* const* peer_bases, void* mc_base,
                                const void* comm_id);
 
@@ -239,10 +249,33 @@ hp_status hp_schedule_begin(hp_ctx* ctx, const int64_t* tau, const int64_t* lat)
 /* Run ticks until the commit log holds >= target_commits pushes or the run is
    complete; *commits (may be NULL) receives the count reached. */
 hp_status hp_schedule_advance(hp_ctx* ctx, int64_t target_commits, int64_t* commits);
+/* CUDA-graph form of hp_schedule_advance, for launch-bound (small) models:
+   the controller advances to target_commits NOW on the host (protocol state,
+   trace, stats move exactly as hp_schedule_advance), but the device work of
+   those ticks -- every fused tick launch, and in distributed contexts the
+   side-stream launches and flag barriers, forked from and joined back to the
+   context stream -- is captured into one CUDA graph (stream capture of the
+   context stream, relaxed mode) instead of running. hp_graph_launch then runs
+   it ONCE on the context stream (a graph holds those ticks' descriptors; a
+   second launch would redo them, so it is refused: HP_ERR_STATE). Until that
+   launch, do not read weights or capture again (HP_ERR_STATE). Not allowed with
+   host gradients (pageable copies cannot be captured) or while per-launch
+   profiling is on (HP_ERR_STATE). *out owned by the caller: hp_graph_destroy. */
+typedef struct hp_graph hp_graph;
+hp_status hp_schedule_capture(hp_ctx* ctx, int64_t target_commits, int64_t* commits,
+                              hp_graph** out);
+hp_status hp_graph_launch(hp_graph* g);
+void hp_graph_destroy(hp_graph* g);
+/* Calibration for latency-bound configs (C1): device microseconds per launch
+   of n back-to-back empty one-CTA kernels on the context stream (launched
+   like the tick kernels, with the PDL attribute), issued directly (graph = 0)
+   or as one CUDA graph (graph = 1); synchronising. */
+hp_status hp_launch_floor(hp_ctx* ctx, int32_t n, int32_t graph, float* us_per_launch);
 /* Whole run: begin + advance to num_vw*waves pushes + final apply flush. */
 hp_status hp_run_schedule(hp_ctx* ctx, const int64_t* tau, const int64_t* lat);
 /* HP_GRAD_EXTERNAL under the controller: COMPLETE(v,p) copies host buffer
-   host_bufs[(v*W*N_m + p) % n] (each fp32[param_count]) to the device. */
+   host_bufs[(v*W*F*N_m + p) % n] (each fp32[param_count]; F = update_freq) to
+   the device. */
 hp_status hp_schedule_set_host_grads(hp_ctx* ctx, const float* const* host_bufs, int32_t n);
 
 /* Flush every pending op and apply, then synchronise the stream. */
@@ -274,6 +307,9 @@ typedef struct {
                                switch's reduced u~ + the w_local multicast stores it
                                receives; NCCL = the data the collectives deliver) */
   int64_t lockstep_batches; /* batches exchanged by the NCCL / NVLS transport */
+  int64_t apply_batches;    /* PS apply batches (flushes that applied >= 1 push):
+                               pushes / apply_batches = the k of SURVEY.md 8(d)'s
+                               byte model 16*F*Nm per push + 8(1+[mu]) per batch */
 } hp_stats;
 hp_status hp_get_stats(hp_ctx* ctx, hp_stats* out);
 

@@ -33,7 +33,11 @@ class Controller {
       lat_[v] = lat ? lat[v] : (int64_t)cfg.Nm * tau_[v];
       if (lat_[v] < 1) return e_->fail(HP_ERR_INVALID, "lat must be >= 1");
     }
-    ctime_.assign(N, std::vector<int64_t>((size_t)e_->last_p() + 2, -1));
+    // STARTs of a VW are scheduled in increasing p (ungated p+Nm after p's
+    // COMPLETE, a gated START before its backlog, Z17), so only the latest
+    // completion time per VW is needed -- never a table over all minibatches
+    last_ct_.assign(N, -1);
+    last_sp_.assign(N, 0);
     events_.clear();
     for (int v = 0; v < N; ++v)
       for (int64_t p = 1; p <= std::min<int64_t>(cfg.Nm, e_->last_p()); ++p) schedule(0, v, p);
@@ -49,12 +53,15 @@ class Controller {
     return e_->flush_pending();   // everything committed so far is enqueued
   }
   void set_host_grads(const float* const* bufs, int n) { host_.assign(bufs, bufs + n); }
+  bool host_grads() const { return !host_.empty(); }
 
  private:
   void schedule(int64_t t, int v, int64_t p) {
+    // complete(p) = max(start(p) + L_v, complete(p-1) + tau_v) (Z13)
     int64_t ct = t + lat_[v];
-    if (p > 1 && ctime_[v][p - 1] >= 0) ct = std::max(ct, ctime_[v][p - 1] + tau_[v]);
-    ctime_[v][p] = ct;
+    if (p > 1 && last_sp_[v] == p - 1) ct = std::max(ct, last_ct_[v] + tau_[v]);
+    last_ct_[v] = ct;
+    last_sp_[v] = p;
     events_[ct].push_back({v, p});
   }
   hp_status tick() {
@@ -93,7 +100,8 @@ class Controller {
 
   Engine* e_;
   std::vector<int64_t> tau_, lat_;
-  std::vector<std::vector<int64_t>> ctime_;
+  std::vector<int64_t> last_ct_;   // per VW: completion time of its latest START
+  std::vector<int64_t> last_sp_;   //   and that START's minibatch
   std::map<int64_t, std::vector<std::pair<int, int64_t>>> events_;
   std::vector<const float*> host_;
   bool active_ = false;
@@ -104,6 +112,12 @@ class Controller {
 struct hp_ctx {
   std::unique_ptr<hp::Engine> eng;
   std::unique_ptr<hp::Controller> ctl;
+};
+
+struct hp_graph {
+  hp_ctx* ctx = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool launched = false;
 };
 
 namespace {
@@ -334,7 +348,7 @@ hp_status hp_connect(hp_ctx* ctx, const void* handles, const void* comm_id) {
 hp_status hp_connect_symmetric(hp_ctx* ctx, const void* const* peer_bases, void* mc_base,
                                const void* comm_id) {
   HP_ENTRY(ctx)
-  if (!peer_bases || !comm_id) return ctx->eng->fail(HP_ERR_INVALID, "NULL peer_bases or id");
+  if (!peer_bases) return ctx->eng->fail(HP_ERR_INVALID, "NULL peer_bases");
   return ctx->eng->connect_symmetric(peer_bases, mc_base, comm_id);
   HP_EXIT(ctx)
 }
@@ -355,10 +369,52 @@ hp_status hp_schedule_begin(hp_ctx* ctx, const int64_t* tau, const int64_t* lat)
 
 hp_status hp_schedule_advance(hp_ctx* ctx, int64_t target, int64_t* commits) {
   HP_ENTRY(ctx)
+  if (ctx->eng->graph_pending())
+    return ctx->eng->fail(HP_ERR_STATE, "a captured graph has not been launched");
   hp_status st = ctx->ctl->advance(target);
   if (commits) *commits = ctx->eng->commits();
   return st;
   HP_EXIT(ctx)
+}
+
+hp_status hp_schedule_capture(hp_ctx* ctx, int64_t target, int64_t* commits, hp_graph** out) {
+  HP_ENTRY(ctx)
+  if (!out) return ctx->eng->fail(HP_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (ctx->ctl->host_grads()) return ctx->eng->fail(HP_ERR_STATE, "host gradients cannot be captured");
+  if (hp_status st = ctx->eng->capture_begin()) return st;
+  hp_status st = ctx->ctl->advance(target);
+  cudaGraphExec_t exec = nullptr;
+  if (hp_status st2 = ctx->eng->capture_end(st == HP_OK, &exec)) return st != HP_OK ? st : st2;
+  if (commits) *commits = ctx->eng->commits();
+  hp_graph* g = new hp_graph;
+  g->ctx = ctx;
+  g->exec = exec;
+  *out = g;
+  return HP_OK;
+  HP_EXIT(ctx)
+}
+
+hp_status hp_graph_launch(hp_graph* g) {
+  if (!g || !g->ctx) return HP_ERR_INVALID;
+  hp_ctx* ctx = g->ctx;
+  HP_ENTRY(ctx)
+  if (g->launched) return ctx->eng->fail(HP_ERR_STATE, "graph already launched");
+  g->launched = true;
+  return ctx->eng->graph_launch(g->exec);
+  HP_EXIT(ctx)
+}
+
+hp_status hp_launch_floor(hp_ctx* ctx, int32_t n, int32_t graph, float* us_per_launch) {
+  HP_ENTRY(ctx)
+  return ctx->eng->launch_floor(n, graph != 0, us_per_launch);
+  HP_EXIT(ctx)
+}
+
+void hp_graph_destroy(hp_graph* g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  delete g;
 }
 
 hp_status hp_run_schedule(hp_ctx* ctx, const int64_t* tau, const int64_t* lat) {

@@ -167,11 +167,17 @@ void Engine::plan_layout() {
 
 hp_status Engine::init() {
   if (cudaSetDevice(cfg_.device) != cudaSuccess) return check_cuda(cudaGetLastError(), "cudaSetDevice");
+  if (hp_status st = check_cuda(preload_kernels(), "kernel preload")) return st;
   if (cfg_.stream) {
     stream_ = (cudaStream_t)cfg_.stream;
   } else {
     if (int e = cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking)) return check_cuda(e, "stream");
     own_stream_ = true;
+  }
+  if (const char* sv = getenv("HP_STRESS")) {
+    const uint64_t seed = strtoull(sv, nullptr, 10);
+    if (seed) stress_ = (seed * 0x9E3779B97F4A7C15ull) ^ (uint64_t)(cfg_.rank + 1) * 0xD1B54A32D192ED03ull;
+    if (const char* us = getenv("HP_STRESS_US")) stress_ns_ = 1000ull * strtoull(us, nullptr, 10);
   }
   // arena: w_global, [m], per VW w_local + R acc slots; each 256-byte aligned.
   // Single-rank contexts own [param_begin, +param_count) of every buffer; with
@@ -286,7 +292,7 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
                            bool* wave_end_out) {
   if (sticky_) return sticky_;
   if (v < 0 || v >= N_) return fail(HP_ERR_INVALID, "vw out of range");
-  if (dist_ && !comm_) return fail(HP_ERR_STATE, "distributed context not connected (hp_connect)");
+  if (dist_ && !connected_) return fail(HP_ERR_STATE, "distributed context not connected (hp_connect)");
   VW& s = vw_[v];
   if (p != s.completed + 1 || p > s.started || p > last_p_)
     return fail(HP_ERR_PROTOCOL, "COMPLETE out of order or minibatch not started");
@@ -326,6 +332,7 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
     grad_host = nullptr;
     g = nullptr;
   }
+  if (grad_host && capturing_) return fail(HP_ERR_STATE, "host gradients cannot be captured");
   if (grad_host) {  // library-owned device copy of a host gradient
     if (s.grad_ring.empty()) {
       s.grad_ring.assign(Nm_, nullptr);
@@ -354,11 +361,13 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
       fork_streams();
       cst = vs_[v];
       for (cudaStream_t o : {xs_, fs_[v]}) {
+        if (!o) continue;                 // no fold stream (HP_SPLIT_FOLDS off)
         cudaEvent_t e = pool_event();
         cudaEventRecord(e, o);
         cudaStreamWaitEvent(cst, e, 0);
       }
     }
+    stress(cst);
     if (hp_status st = check_cuda(cudaMemcpyAsync(dst, src, (size_t)s.len * 4,
                                                   cudaMemcpyHostToDevice, cst), "H2D grad"))
       return st;
@@ -611,6 +620,7 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   d.done = nullptr;
   if (dyn_env && loads >= dyn_min && n >= dyn_n && (dyn_pulls || d.ng == 0))
     tile_slot(st, &d.ctr, &d.done);
+  stress(st);
   prof_begin(st);
   int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, st, max_blocks);
   int inl = 0;
@@ -693,7 +703,17 @@ hp_status Engine::profile_sync(int64_t max, float* ms, int32_t* vw, int32_t* wai
 // that exceeds its deadline sets a device error flag, reported as
 // HP_ERR_COMM at the next synchronising call. HP_FLAG_BARRIER=0 uses a
 // 4-byte NCCL all-reduce instead. Profiled like a launch (shape nf = 126).
+void Engine::stress(cudaStream_t st) {
+  if (!stress_) return;
+  stress_ ^= stress_ << 13;
+  stress_ ^= stress_ >> 7;
+  stress_ ^= stress_ << 17;
+  if (stress_ & 1) return;
+  launch_spin((stress_ >> 8) % (stress_ns_ + 1), st);
+}
+
 hp_status Engine::xbarrier() {
+  stress(xs_);
   prof_begin(xs_);
   if (flag_barrier_) {
     ++epoch_;
@@ -706,8 +726,8 @@ hp_status Engine::xbarrier() {
     for (int q = 0; q < G_; ++q)
       fb.flags[q] = (unsigned long long*)(peer_[q] + lay_[q].flag_off);
     if (int e = launch_flag_barrier(fb, xs_)) return check_cuda(e, "flag barrier");
-  } else if (comm_->barrier(xs_) != 0) {
-    return fail(HP_ERR_COMM, comm_->error());
+  } else if (!comm_ || comm_->barrier(xs_) != 0) {
+    return fail(HP_ERR_COMM, comm_ ? comm_->error() : "no communicator for the NCCL barrier");
   }
   prof_end(xs_, 0.0, 0.0, 126 << 24);
   return HP_OK;
@@ -859,6 +879,7 @@ hp_status Engine::flush_local() {
     a.seg_end = d.ns;
   }
   applied_ += (int64_t)ba_.size();
+  apply_batches_ += ba_.empty() ? 0 : 1;
   // 3. w_local: pulled VWs and VWs whose folds are due now (phase D), or the
   //    single due fold of this batch's own complete, folded inline (phase B)
   for (int v = 0; v < N_; ++v) {
@@ -906,16 +927,29 @@ hp_status Engine::flush_local() {
 }
 
 cudaEvent_t Engine::pool_event() {
-  // events are reused round-robin; an event is only waited on shortly after it
-  // is recorded, long before the pool wraps
-  if (evpool_.size() < 256) {
-    cudaEvent_t e;
-    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    evpool_.push_back(e);
-    return e;
+  // Events are reused round-robin. A cudaStreamWaitEvent already enqueued keeps
+  // the point the event was recorded at, so re-recording is safe -- except for
+  // an event still stored as a dependency for a LATER wait (xacc_, xwl_, lastc_,
+  // lastw_): those are skipped, so a stored dependency never silently moves.
+  auto stored = [&](cudaEvent_t e) {
+    for (const auto& x : xacc_)
+      for (cudaEvent_t y : x)
+        if (y == e) return true;
+    for (const auto* vec : {&xwl_, &lastc_, &lastw_})
+      for (cudaEvent_t y : *vec)
+        if (y == e) return true;
+    return false;
+  };
+  if (evpool_.size() >= 256) {
+    for (size_t tries = 0; tries < evpool_.size(); ++tries) {
+      cudaEvent_t e = evpool_[evnext_];
+      evnext_ = (evnext_ + 1) % evpool_.size();
+      if (!stored(e)) return e;
+    }
   }
-  cudaEvent_t e = evpool_[evnext_];
-  evnext_ = (evnext_ + 1) % evpool_.size();
+  cudaEvent_t e;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  evpool_.push_back(e);
   return e;
 }
 
@@ -935,6 +969,7 @@ hp_status Engine::flush_applies() {
 
 hp_status Engine::sync() {
   if (sticky_) return sticky_;
+  if (capturing_ || graph_pending_) return fail(HP_ERR_STATE, "a captured graph has not been launched");
   for (auto& vp : ungated_) rec('S', vp.first, "START", vp.second, wave_of(vp.second, U_));
   ungated_.clear();
   if (hp_status st = flush_applies()) return st;
@@ -950,6 +985,85 @@ hp_status Engine::sync() {
       return fail(HP_ERR_COMM, "K7 readiness flag wait timed out (a rank stopped issuing barriers)");
     }
   }
+  return HP_OK;
+}
+
+hp_status Engine::capture_begin() {
+  if (sticky_) return sticky_;
+  if (capturing_ || graph_pending_) return fail(HP_ERR_STATE, "a captured graph has not been launched");
+  if (prof_on_) return fail(HP_ERR_STATE, "per-launch profiling is on: cannot capture");
+  // earlier host-queued device work belongs to the stream before the graph
+  if (hp_status st = flush_pending()) return st;
+  if (int e = cudaStreamBeginCapture(stream_, cudaStreamCaptureModeRelaxed))
+    return check_cuda(e, "cudaStreamBeginCapture");
+  capturing_ = true;
+  return HP_OK;
+}
+
+hp_status Engine::capture_end(bool ok, cudaGraphExec_t* exec) {
+  if (!capturing_) return fail(HP_ERR_STATE, "not capturing");
+  capturing_ = false;
+  cudaGraph_t g = nullptr;
+  const int e = cudaStreamEndCapture(stream_, &g);
+  if (!ok) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    // the host state moved past device work that will never run
+    sticky_ = HP_ERR_STATE;
+    return sticky_;
+  }
+  if (e) return check_cuda(e, "cudaStreamEndCapture");
+  const int e2 = cudaGraphInstantiate(exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e2) return check_cuda(e2, "cudaGraphInstantiate");
+  graph_pending_ = true;
+  return HP_OK;
+}
+
+hp_status Engine::graph_launch(cudaGraphExec_t exec) {
+  if (sticky_) return sticky_;
+  if (!graph_pending_) return fail(HP_ERR_STATE, "no captured graph pending");
+  graph_pending_ = false;
+  return check_cuda(cudaGraphLaunch(exec, stream_), "cudaGraphLaunch");
+}
+
+// hp_launch_floor: device time per launch of n back-to-back empty kernels on
+// the context stream, issued directly or as one captured graph (after one
+// warm-up round of the same form).
+hp_status Engine::launch_floor(int n, bool graph, float* us) {
+  if (sticky_) return sticky_;
+  if (capturing_ || graph_pending_) return fail(HP_ERR_STATE, "a captured graph has not been launched");
+  if (n < 1 || !us) return fail(HP_ERR_INVALID, "n >= 1 and us needed");
+  if (hp_status st = flush_pending()) return st;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaGraphExec_t exec = nullptr;
+  int err = 0;
+  if (graph) {
+    cudaGraph_t g = nullptr;
+    err = cudaStreamBeginCapture(stream_, cudaStreamCaptureModeRelaxed);
+    for (int i = 0; i < n && !err; ++i) err = launch_empty(stream_);
+    const int e2 = cudaStreamEndCapture(stream_, &g);
+    if (!err) err = e2;
+    if (!err) err = cudaGraphInstantiate(&exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+  }
+  float ms = 0.f;
+  for (int rep = 0; rep < 2 && !err; ++rep) {     // rep 0 warms up
+    cudaEventRecord(e0, stream_);
+    if (graph) err = cudaGraphLaunch(exec, stream_);
+    else
+      for (int i = 0; i < n && !err; ++i) err = launch_empty(stream_);
+    cudaEventRecord(e1, stream_);
+    if (!err) err = cudaEventSynchronize(e1);
+    if (!err) err = cudaEventElapsedTime(&ms, e0, e1);
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (err) return check_cuda(err, "launch floor");
+  *us = 1e3f * ms / (float)n;
   return HP_OK;
 }
 
@@ -979,10 +1093,12 @@ void Engine::stats(hp_stats* out) const {
   }
   out->nvl_bytes = nvl_bytes_;
   out->lockstep_batches = lockstep_batches_;
+  out->apply_batches = apply_batches_;
 }
 
 hp_status Engine::profile_enable(bool on) {
   if (sticky_) return sticky_;
+  if (capturing_ || graph_pending_) return fail(HP_ERR_STATE, "a captured graph has not been launched");
   prof_on_ = on;
   ev_used_ = 0;
   prof_bytes_ = 0;

@@ -90,6 +90,13 @@ class Engine {
   }
   hp_status sync();
   hp_status read(int which, int64_t off, int64_t cnt, float* dst);
+  // CUDA-graph capture of the device work of a controller advance
+  // (hp_schedule_capture): begin -> the caller advances -> end(graph exec)
+  hp_status capture_begin();
+  hp_status capture_end(bool ok, cudaGraphExec_t* exec);
+  hp_status graph_launch(cudaGraphExec_t exec);
+  bool graph_pending() const { return graph_pending_; }
+  hp_status launch_floor(int n, bool graph, float* us);
 
   void set_tick(int64_t t) { tick_ = t; }
   bool at_gate(int v) const { return vw_[v].at_gate; }
@@ -177,7 +184,9 @@ class Engine {
   char* mc_ = nullptr;                // multicast mapping of the arenas (NVLS)
   bool ext_arena_ = false;            // cfg.arena: caller-owned
   std::vector<void*> opened_;         // IPC mappings to close
-  Comm* comm_ = nullptr;
+  Comm* comm_ = nullptr;              // NCCL communicator (nullptr: co-located ranks
+                                      // connected without NCCL, hp_connect_symmetric)
+  bool connected_ = false;
   // a9 overlap (world > 1): barrier/apply/pull launches run on an exchange
   // stream; a compute-stream launch waits only for the exchange events of the
   // VWs whose buffers it touches.
@@ -207,10 +216,20 @@ class Engine {
   char* tiles_ = nullptr;
   std::vector<cudaStream_t> tile_streams_;
   bool tile_slot(cudaStream_t st, unsigned long long** ctr, unsigned int** done);
+  // HP_STRESS=<seed> (HP_STRESS_US, default 50): before a launch, with
+  // probability 1/2, an idle kernel of 0..HP_STRESS_US microseconds on the
+  // launch stream (race stress of the stream / event / flag protocol; the
+  // arithmetic is unchanged). Per-rank xorshift stream, seeded seed ^ rank.
+  uint64_t stress_ = 0;
+  uint64_t stress_ns_ = 50000;
+  void stress(cudaStream_t st);
   std::vector<cudaEvent_t> evpool_;
   size_t evnext_ = 0;
   double nvl_bytes_ = 0;
   int64_t lockstep_batches_ = 0;
+  bool capturing_ = false;            // stream capture of stream_ in progress
+  bool graph_pending_ = false;        // a captured graph awaits its launch
+  int64_t apply_batches_ = 0;
   int N_, Nm_, R_;
   int64_t U_ = 1;                     // minibatches per clock: F * Nm (NEXT-4)
   bool convex_ = false;               // HP_GRAD_CONVEX: stash ring + STASH ops

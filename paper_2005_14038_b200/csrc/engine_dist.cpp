@@ -223,6 +223,7 @@ hp_status Engine::dist_apply(std::vector<Prim>* prims_out, bool* fuse_out) {
       if (hp_status st = emit(d, begin_, n_, xs_, xblocks_, x_link)) return st;
     }
     applied_ += (int64_t)ba_.size();
+    apply_batches_++;
     if (hp_status st = xbarrier()) return st;
     cudaEvent_t e = pool_event();       // acc slots read by the applies are free
     cudaEventRecord(e, xs_);
@@ -378,7 +379,17 @@ hp_status Engine::dist_pull(const std::vector<Prim>& prims, bool fuse_pull) {
       if (vw_[v].here) {
         xwl_[v] = e;
         lastw_[v] = nullptr;              // ordered behind e
-        if (!strict) xacc_[v][vw_[v].c_local % R_] = e;   // read as the partial u~
+        // the pull read a partial aggregate (AT_LEAST; STRICT with F > 1): the
+        // acc slot of the open clock or, STRICT, the snapshot taken at the gate.
+        // Completes that rewrite it wait for e. The snapshot is rewritten by a
+        // complete of a later clock, whatever its slot: every slot waits then
+        // (xs_ is in order, so e covers the events it replaces).
+        const float* part = vw_[v].pull_partial;
+        if (part && part == vw_[v].snap) {
+          for (auto& x : xacc_[v]) x = e;
+        } else if (part || !strict) {
+          xacc_[v][vw_[v].c_local % R_] = e;
+        }
       }
   }
   return HP_OK;
@@ -477,6 +488,7 @@ hp_status Engine::flush_lockstep(int slot) {
     if (nvls_dyn) tile_slot(xs_, &d.ctr, &d.done);
     const double fr = n_ > 0 ? (double)n1 / (double)n_ : 0.0;   // multicast share
     const double bytes = 4.0 * (double)n1 * (2 + G_ + (pull ? G_ : 0));
+    stress(xs_);
     prof_begin(xs_);
     const int err = launch_nvls(d, xs_, xblocks_);
     // per GPU and direction: its acc replica served to every owner's reduction
@@ -528,6 +540,7 @@ hp_status Engine::flush_lockstep(int slot) {
   }
   applied_ += (int64_t)ba_.size();
   lockstep_batches_++;
+  apply_batches_++;
   for (int v : bpull_) {
     VW& t = vw_[v];
     std::vector<int64_t> folds;
@@ -614,7 +627,7 @@ hp_status Engine::ipc_handle(void* out) {
 hp_status Engine::connect(const void* handles, const void* comm_id) {
   if (sticky_) return sticky_;
   if (!dist_) return fail(HP_ERR_STATE, "hp_connect needs world > 1");
-  if (comm_) return fail(HP_ERR_STATE, "already connected");
+  if (connected_) return fail(HP_ERR_STATE, "already connected");
   if (cfg_.transport == HP_XPORT_NVLS)
     return fail(HP_ERR_STATE, "HP_XPORT_NVLS needs hp_connect_symmetric with a multicast mapping");
   for (int q = 0; q < G_; ++q) {
@@ -633,7 +646,7 @@ hp_status Engine::connect(const void* handles, const void* comm_id) {
 hp_status Engine::connect_symmetric(const void* const* bases, void* mc, const void* comm_id) {
   if (sticky_) return sticky_;
   if (!dist_) return fail(HP_ERR_STATE, "hp_connect_symmetric needs world > 1");
-  if (comm_) return fail(HP_ERR_STATE, "already connected");
+  if (connected_) return fail(HP_ERR_STATE, "already connected");
   if (!ext_arena_) return fail(HP_ERR_STATE, "hp_connect_symmetric needs cfg.arena");
   if (cfg_.transport == HP_XPORT_NVLS && !mc)
     return fail(HP_ERR_STATE, "HP_XPORT_NVLS needs a multicast mapping");
@@ -648,10 +661,19 @@ hp_status Engine::connect_symmetric(const void* const* bases, void* mc, const vo
 }
 
 hp_status Engine::finish_connect(const void* comm_id) {
-  std::string err;
-  comm_ = comm_create(comm_id, G_, rank_, &err);
-  if (!comm_) return fail(HP_ERR_COMM, err);
   if (const char* fb = getenv("HP_FLAG_BARRIER")) flag_barrier_ = atoi(fb) != 0;
+  if (comm_id) {
+    std::string err;
+    comm_ = comm_create(comm_id, G_, rank_, &err);
+    if (!comm_) return fail(HP_ERR_COMM, err);
+  } else {
+    // co-located ranks (e.g. threads of one process sharing a GPU): no NCCL
+    // communicator, so the barriers are the K7 device flags and the exchange
+    // is the PEER path (NCCL refuses two ranks on one device)
+    if (!flag_barrier_) return fail(HP_ERR_STATE, "connecting without a communicator needs the flag barrier");
+    if (cfg_.transport == HP_XPORT_NCCL)
+      return fail(HP_ERR_STATE, "HP_XPORT_NCCL needs a communicator id");
+  }
   if (flag_barrier_) {
     if (int e = cudaMalloc((void**)&flag_err_, sizeof(int))) return check_cuda(e, "flag error");
     if (int e = cudaMemset(flag_err_, 0, sizeof(int))) return check_cuda(e, "flag error");
@@ -665,8 +687,10 @@ hp_status Engine::finish_connect(const void* comm_id) {
     if (atoi(pr) == 0) prio_lo = prio_hi = 0;
   if (int e = cudaStreamCreateWithPriority(&xs_, cudaStreamNonBlocking, prio_hi))
     return check_cuda(e, "stream");
-  if (int e = cudaStreamCreateWithPriority(&xs2_, cudaStreamNonBlocking, prio_hi))
-    return check_cuda(e, "stream");
+  // (the second exchange stream serves only the NVLS / peer split)
+  if (cfg_.transport == HP_XPORT_NVLS)
+    if (int e = cudaStreamCreateWithPriority(&xs2_, cudaStreamNonBlocking, prio_hi))
+      return check_cuda(e, "stream");
   if (const char* ns = getenv("HP_NVLS_SPLIT")) nvls_split_ = std::max(0, std::min(100, atoi(ns)));
   xacc_.assign(N_, std::vector<cudaEvent_t>(R_, nullptr));
   xwl_.assign(N_, nullptr);
@@ -681,14 +705,40 @@ hp_status Engine::finish_connect(const void* comm_id) {
     {
       if (int e = cudaStreamCreateWithPriority(&vs_[v], cudaStreamNonBlocking, prio_lo))
         return check_cuda(e, "stream");
-      if (int e = cudaStreamCreateWithPriority(&fs_[v], cudaStreamNonBlocking, prio_hi))
-        return check_cuda(e, "stream");
+      if (split_folds_)                 // fold streams only for split acc / fold launches
+        if (int e = cudaStreamCreateWithPriority(&fs_[v], cudaStreamNonBlocking, prio_hi))
+          return check_cuda(e, "stream");
     }
   if (const char* xb = getenv("HP_XBLOCKS")) xblocks_ = atoi(xb);
   if (const char* ab = getenv("HP_ABLOCKS")) ablocks_ = atoi(ab);
-  // everyone's init writes are complete before anyone reads a peer
-  if (comm_->barrier(stream_) != 0) return fail(HP_ERR_COMM, comm_->error());
-  return check_cuda(cudaStreamSynchronize(stream_), "connect sync");
+  // everyone's init writes are complete before anyone reads a peer (without a
+  // communicator: the first flag barrier, epoch 1 on every rank -- the flag
+  // arrays were zeroed by every rank's hp_init_ex, which the caller ordered
+  // before any hp_connect_symmetric)
+  if (comm_) {
+    if (comm_->barrier(stream_) != 0) return fail(HP_ERR_COMM, comm_->error());
+  } else {
+    ++epoch_;
+    FlagBarrier fb;
+    memset(&fb, 0, sizeof fb);
+    fb.G = G_;
+    fb.me = rank_;
+    fb.epoch = epoch_;
+    fb.err = flag_err_;
+    for (int q = 0; q < G_; ++q) fb.flags[q] = (unsigned long long*)(peer_[q] + lay_[q].flag_off);
+    if (int e = launch_flag_barrier(fb, stream_)) return check_cuda(e, "flag barrier");
+  }
+  connected_ = true;
+  if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "connect sync")) return st;
+  if (flag_err_) {
+    int bad = 0;
+    if (int e = cudaMemcpy(&bad, flag_err_, sizeof bad, cudaMemcpyDeviceToHost)) return check_cuda(e, "flag error");
+    if (bad) {
+      sticky_ = HP_ERR_COMM;
+      return fail(HP_ERR_COMM, "connect: a rank did not reach the first flag barrier");
+    }
+  }
+  return HP_OK;
 }
 
 }  // namespace hp

@@ -14,6 +14,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <mutex>
+
 #include "tick_desc.h"
 
 namespace hp {
@@ -684,6 +686,86 @@ int launch_nvls(const NvlsDesc& d, void* stream, int max_blocks) {
   if (u >= 8) return dyn ? launch_nvls_u<8, true>(d, s, max_blocks) : launch_nvls_u<8, false>(d, s, max_blocks);
   if (u <= 2) return dyn ? launch_nvls_u<2, true>(d, s, max_blocks) : launch_nvls_u<2, false>(d, s, max_blocks);
   return dyn ? launch_nvls_u<4, true>(d, s, max_blocks) : launch_nvls_u<4, false>(d, s, max_blocks);
+}
+
+// HP_STRESS (race stress in place of compute-sanitizer):
+// a one-warp kernel that idles for `ns` nanoseconds of %globaltimer, injected
+// on a stream before a launch to perturb the relative timing of streams and
+// ranks. It touches no memory.
+__global__ void spin_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(256);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+// Launch-floor probe (hp_launch_floor): an empty kernel launched like a tick
+// kernel (one CTA of 256 threads, PDL attribute) -- the per-launch cost the
+// latency-bound C1 ticks are compared with.
+__global__ void __launch_bounds__(256) empty_kernel() { cudaGridDependencySynchronize(); }
+
+int launch_empty(void* stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(256);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, empty_kernel);
+}
+
+int launch_spin(unsigned long long ns, void* stream) {
+  spin_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ns);
+  return (int)cudaGetLastError();
+}
+
+// Lazy module loading (the CUDA default) loads a kernel at its first launch,
+// and a load may wait for the context to go idle. A flag barrier spinning on
+// the device for a peer whose producer kernel is being loaded would then
+// deadlock until the barrier's deadline (the CUDA guide's lazy-loading caveat
+// for kernels that wait on each other) -- first seen with co-located ranks on
+// one GPU. So every kernel instance the launchers can pick is loaded up front,
+// once per process (cudaFuncGetAttributes forces the load).
+template <int GM, bool MOM>
+void preload_gm() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, tick_kernel<GM, MOM, 4, true, true>);
+  cudaFuncGetAttributes(&a, tick_kernel<GM, MOM, 4, true, false>);
+  cudaFuncGetAttributes(&a, tick_kernel<GM, MOM, 4, false, true>);
+  cudaFuncGetAttributes(&a, tick_kernel<GM, MOM, 4, false, false>);
+  if constexpr (GM != 3) cudaFuncGetAttributes(&a, tick_kernel_o4<GM, MOM, 2, false, true>);
+  else cudaFuncGetAttributes(&a, tick_kernel<GM, MOM, 2, false, true>);
+  cudaFuncGetAttributes(&a, tick_kernel<GM, MOM, 2, false, false>);
+}
+
+int preload_kernels() {
+  static int err = -1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncAttributes a;
+    preload_gm<0, false>();
+    preload_gm<0, true>();
+    preload_gm<1, false>();
+    preload_gm<1, true>();
+    preload_gm<2, false>();
+    preload_gm<2, true>();
+    preload_gm<3, false>();
+    preload_gm<3, true>();
+    for (auto k : {nvls_kernel<2, true>, nvls_kernel<2, false>, nvls_kernel<4, true>,
+                   nvls_kernel<4, false>, nvls_kernel<8, true>, nvls_kernel<8, false>})
+      cudaFuncGetAttributes(&a, k);
+    cudaFuncGetAttributes(&a, flag_barrier_kernel);
+    cudaFuncGetAttributes(&a, spin_kernel);
+    cudaFuncGetAttributes(&a, empty_kernel);
+    cudaFuncGetAttributes(&a, init_kernel);
+    err = (int)cudaGetLastError();
+  });
+  return err;
 }
 
 int launch_flag_barrier(const FlagBarrier& fb, void* stream) {

@@ -180,6 +180,13 @@ struct FlagBarrier {
   int32_t G, me;
 };
 int launch_flag_barrier(const FlagBarrier& fb, void* stream);
+// Load every kernel instance now (once per process; lazy module loading could
+// otherwise stall a spinning flag barrier). Returns a cudaError_t as int.
+int preload_kernels();
+// hp_launch_floor: an empty one-CTA kernel launched with the PDL attribute.
+int launch_empty(void* stream);
+// HP_STRESS: an idle one-warp kernel of `ns` nanoseconds on `stream`.
+int launch_spin(unsigned long long ns, void* stream);
 
 // Launch the fused tick kernel (kernels.cu). grad_mode: HP_GRAD_*.
 // Returns a cudaError_t as int.

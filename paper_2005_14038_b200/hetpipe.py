@@ -48,7 +48,7 @@ class hp_stats(C.Structure):
                 ("launches", C.c_int64), ("ticks", C.c_int64),
                 ("alg_bytes", C.c_double), ("wait_ticks", C.c_int64 * 8),
                 ("pulls", C.c_int64 * 8), ("nvl_bytes", C.c_double),
-                ("lockstep_batches", C.c_int64)]
+                ("lockstep_batches", C.c_int64), ("apply_batches", C.c_int64)]
 
 
 class hp_unit(C.Structure):
@@ -92,6 +92,11 @@ EXPORTS = {
     "hp_schedule_advance": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
     "hp_run_schedule": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "hp_schedule_set_host_grads": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "hp_schedule_capture": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_void_p)]),
+    "hp_graph_launch": (C.c_int, [C.c_void_p]),
+    "hp_graph_destroy": (None, [C.c_void_p]),
+    "hp_launch_floor": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_float)]),
     "hp_sync": (C.c_int, [C.c_void_p]),
     "hp_read_weights": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]),
     "hp_trace_dump": (C.c_int, [C.c_void_p, C.c_char_p]),
@@ -241,9 +246,12 @@ class Context:
         cb = C.create_string_buffer(comm_id, 128)
         self._chk(self.lib.hp_connect(self.h, hb, cb))
 
-    def connect_symmetric(self, bases: Sequence[int], mc_base: int, comm_id: bytes) -> None:
+    def connect_symmetric(self, bases: Sequence[int], mc_base: int,
+                          comm_id: Optional[bytes]) -> None:
+        """comm_id None: co-located ranks without an NCCL communicator (K7 flag
+        barriers, PEER exchange; include/hetpipe.h hp_connect_symmetric)."""
         arr = (C.c_void_p * len(bases))(*bases)
-        cb = C.create_string_buffer(comm_id, 128)
+        cb = None if comm_id is None else C.create_string_buffer(comm_id, 128)
         self._chk(self.lib.hp_connect_symmetric(self.h, arr, mc_base or None, cb))
 
     def set_tick(self, t: int) -> int:
@@ -268,6 +276,19 @@ class Context:
         self._chk(self.lib.hp_run_schedule(
             self.h, t.ctypes.data_as(C.c_void_p),
             None if l_ is None else l_.ctypes.data_as(C.c_void_p)))
+
+    def schedule_capture(self, target_commits: int) -> "Graph":
+        """hp_schedule_capture: advance the controller now, capture the device
+        work into a CUDA graph; Graph.launch() runs it (once)."""
+        n, g = C.c_int64(), C.c_void_p()
+        self._chk(self.lib.hp_schedule_capture(self.h, target_commits, C.byref(n), C.byref(g)))
+        return Graph(self, g)
+
+    def launch_floor(self, n: int = 1000, graph: bool = False) -> float:
+        """hp_launch_floor: device us per empty launch (direct or in a graph)."""
+        us = C.c_float()
+        self._chk(self.lib.hp_launch_floor(self.h, n, 1 if graph else 0, C.byref(us)))
+        return us.value
 
     def schedule_set_host_grads(self, bufs: Sequence[np.ndarray]) -> None:
         self._host_bufs = list(bufs)
@@ -330,6 +351,27 @@ class Context:
         ms, b, n = C.c_double(), C.c_double(), C.c_int64()
         self._chk(self.lib.hp_profile_read(self.h, C.byref(ms), C.byref(b), C.byref(n)))
         return ms.value, b.value, n.value
+
+
+class Graph:
+    """A captured controller advance (hp_graph); launch() once, then free."""
+
+    def __init__(self, ctx: Context, g: C.c_void_p):
+        self.ctx, self.g = ctx, g
+
+    def launch(self) -> None:
+        self.ctx._chk(self.ctx.lib.hp_graph_launch(self.g))
+
+    def close(self) -> None:
+        if self.g:
+            self.ctx.lib.hp_graph_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _profile_launches(self, max_records: int = 1 << 16):

@@ -113,6 +113,12 @@ int launch_nvls(const NvlsDesc& d, void*, int) {
   return 0;
 }
 
+int preload_kernels() { return 0; }
+int launch_empty(void*) { return 0; }
+
+// HP_STRESS spin: a no-op here (emulated kernels run at launch on the host)
+int launch_spin(unsigned long long, void*) { return 0; }
+
 // K7 flag barrier on host threads (ranks are threads of one process here)
 int launch_flag_barrier(const FlagBarrier& fb, void*) {
   for (int q = 0; q < fb.G; ++q) __atomic_store_n(fb.flags[q] + fb.me, fb.epoch, __ATOMIC_RELEASE);

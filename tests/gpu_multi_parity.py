@@ -6,37 +6,22 @@ Prints 'MULTI-GPU PARITY OK' on success, exits 1 otherwise."""
 import os
 import random
 import sys
-import tempfile
 
-import numpy as np
+
 import torch
 import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from oracle import run_schedule  # noqa: E402
 from paper_2005_14038_b200 import dist as hdist  # noqa: E402
+from placement_check import check, collect, host_gradients  # noqa: E402
 from workloads import (C3, C4, C5, C5E, GRAD_DYADIC, WSPConfig, ceil_shards,  # noqa: E402
                        sample_indices, even_shards)
 
 from workloads import models as M  # noqa: E402
 
 XPORT = {"peer": 0, "nccl": 1, "nvls": 2}
-
-
-def host_gradients(cfg):
-    """EXTERNAL mode: the VWs' whole gradients as host buffers, filled with the
-    same Philox values the synthetic mode draws (oracle.gradient)."""
-    from oracle import gradient
-    idx = np.arange(cfg.nparams)
-    last_p = cfg.waves * cfg.Nm
-    n = cfg.num_vw * last_p + 1
-    bufs = [np.zeros(cfg.nparams, dtype=np.float32) for _ in range(n)]
-    for v in range(cfg.num_vw):
-        for p in range(1, last_p + 1):
-            bufs[(v * last_p + p) % n][:] = gradient(idx, v, p, cfg)
-    return bufs
 
 
 def run(cfg, G, k, rank, local, sampled, transport="peer", bounds=None, external=False):
@@ -53,71 +38,14 @@ def run(cfg, G, k, rank, local, sampled, transport="peer", bounds=None, external
         ctx = hdist.placed_context(cfg, rank, G, k, device=local, stream=stream.cuda_stream,
                                    transport=XPORT[transport], **extra)
     if external:
-        bufs = host_gradients(cfg)
-        ctx.schedule_set_host_grads(bufs)
+        ctx.schedule_set_host_grads(host_gradients(cfg))
     ctx.run_schedule(cfg.tau, cfg.latency())
-    with tempfile.NamedTemporaryFile(suffix=".trace") as f:
-        tr = ctx.trace_lines(f.name)
-    wg = ctx.read_weights(-1)
-    m = ctx.read_weights(-2) if cfg.momentum else None
-    wl = {}
-    for v in range(cfg.num_vw):
-        if any((v * k + j) % G == rank for j in range(k)):
-            wl[v] = ctx.read_weights(v)
-    nvl = ctx.stats().nvl_bytes
-    lock = ctx.stats().lockstep_batches
+    res = collect(ctx, cfg, G, k, rank, sampled, bounds)
     ctx.close()
     del keep
-    if sampled is not None:      # ship only sampled entries (full arrays are GBs)
-        sb = bounds or even_shards(cfg.nparams, G)
-        lo = sb[rank]
-        wg = {int(i): float(wg[i - lo]) for i in sampled if sb[rank] <= i < sb[rank + 1]}
-        m = None if m is None else {int(i): float(m[i - lo]) for i in sampled if sb[rank] <= i < sb[rank + 1]}
-        st = even_shards(cfg.nparams, k)
-        wl2 = {}
-        for v, arr in wl.items():
-            j = [j for j in range(k) if (v * k + j) % G == rank][0]
-            wl2[v] = {int(i): float(arr[i - st[j]]) for i in sampled if st[j] <= i < st[j + 1]}
-        wl = wl2
     objs = [None] * G
-    dist.all_gather_object(objs, (tr, wg, m, wl, nvl, lock))
+    dist.all_gather_object(objs, res)
     return objs
-
-
-def normwise(a, b):
-    a = np.asarray(a, dtype=np.float64)
-    b = np.asarray(b, dtype=np.float64)
-    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
-
-
-def check(cfg, G, k, objs, sampled, exact=True):
-    """exact: bit-identical arrays (commit-order applies); otherwise reading
-    Z15's normwise bound 1e-5 per buffer (NCCL / NVLS sum a lockstep wave's N
-    updates in their own order before the single apply)."""
-    eq = (lambda a, b: np.array_equal(a, b)) if exact else (lambda a, b: normwise(a, b) <= 1e-5)
-    o = run_schedule(cfg, idx=None if sampled is None else np.array(sampled))
-    for r in range(G):
-        assert objs[r][0] == o.trace, f"trace of rank {r}"
-    if sampled is None:
-        assert eq(np.concatenate([objs[r][1] for r in range(G)]), o.wg)
-        if cfg.momentum:
-            assert eq(np.concatenate([objs[r][2] for r in range(G)]), o.m)
-        for v in range(cfg.num_vw):
-            parts = [objs[(v * k + j) % G][3][v] for j in range(k)]
-            assert eq(np.concatenate(parts), o.wl[v]), f"w_local({v})"
-    else:
-        pos = {int(i): n for n, i in enumerate(sampled)}
-        wg = {}
-        for r in range(G):
-            wg.update(objs[r][1])
-        assert eq(np.array([wg[i] for i in sampled], dtype=np.float32), o.wg)
-        for v in range(cfg.num_vw):
-            wl = {}
-            for j in range(k):
-                wl.update(objs[(v * k + j) % G][3][v])
-            assert eq(np.array([wl[i] for i in sampled], dtype=np.float32), o.wl[v]), f"w_local({v})"
-    nvl = sum(objs[r][4] for r in range(G))
-    assert (nvl == 0) == (k == G), nvl
 
 
 def main():

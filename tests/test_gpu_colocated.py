@@ -1,0 +1,190 @@
+"""Distributed placements on ONE B200: G ranks as G threads of this process,
+each driving its own context (its own arena, streams and replicated
+controller), connected through hp_connect_symmetric WITHOUT an NCCL
+communicator (include/hetpipe.h: comm_id NULL -> K7 device flag barriers,
+PEER exchange). The exchange code is the multi-GPU one -- the PS shard owner's
+apply launch loads the pushed u~ slices from the other ranks' arenas, the
+owner-side pull stores w_global into the pullers' w_local, the a9 stream /
+event DAG (accumulation streams, exchange stream, fold streams) -- only the
+"peer" memory sits in the same HBM. So a 1-GPU box verifies rows a4 / a7 / a9
+of the distributed engine bit-exact against the oracle (PAPER.md P:920-930
+push/apply, P:949-951 pull and the pipeline running while a VW waits).
+
+HP_STRESS injects random idle kernels before launches and barriers on every
+stream of every rank (race stress in place of compute-sanitizer, SURVEY.md
+section 5); the results must stay bit-exact."""
+import os
+import random
+
+import pytest
+
+from placement_check import check, host_gradients, run_colocated
+from workloads import (C3, C5, GRAD_CONVEX, GRAD_EXTERNAL, WSPConfig, even_shards,
+                       sample_indices)
+from workloads import models as M
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2005_14038_b200 import build, hetpipe
+    build.build()
+    hetpipe.load()
+    return hetpipe
+
+
+def dev_alloc(nbytes):
+    import torch
+    t = torch.empty(max(nbytes, 256), dtype=torch.uint8, device="cuda:0")
+    assert t.data_ptr() % 256 == 0
+    return t.data_ptr(), t
+
+
+def run(hp, cfg, G, k, sampled=None, bounds=None, **over):
+    return run_colocated(hp, cfg, G, k, dev_alloc, sampled=sampled, bounds=bounds, **over)
+
+
+def sampled_of(cfg, G, bounds=None):
+    return sample_indices(cfg.nparams, 104729, bounds or even_shards(cfg.nparams, G))
+
+
+# (id, cfg, G, k, sampled, environment knobs)
+CASES = [
+    # BASELINE configs[2] (C3: ResNet-152 size, HD speeds, D = 4) at full size
+    ("C3-full-G4-k1", C3.replace(waves=3), 4, 1, True, {}),
+    ("C3-full-G4-k2", C3.replace(waves=3), 4, 2, True, {}),
+    ("C3-full-G2-k1", C3.replace(waves=3), 2, 1, True, {}),
+    # configs[4] (C5: VGG-19 size, 8 VWs, heavy-ball momentum) at full size, 2 VWs per rank
+    ("C5-full-G4-mom", C5.replace(waves=2, D=4), 4, 1, True, {}),
+    ("C3-G4-k1", C3.replace(nparams=40_000, waves=8), 4, 1, False, {}),
+    ("C3-G4-k2-mom", C3.replace(nparams=40_003, waves=8, momentum=0.9), 4, 2, False, {}),
+    ("lazy-atleast-G3", WSPConfig("lazy", 3, 3, 1, 12_345, 7, (3, 5, 4), pull_policy=1,
+                                  local_semantics=1), 3, 1, False, {}),
+    ("convexF2-G3", WSPConfig("cf", 3, 2, 1, 20_011, 5, (3, 5, 4), grad_mode=GRAD_CONVEX,
+                              lr=0.05, F=2), 3, 1, False, {}),
+    ("convex-G4-k2", C3.replace(nparams=20_000, waves=5, grad_mode=GRAD_CONVEX, lr=0.05),
+     4, 2, False, {}),
+    ("F2-strict-G2", WSPConfig("f2", 3, 2, 1, 33_333, 5, (3, 7, 4), F=2), 2, 1, False, {}),
+    # reader-side pulls everywhere (HP_PULL_PUSH=0) and split acc / fold launches
+    # (HP_SPLIT_FOLDS=1, incl. F = 2 STRICT whose pull reads the open clock's
+    # aggregate while later completes join it: ADVICE round 1)
+    ("C3-G4-pull-reader", C3.replace(nparams=40_000, waves=6), 4, 1, False, {"HP_PULL_PUSH": "0"}),
+    ("C3-G4-split", C3.replace(nparams=40_000, waves=6), 4, 1, False, {"HP_SPLIT_FOLDS": "1"}),
+    ("F2-split-G2", WSPConfig("f2s", 3, 2, 1, 33_333, 5, (3, 7, 4), F=2), 2, 1, False,
+     {"HP_SPLIT_FOLDS": "1"}),
+    ("F2-split-G3-k2", WSPConfig("f2s3", 4, 2, 2, 20_000, 5, (3, 7, 4, 5), F=2), 3, 2, False,
+     {"HP_SPLIT_FOLDS": "1"}),
+    ("lazy-split-G2", WSPConfig("ls", 3, 3, 1, 12_345, 7, (3, 5, 4), pull_policy=1,
+                                local_semantics=1), 2, 1, False, {"HP_SPLIT_FOLDS": "1"}),
+    # bounded exchange / accumulation grids (co-scheduling knobs of DESIGN 9f)
+    ("C3-G4-grids", C3.replace(nparams=40_000, waves=6), 4, 1, False,
+     {"HP_XBLOCKS": "80", "HP_ABLOCKS": "216"}),
+]
+
+
+@pytest.mark.parametrize("name,cfg,G,k,sampled,env", CASES, ids=[c[0] for c in CASES])
+def test_colocated_parity(hp, monkeypatch, name, cfg, G, k, sampled, env):
+    assert streams_needed(cfg.num_vw, G, k, "HP_SPLIT_FOLDS" in env) <= 30
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    smp = sampled_of(cfg, G) if sampled else None
+    out = run(hp, cfg, G, k, sampled=smp)
+    check(cfg, G, k, out, smp)
+
+
+def test_colocated_layer_rr_bounds(hp):
+    """The paper's default PS placement, layers round-robin over the servers
+    (P:100-103): VGG-19's fc6 puts most of the model on one shard (uneven
+    hp_config.ps_bounds), full size, momentum."""
+    G = 4
+    cfg = C5.replace(waves=2, D=4, num_vw=G, tau=C5.tau[:G])
+    bounds = M.layer_rr_bounds(M.vgg19(), G)
+    smp = sampled_of(cfg, G, bounds)
+    out = run(hp, cfg, G, 1, sampled=smp, bounds=bounds)
+    check(cfg, G, 1, out, smp)
+
+
+@pytest.mark.parametrize("G,k", [(2, 1), (4, 2)])
+def test_colocated_external_host_gradients(hp, G, k):
+    """EXTERNAL: the caller's host gradients; every rank copies its stages of
+    the VWs' whole gradients on the VW's accumulation stream."""
+    import torch
+    cfg = C3.replace(nparams=20_000, waves=4, D=1)
+    # pinned buffers: a pageable cudaMemcpyAsync blocks its host thread until
+    # the stream drains, holding the process's shared staging buffer -- with
+    # co-located ranks one rank's copy could then wait on a flag barrier that
+    # needs another rank's copy (separate processes have separate staging)
+    pinned = [torch.from_numpy(b).pin_memory() for b in host_gradients(cfg)]
+    out = run(hp, cfg, G, k, grad_mode=GRAD_EXTERNAL, host_grads=[t.numpy() for t in pinned])
+    check(cfg, G, k, out)
+
+
+def streams_needed(N, G, k, split):
+    """CUDA streams the G co-located contexts create: per rank the context
+    stream, the exchange stream and one accumulation stream per local VW (+ one
+    fold stream each under HP_SPLIT_FOLDS). Kept <= 30 so that, with
+    CUDA_DEVICE_MAX_CONNECTIONS=32 (tests/conftest.py), no two streams share a
+    hardware queue: a rank's spinning flag barrier must never sit in front of
+    another rank's producer in one queue (on separate GPUs that cannot occur)."""
+    tot = 0
+    for r in range(G):
+        loc = sum(1 for v in range(N) if any((v * k + j) % G == r for j in range(k)))
+        tot += 2 + loc * (2 if split else 1)
+    return tot
+
+
+def _random_case(seed):
+    rng = random.Random(seed)
+    while True:
+        case = _draw_case(rng)
+        cfg, G, k, _, env = case
+        if streams_needed(cfg.num_vw, G, k, "HP_SPLIT_FOLDS" in env) <= 30:
+            return case
+
+
+def _draw_case(rng):
+    G = rng.choice([2, 3, 4])
+    N = rng.randint(1, 6)
+    Nm = rng.randint(1, 4)
+    tau = tuple(rng.randint(1, 9) for _ in range(N))
+    k = rng.randint(1, G)
+    convex = rng.random() < 0.3
+    cfg = WSPConfig("rnd", N, Nm, rng.randint(0, 3), rng.choice([4099, 20_000, 33_333]),
+                    rng.randint(2, 6), tau, momentum=rng.choice([0.0, 0.9]),
+                    pull_policy=rng.choice([0, 1]), local_semantics=rng.choice([0, 1]),
+                    lat=tuple(t * rng.randint(1, Nm + 1) for t in tau),
+                    grad_mode=GRAD_CONVEX if convex else 0, lr=0.05 if convex else 0.01,
+                    F=rng.choice([1, 1, 2]))
+    over = dict(merge_ticks=rng.randint(0, 1), acc_slots=rng.choice([2, 3]),
+                apply_mode=rng.randint(0, 1))
+    env = {}
+    if rng.random() < 0.3:
+        env["HP_SPLIT_FOLDS"] = "1"
+    if rng.random() < 0.3:
+        env["HP_PULL_PUSH"] = "0"
+    return cfg, G, k, over, env
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_colocated_random(hp, monkeypatch, seed):
+    cfg, G, k, over, env = _random_case(1000 + seed)
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    out = run(hp, cfg, G, k, **over)
+    check(cfg, G, k, out)
+
+
+@pytest.mark.parametrize("seed", range(1, 51))
+def test_colocated_stress(hp, monkeypatch, seed):
+    """HP_STRESS=seed: random 0..50 us idle kernels before half the launches and
+    barriers of every stream of every rank; results stay bit-exact."""
+    cfg, G, k, over, env = _random_case(5000 + seed)
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    monkeypatch.setenv("HP_STRESS", str(seed))
+    out = run(hp, cfg.replace(nparams=min(cfg.nparams, 20_000)), G, k, **over)
+    check(cfg.replace(nparams=min(cfg.nparams, 20_000)), G, k, out)
