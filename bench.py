@@ -655,14 +655,16 @@ def main():
             "launches_per_tick": res["launches"] / max(res["ticks"], 1),
             "us_per_launch": 1e3 * res["ms_max"] / max(res["launches"], 1),
             "launch_floor_us": {"graph": floor_graph, "direct": floor_direct},
-            "ratio_to_floor": (1e3 * res["ms_max"] / max(res["launches"], 1)) / floor_graph
-            if graph else (1e3 * res["ms_max"] / max(res["launches"], 1)) / floor_direct,
+            "ratio_to_floor": (1e3 * res["ms_max"] / max(res["ticks"], 1)) /
+                              (floor_graph if graph else floor_direct),
             "issued_directly": {"tick_us": 1e3 * direct["ms_max"] / max(direct["ticks"], 1),
                                 "value": direct["value"],
                                 "us_per_launch": 1e3 * direct["ms_max"] / max(direct["launches"], 1)},
             "def": "device time of the timed rounds / controller ticks; floor = empty one-CTA "
                    "kernels back to back on the same stream (hp_launch_floor), in a graph and "
-                   "issued directly"}
+                   "issued directly; ratio_to_floor = tick_us / the floor of the same issue "
+                   "mode (captured ticks of a small context run through the multi-tick kernel, "
+                   "hp_schedule_capture)"}
 
     # ---- N>1: the ED-local C2 placement and the same config on one GPU
     extras = {}

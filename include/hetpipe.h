@@ -88,6 +88,8 @@ enum { HP_APPLY_DEFERRED = 0, HP_APPLY_ON_ARRIVAL = 1 };
    they match the sequential commit-order apply within rounding (reading Z15,
    normwise <= 1e-5), not bit-exactly; the trace is identical. */
 enum { HP_XPORT_PEER = 0, HP_XPORT_NCCL = 1, HP_XPORT_NVLS = 2 };
+/* hp_config.lr_schedule */
+enum { HP_LR_CONSTANT = 0, HP_LR_THEOREM1 = 1 };
 
 typedef struct {
   int32_t num_vw;          /* N virtual workers, 1..8 */
@@ -123,7 +125,12 @@ typedef struct {
                               aggregates and pushes F*Nm minibatches per clock, its gated
                               STARTs are (c+2)*F*Nm, s_global = F(D+2)Nm - 2; `waves`
                               counts clocks. Default 1 */
-  int32_t reserved2;
+  int32_t lr_schedule;     /* HP_LR_CONSTANT (default): u = fl(-lr * g). HP_LR_THEOREM1:
+                              u(v,p) = fl(-eta_t * g) with eta_t = fl(lr / fl(sqrt(t))),
+                              t = (p-1)*num_vw + v + 1 -- Theorem 1's schedule
+                              eta_t = sigma/sqrt(t) with lr = sigma, the
+                              updates numbered worker-fastest (reading Z26); needs
+                              num_vw * waves * F * N_m < 2^24 */
   float conv_a;            /* HP_GRAD_CONVEX curvature a (default 0.5) */
   float conv_sigma;        /* HP_GRAD_CONVEX noise scale sigma (default 1.0) */
   const int64_t* ps_bounds;/* optional PS shard boundaries (world > 1): world+1 values,
@@ -249,13 +256,12 @@ hp_status hp_schedule_begin(hp_ctx* ctx, const int64_t* tau, const int64_t* lat)
 /* Run ticks until the commit log holds >= target_commits pushes or the run is
    complete; *commits (may be NULL) receives the count reached. */
 hp_status hp_schedule_advance(hp_ctx* ctx, int64_t target_commits, int64_t* commits);
-/* CUDA-graph form of hp_schedule_advance, for launch-bound (small) models:
+/* CUDA-graph form of hp_schedule_advance, for launch-bound (small) models on
+   single-rank contexts (world = 1; a distributed context gets HP_ERR_STATE):
    the controller advances to target_commits NOW on the host (protocol state,
    trace, stats move exactly as hp_schedule_advance), but the device work of
-   those ticks -- every fused tick launch, and in distributed contexts the
-   side-stream launches and flag barriers, forked from and joined back to the
-   context stream -- is captured into one CUDA graph (stream capture of the
-   context stream, relaxed mode) instead of running. hp_graph_launch then runs
+   those ticks -- every fused tick launch -- is captured into one CUDA graph
+   (stream capture of the context stream, relaxed mode) instead of running. hp_graph_launch then runs
    it ONCE on the context stream (a graph holds those ticks' descriptors; a
    second launch would redo them, so it is refused: HP_ERR_STATE). Until that
    launch, do not read weights or capture again (HP_ERR_STATE). Not allowed with
@@ -310,6 +316,9 @@ typedef struct {
   int64_t apply_batches;    /* PS apply batches (flushes that applied >= 1 push):
                                pushes / apply_batches = the k of SURVEY.md 8(d)'s
                                byte model 16*F*Nm per push + 8(1+[mu]) per batch */
+  int64_t desc_splits;      /* extra launches because a tick descriptor table
+                               (kMaxC/A/G/F/S, tick_desc.h) was full, plus owner-side
+                               pulls refused for more than kMaxP targets */
 } hp_stats;
 hp_status hp_get_stats(hp_ctx* ctx, hp_stats* out);
 

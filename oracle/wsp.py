@@ -126,10 +126,22 @@ def initial_weights(idx: np.ndarray, cfg: WSPConfig) -> np.ndarray:
     return (2.0 * ((x >> 8).astype(np.float64) * 2.0 ** -24) - 1.0).astype(F32)
 
 
+def step_size(vw: int, p: int, cfg: WSPConfig) -> np.float32:
+    """eta of minibatch p of VW vw: the constant lr (Z2), or Theorem 1's
+    schedule eta_t = sigma / sqrt(t) (App. A)
+    with sigma = cfg.lr and the updates numbered worker-fastest,
+    t = (p - 1) * N + vw + 1 (the loop "over the workers (t mod N)" of P:1516-1520;
+    reading Z26). float32: fl(sigma / fl(sqrt(t))), t exact."""
+    if getattr(cfg, "lr_schedule", 0) == 0:
+        return F32(cfg.lr)
+    t = F32((p - 1) * cfg.num_vw + vw + 1)
+    return F32(cfg.lr) / np.sqrt(t)
+
+
 def update(idx: np.ndarray, vw: int, p: int, cfg: WSPConfig,
            w: Optional[np.ndarray] = None) -> np.ndarray:
-    """u_p = fl(-lr * g_p): one float32 rounding (Z2, Z10)."""
-    return F32(-cfg.lr) * gradient(idx, vw, p, cfg, w)
+    """u_p = fl(-eta * g_p): one float32 rounding (Z2, Z10); eta = step_size."""
+    return (-step_size(vw, p, cfg)) * gradient(idx, vw, p, cfg, w)
 
 
 # --------------------------------------------------------------------------- #

@@ -118,6 +118,8 @@ struct hp_graph {
   hp_ctx* ctx = nullptr;
   cudaGraphExec_t exec = nullptr;
   bool launched = false;
+  std::vector<void*> bufs;            // multi-tick descriptor buffers the graph reads
+  cudaEvent_t done = nullptr;         // recorded after the launch
 };
 
 namespace {
@@ -209,6 +211,10 @@ const char* validate(hp_config& cfg) {
 
   else if (cfg.transport < 0 || cfg.transport > 2) bad = "bad transport";
   else if (cfg.update_freq < 1 || cfg.update_freq > 64) bad = "update_freq must be 1..64";
+  else if (cfg.lr_schedule < 0 || cfg.lr_schedule > 1) bad = "bad lr_schedule";
+  else if (cfg.lr_schedule == HP_LR_THEOREM1 &&
+           (int64_t)cfg.num_vw * cfg.waves * cfg.update_freq * cfg.Nm >= (1ll << 24))
+    bad = "lr_schedule THEOREM1 needs num_vw * waves * F * Nm < 2^24 (t exact in fp32)";
 
   if (!bad && cfg.world > 1 && cfg.ps_bounds) {
     const int64_t* b = cfg.ps_bounds;
@@ -390,6 +396,7 @@ hp_status hp_schedule_capture(hp_ctx* ctx, int64_t target, int64_t* commits, hp_
   hp_graph* g = new hp_graph;
   g->ctx = ctx;
   g->exec = exec;
+  g->bufs = ctx->eng->take_graph_bufs();
   *out = g;
   return HP_OK;
   HP_EXIT(ctx)
@@ -401,7 +408,12 @@ hp_status hp_graph_launch(hp_graph* g) {
   HP_ENTRY(ctx)
   if (g->launched) return ctx->eng->fail(HP_ERR_STATE, "graph already launched");
   g->launched = true;
-  return ctx->eng->graph_launch(g->exec);
+  if (hp_status st = ctx->eng->graph_launch(g->exec)) return st;
+  if (!g->bufs.empty()) {           // the buffers live until the graph has run
+    cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming);
+    cudaEventRecord(g->done, (cudaStream_t)ctx->eng->stream());
+  }
+  return HP_OK;
   HP_EXIT(ctx)
 }
 
@@ -413,6 +425,11 @@ hp_status hp_launch_floor(hp_ctx* ctx, int32_t n, int32_t graph, float* us_per_l
 
 void hp_graph_destroy(hp_graph* g) {
   if (!g) return;
+  if (g->done) {
+    cudaEventSynchronize(g->done);
+    cudaEventDestroy(g->done);
+  }
+  for (void* b : g->bufs) cudaFree(b);
   if (g->exec) cudaGraphExecDestroy(g->exec);
   delete g;
 }

@@ -3,6 +3,7 @@
 // it completes on a rank only after every rank's stream reached it, which is
 // the device-side barrier the distributed flush needs.
 #include <dlfcn.h>
+#include <cstdlib>
 
 #include <cstring>
 #include <string>
@@ -42,14 +43,12 @@ Api* api(std::string* err) {
     return a.h ? &a : nullptr;
   }
   tried = true;
-  const char* names[] = {
-      "libnccl.so.2",
-      "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
-      "/usr/lib/x86_64-linux-gnu/libnccl.so.2"};
-  for (const char* n : names) {
-    a.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
-    if (a.h) break;
-  }
+  // the NCCL the process already has (torch loads its own), else $HP_NCCL_LIB
+  // (the binding points it at torch's bundled copy), else the loader's search
+  a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!a.h)
+    if (const char* env = getenv("HP_NCCL_LIB")) a.h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  if (!a.h) a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!a.h) {
     if (err) *err = "libnccl.so.2 not loadable";
     return nullptr;

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 
 namespace hp {
@@ -120,6 +121,8 @@ RankLayout Engine::layout_of(int q) const {
 
 Engine::~Engine() {
   delete comm_;
+  for (void* b : graph_bufs_) cudaFree(b);
+  if (up_) cudaStreamDestroy(up_);
   if (flag_err_) cudaFree(flag_err_);
   if (tiles_) cudaFree(tiles_);
   for (auto e : evpool_) cudaEventDestroy(e);
@@ -173,6 +176,15 @@ hp_status Engine::init() {
   } else {
     if (int e = cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking)) return check_cuda(e, "stream");
     own_stream_ = true;
+  }
+  {
+    // small single-rank contexts run a capture's ticks through the multi-tick
+    // kernel (HP_TICK_BATCH=0 disables; HP_TICK_BATCH_MAX_N: largest n)
+    const char* tb = getenv("HP_TICK_BATCH");
+    const char* tn = getenv("HP_TICK_BATCH_MAX_N");
+    const int64_t max_n = tn ? atoll(tn) : (1 << 16);
+    batch_ok_ = (!tb || atoi(tb) != 0) && cfg_.world <= 1 && cfg_.grad_mode != HP_GRAD_EXTERNAL &&
+                cfg_.param_count > 0 && cfg_.param_count <= max_n;
   }
   if (const char* sv = getenv("HP_STRESS")) {
     const uint64_t seed = strtoull(sv, nullptr, 10);
@@ -279,7 +291,17 @@ void Engine::fill_fold(DFold& f, int v, int64_t x) const {
   f.p = (uint32_t)q;
   f.op = x > 0 ? 0u : 1u;
   f.grad = x > 0 ? fold_grad(v, q) : nullptr;
+  f.neg_lr = neg_lr_of(v, q);
   f.stash = convex_ ? vw_[v].stash[(q - 1) % Nm_] : nullptr;
+}
+
+float Engine::neg_lr_of(int v, int64_t p) const {
+  if (cfg_.lr_schedule == HP_LR_CONSTANT) return -cfg_.lr;
+  // eta_t = sigma / sqrt(t) (Theorem 1): fl(sqrt) and
+  // fl(/) are correctly rounded IEEE ops, t < 2^24 is exact in fp32; negation
+  // is exact
+  const float t = (float)((p - 1) * (int64_t)N_ + v + 1);
+  return -(cfg_.lr / sqrtf(t));
 }
 
 const float* Engine::fold_grad(int v, int64_t p) const {
@@ -307,6 +329,7 @@ hp_status Engine::complete(int v, int64_t p, const float* grad_dev, const float*
   for (auto& b : bc_) again |= b.v == v;
   if (convex_)
     for (int64_t q : s.pending_folds) again |= q < 0;
+  if ((int)bc_.size() >= kMaxC && !again) desc_splits_++;
   if (again || (int)bc_.size() >= kMaxC)
     if (hp_status st = flush()) return st;
   const int64_t c = wave_of(p, U_);            // the clock p belongs to (F waves)
@@ -615,11 +638,19 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   static const int dyn_env = getenv("HP_DYN") ? atoi(getenv("HP_DYN")) : 1;
   static const int dyn_min = getenv("HP_DYN_MINLOADS") ? atoi(getenv("HP_DYN_MINLOADS")) : 2;
   static const int dyn_pulls = getenv("HP_DYN_PULLS") ? atoi(getenv("HP_DYN_PULLS")) : 1;
-  static const int64_t dyn_n = getenv("HP_DYN_MIN_N") ? atoll(getenv("HP_DYN_MIN_N")) : 0;
+  // (small launches take the static grid: a tile claim is a chain of L2
+  // atomics that costs more than a 4096-param tick, C1)
+  static const int64_t dyn_n = getenv("HP_DYN_MIN_N") ? atoll(getenv("HP_DYN_MIN_N")) : (1 << 20);
   d.ctr = nullptr;
   d.done = nullptr;
   if (dyn_env && loads >= dyn_min && n >= dyn_n && (dyn_pulls || d.ng == 0))
     tile_slot(st, &d.ctr, &d.done);
+  if (capturing_ && batch_ok_ && st == stream_) {
+    batch_.push_back(d);
+    alg_bytes_ += bytes;
+    if (batch_.size() >= kTickBatch) return flush_batch();
+    return HP_OK;
+  }
   stress(st);
   prof_begin(st);
   int err = launch_tick(d, cfg_.grad_mode, m_ != nullptr, st, max_blocks);
@@ -825,6 +856,7 @@ hp_status Engine::flush_local() {
     c.v = (uint32_t)b.v;
     c.p = (uint32_t)b.p;
     c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc | (b.snap ? kSnapAcc : 0u);
+    c.neg_lr = neg_lr_of(b.v, b.p);
   }
   // 2. applies in commit order. The longest suffix whose waves were completed
   //    in this batch, in complete order, is applied straight from registers in
@@ -862,6 +894,7 @@ hp_status Engine::flush_local() {
   }
   size_t a0 = 0;
   while (reg_from - a0 > (size_t)kMaxA) {
+    desc_splits_++;
     TickDesc pre;
     memset(&pre, 0, sizeof pre);
     for (int k = 0; k < kMaxA; ++k, ++a0) {
@@ -905,6 +938,7 @@ hp_status Engine::flush_local() {
     size_t fi = 0;
     do {  // split a group whose folds overflow the descriptor
       if (d.ng == kMaxG || d.nf == kMaxF) {
+        desc_splits_++;
         if (hp_status st = emit(d, begin_, n_)) return st;
         memset(&d, 0, sizeof d);
       }
@@ -992,6 +1026,10 @@ hp_status Engine::capture_begin() {
   if (sticky_) return sticky_;
   if (capturing_ || graph_pending_) return fail(HP_ERR_STATE, "a captured graph has not been launched");
   if (prof_on_) return fail(HP_ERR_STATE, "per-launch profiling is on: cannot capture");
+  // (distributed contexts: a captured flag barrier would spin inside a graph
+  // whose concurrency with the peers' work CUDA does not promise; they issue
+  // their exchange directly)
+  if (dist_) return fail(HP_ERR_STATE, "graph capture is for single-rank contexts");
   // earlier host-queued device work belongs to the stream before the graph
   if (hp_status st = flush_pending()) return st;
   if (int e = cudaStreamBeginCapture(stream_, cudaStreamCaptureModeRelaxed))
@@ -1002,6 +1040,9 @@ hp_status Engine::capture_begin() {
 
 hp_status Engine::capture_end(bool ok, cudaGraphExec_t* exec) {
   if (!capturing_) return fail(HP_ERR_STATE, "not capturing");
+  if (ok && !batch_.empty())
+    if (flush_batch() != HP_OK) ok = false;
+  batch_.clear();
   capturing_ = false;
   cudaGraph_t g = nullptr;
   const int e = cudaStreamEndCapture(stream_, &g);
@@ -1018,6 +1059,30 @@ hp_status Engine::capture_end(bool ok, cudaGraphExec_t* exec) {
   if (e2) return check_cuda(e2, "cudaGraphInstantiate");
   graph_pending_ = true;
   return HP_OK;
+}
+
+// One multi-tick launch for the descriptors collected during a capture: they
+// are uploaded now (synchronously, on a stream that is not captured) into a
+// device buffer the graph owns, and the launch is recorded into the graph.
+hp_status Engine::flush_batch() {
+  if (batch_.empty()) return HP_OK;
+  const size_t bytes = batch_.size() * sizeof(TickDesc);
+  void* dev = nullptr;
+  if (cudaMalloc(&dev, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(HP_ERR_OOM, "tick batch allocation failed");
+  }
+  graph_bufs_.push_back(dev);
+  if (!up_)
+    if (int e = cudaStreamCreateWithFlags(&up_, cudaStreamNonBlocking)) return check_cuda(e, "stream");
+  if (int e = cudaMemcpyAsync(dev, batch_.data(), bytes, cudaMemcpyHostToDevice, up_))
+    return check_cuda(e, "tick batch upload");
+  if (int e = cudaStreamSynchronize(up_)) return check_cuda(e, "tick batch upload");
+  const int err = launch_multi_tick((const TickDesc*)dev, (int)batch_.size(), n_, cfg_.grad_mode,
+                                    m_ != nullptr, stream_);
+  launches_++;
+  batch_.clear();
+  return check_cuda(err, "multi-tick kernel");
 }
 
 hp_status Engine::graph_launch(cudaGraphExec_t exec) {
@@ -1094,6 +1159,7 @@ void Engine::stats(hp_stats* out) const {
   out->nvl_bytes = nvl_bytes_;
   out->lockstep_batches = lockstep_batches_;
   out->apply_batches = apply_batches_;
+  out->desc_splits = desc_splits_;
 }
 
 hp_status Engine::profile_enable(bool on) {

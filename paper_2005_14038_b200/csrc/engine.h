@@ -96,6 +96,7 @@ class Engine {
   hp_status capture_end(bool ok, cudaGraphExec_t* exec);
   hp_status graph_launch(cudaGraphExec_t exec);
   bool graph_pending() const { return graph_pending_; }
+  void* stream() const { return stream_; }
   hp_status launch_floor(int n, bool graph, float* us);
 
   void set_tick(int64_t t) { tick_ = t; }
@@ -165,6 +166,9 @@ class Engine {
   void rec(char phase, int v, const char* kind, int64_t p, int64_t c);
   std::pair<bool, bool> gate_open(int v) const;
   const float* fold_grad(int v, int64_t p) const;
+  // -eta of u(v, p): -lr, or Theorem 1's -sigma/sqrt(t) with t = (p-1)*N + v + 1
+  // (hp_config.lr_schedule, reading Z26)
+  float neg_lr_of(int v, int64_t p) const;
   // one w_local op of VW v from its pending list: x > 0 FOLD u_x, x < 0 STASH
   // for START(-x) (CONVEX); sets the stash slot / EXTERNAL gradient it reads
   void fill_fold(DFold& f, int v, int64_t x) const;
@@ -228,8 +232,20 @@ class Engine {
   double nvl_bytes_ = 0;
   int64_t lockstep_batches_ = 0;
   bool capturing_ = false;            // stream capture of stream_ in progress
+  // Multi-tick batching while capturing a small single-rank context
+  // (launch_multi_tick): the captured ticks' descriptors are collected and run
+  // by one multi-tick kernel per batch; their device copies belong to the graph.
+  bool batch_ok_ = false;             // context qualifies (set at init)
+  std::vector<TickDesc> batch_;
+  std::vector<void*> graph_bufs_;     // descriptor buffers of the capture in progress
+  cudaStream_t up_ = nullptr;         // upload stream (never captured)
+  hp_status flush_batch();
+ public:
+  std::vector<void*> take_graph_bufs() { std::vector<void*> b; b.swap(graph_bufs_); return b; }
+ private:
   bool graph_pending_ = false;        // a captured graph awaits its launch
   int64_t apply_batches_ = 0;
+  int64_t desc_splits_ = 0;           // launches split because a descriptor table was full
   int N_, Nm_, R_;
   int64_t U_ = 1;                     // minibatches per clock: F * Nm (NEXT-4)
   bool convex_ = false;               // HP_GRAD_CONVEX: stash ring + STASH ops

@@ -70,6 +70,7 @@ hp_status Engine::dist_accumulate(const std::vector<bool>& pulled) {
       c.v = (uint32_t)b.v;
       c.p = (uint32_t)b.p;
       c.flags = (b.first ? kFirst : kLoadAcc) | kStoreAcc | (b.snap ? kSnapAcc : 0u);
+      c.neg_lr = neg_lr_of(b.v, b.p);
     }
     const bool hold = strict && s.at_gate;
     std::vector<int64_t> folds;
@@ -109,6 +110,7 @@ hp_status Engine::dist_accumulate(const std::vector<bool>& pulled) {
     size_t fi = 0;
     while (fi < folds.size()) {
       if (d.ng == kMaxG || d.nf == kMaxF) {
+        desc_splits_++;
         if (hp_status st = emit(d, s.a0, s.len, fst, ablocks_)) return st;
         memset(&d, 0, sizeof d);
       }
@@ -168,9 +170,19 @@ hp_status Engine::dist_apply(std::vector<Prim>* prims_out, bool* fuse_out) {
     float* base = (float*)(peer_[pr.q] + L.wl_off[pr.v]);
     ptargets.push_back({base + (begin_ - pr.a), x0 - begin_, x1 - begin_});   // i -> [begin_+i-a]
   }
+  // every rank must take the same decision: fuse only if no owner's shard
+  // meets more than kMaxP targets (shards may be uneven, hp_config.ps_bounds)
+  size_t max_targets = 0;
+  for (int o = 0; o < G_; ++o) {
+    size_t cnt = 0;
+    for (const Prim& pr : prims)
+      cnt += std::max(pr.a, shard_b_[o]) < std::min(pr.a + pr.len, shard_b_[o + 1]) ? 1 : 0;
+    max_targets = std::max(max_targets, cnt);
+  }
   const bool fuse_pull = *fuse_out = push_pull_ && strict && U_ == Nm_ && !ba_.empty() &&
-                                     !bpull_.empty() &&
-                         ptargets.size() <= (size_t)kMaxP;
+                                     !bpull_.empty() && max_targets <= (size_t)kMaxP;
+  if (push_pull_ && strict && U_ == Nm_ && !ba_.empty() && !bpull_.empty() && !fuse_pull)
+    desc_splits_++;                   // owner-side pull refused: too many targets
   // NVLink traffic of this rank's links while every owner runs its apply
   // launch at once (the barrier aligns them): the ũ slices it loads from peers
   // and the owner-side pull stores it receives (in), what peers load from it and
@@ -198,6 +210,7 @@ hp_status Engine::dist_apply(std::vector<Prim>* prims_out, bool* fuse_out) {
   }
   int n_apply_launches = 0;
   for (size_t k2 = 0; k2 < ba_.size(); k2 += kMaxA) ++n_apply_launches;
+  if (n_apply_launches > 1) desc_splits_ += n_apply_launches - 1;
   const double x_link = n_apply_launches ? std::max(x_in, x_out) / n_apply_launches : 0.0;
   if (!ba_.empty()) {
     for (const BApply& a : ba_) xs_wait(a.v);
@@ -212,7 +225,10 @@ hp_status Engine::dist_apply(std::vector<Prim>* prims_out, bool* fuse_out) {
       memset(&d, 0, sizeof d);
       while (k < ba_.size() && d.na < kMaxA) {
         const int b = d.ns;
-        if (add_segs(d, begin_, n_, true, ba_[k].v, ba_[k].slot) < 0) break;
+        if (add_segs(d, begin_, n_, true, ba_[k].v, ba_[k].slot) < 0) {
+          desc_splits_++;               // segment table full: the rest in a later launch
+          break;
+        }
         d.a[d.na].seg_begin = b;
         d.a[d.na].seg_end = d.ns;
         d.na++;
@@ -283,6 +299,7 @@ hp_status Engine::dist_pull(const std::vector<Prim>& prims, bool fuse_pull) {
         bool first_part = true;
         do {
           if (d.ng == kMaxG || d.nf == kMaxF || d.ns == kMaxS) {
+            desc_splits_++;
             if (hp_status st = emit(d, rg.first, rg.second, xs_, xblocks_)) return st;
             memset(&d, 0, sizeof d);
           }
@@ -354,6 +371,7 @@ hp_status Engine::dist_pull(const std::vector<Prim>& prims, bool fuse_pull) {
       bool first_part = true;
       do {
         if (d.ng == kMaxG || d.nf == kMaxF) {
+          desc_splits_++;
           if (hp_status st = emit(d, rg.first, rg.second, xs_, xblocks_, r_link)) return st;
           fresh();
         }

@@ -14,6 +14,7 @@
 //                      then the VW's due folds w += u in minibatch order; store
 // Passed by value as a __grid_constant__ kernel parameter (< 4 KB).
 #pragma once
+#include <stddef.h>
 #include <stdint.h>
 
 namespace hp {
@@ -25,6 +26,7 @@ constexpr int kMaxF = 40;   // folds per launch
 constexpr int kMaxS = 32;   // source segments per launch
 constexpr int kMaxP = 16;   // pushed-pull store targets per launch
 constexpr int kTileSlots = 64;   // launch streams with dynamic tile counters per context
+constexpr size_t kTickBatch = 512;   // tick descriptors per multi-tick launch (captures)
 
 enum : uint32_t {
   kFirst = 1u,       // first minibatch of its wave: a = u
@@ -44,7 +46,7 @@ struct DComplete {
   float* snap;         // kSnapAcc: the waiting VW's open-clock aggregate (reading Z25)
   uint32_t v, p;
   uint32_t flags;
-  uint32_t pad;
+  float neg_lr;        // -eta of u_p: -lr, or -sigma/sqrt(t) (hp_config.lr_schedule)
 };
 
 // A source array split into segments by local index: element i of the launch
@@ -75,7 +77,7 @@ struct DFold {
   float* stash;        // CONVEX: FOLD reads w_p here; STASH writes w here
   uint32_t v, p;
   uint32_t op;         // 0 FOLD, 1 STASH
-  uint32_t pad;
+  float neg_lr;        // -eta of u_p (as DComplete::neg_lr)
 };
 
 struct DGroup {
@@ -93,7 +95,7 @@ struct TickDesc {
   int64_t blk_base;     // param_begin / 4 (param_begin is a multiple of 32)
   float* wg;            // w_global shard
   float* m;             // momentum shard (nullptr for SGD)
-  float neg_lr;         // -lr (negation is exact, Z10)
+  float neg_lr;         // -lr (unused by the kernels: every op carries its own -eta)
   float mu;             // momentum
   float conv_a, conv_sigma;   // CONVEX workload
   uint32_t key0, key1;  // Philox key = seed
@@ -180,6 +182,11 @@ struct FlagBarrier {
   int32_t G, me;
 };
 int launch_flag_barrier(const FlagBarrier& fb, void* stream);
+// Run `count` tick descriptors (device memory, in order) in one launch over
+// [0, n) of a single-rank context (static element -> thread map; FLOAT,
+// DYADIC, CONVEX). Returns a cudaError_t as int.
+int launch_multi_tick(const TickDesc* descs, int count, int64_t n, int grad_mode, bool momentum,
+                      void* stream);
 // Load every kernel instance now (once per process; lazy module loading could
 // otherwise stall a spinning flag barrier). Returns a cudaError_t as int.
 int preload_kernels();

@@ -9,9 +9,27 @@ from __future__ import annotations
 
 from typing import Optional
 
+import os
+
 from workloads import even_shards
 
 from . import hetpipe
+
+
+def _nccl_hint() -> None:
+    """Point the library at torch's bundled NCCL (HP_NCCL_LIB) unless set; the
+    library first reuses an NCCL already loaded in the process."""
+    if os.environ.get("HP_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl  # the pip package torch's NCCL comes from
+        for d in nvidia.nccl.__path__:
+            cand = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["HP_NCCL_LIB"] = cand
+                return
+    except ImportError:
+        pass
 
 
 def shard_bounds(nparams: int, world: int, rank: int):
@@ -36,6 +54,7 @@ def placed_context(cfg, rank: int, world: int, span: int, device: int = 0, strea
     torch.distributed (process group `pg`, default group), then hp_connect maps
     the peers. After this every rank must drive the same protocol calls."""
     import torch.distributed as dist
+    _nccl_hint()
     c = hetpipe.config_from(cfg, world=world, rank=rank, vw_span=span, device=device,
                             stream=stream or None, **overrides)
     ctx = hetpipe.Context(c)
@@ -57,6 +76,7 @@ def symmetric_context(cfg, rank: int, world: int, span: int, device: int = 0, st
     import torch
     import torch.distributed as dist
     import torch.distributed._symmetric_memory as symm
+    _nccl_hint()
     c = hetpipe.config_from(cfg, world=world, rank=rank, vw_span=span, device=device,
                             stream=stream or None, **overrides)
     nbytes = hetpipe.arena_bytes(c)

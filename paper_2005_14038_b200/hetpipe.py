@@ -35,7 +35,7 @@ class hp_config(C.Structure):
                 ("merge_ticks", C.c_int32), ("world", C.c_int32), ("rank", C.c_int32),
                 ("vw_span", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p),
                 ("transport", C.c_int32), ("reserved", C.c_int32),
-                ("update_freq", C.c_int32), ("reserved2", C.c_int32),
+                ("update_freq", C.c_int32), ("lr_schedule", C.c_int32),
                 ("conv_a", C.c_float), ("conv_sigma", C.c_float), ("ps_bounds", C.c_void_p),
                 ("arena", C.c_void_p)]
 
@@ -48,7 +48,8 @@ class hp_stats(C.Structure):
                 ("launches", C.c_int64), ("ticks", C.c_int64),
                 ("alg_bytes", C.c_double), ("wait_ticks", C.c_int64 * 8),
                 ("pulls", C.c_int64 * 8), ("nvl_bytes", C.c_double),
-                ("lockstep_batches", C.c_int64), ("apply_batches", C.c_int64)]
+                ("lockstep_batches", C.c_int64), ("apply_batches", C.c_int64),
+                ("desc_splits", C.c_int64)]
 
 
 class hp_unit(C.Structure):
@@ -168,6 +169,7 @@ def config_from(cfg, **overrides) -> hp_config:
     c.pull_policy, c.local_semantics = cfg.pull_policy, cfg.local_semantics
     c.conv_a, c.conv_sigma = getattr(cfg, "conv_a", 0.5), getattr(cfg, "conv_sigma", 1.0)
     c.update_freq = getattr(cfg, "F", 1)
+    c.lr_schedule = getattr(cfg, "lr_schedule", 0)
     bounds = overrides.pop("ps_bounds", None)
     for k, v in overrides.items():
         setattr(c, k, v)

@@ -1,0 +1,81 @@
+#!/usr/bin/env bash
+# One parameterised driver for the measurement sessions on a B200 box (it
+# replaces round 1's one-off scripts/gpuN.sh files, kept in git history at
+# b751f1a). Run from the repo root, e.g.
+#   gpurun --timeout 1800 -- 'bash scripts/session.sh validate r02_final'
+#   gpurun --gpus 4 --timeout 2400 -- 'bash scripts/session.sh multi r02_g4'
+# Every job writes under gpurun_out/<tag>/ and appends "<step>=<rc>" to its
+# status.txt; the files worth keeping are copied into profiles/ by hand.
+#
+# jobs:
+#   validate  smoke, pytest -m gpu, bench N=1 (C2) + reference arm, C1 line
+#   ncu       ncu launch list of the N=1 bench + one --set full tick-kernel capture
+#   ncu_c1    --set full capture of the C1 tick kernels (latency-bound launches)
+#   single    single-GPU workloads: C3 / C4 / C5 on one GPU, F=2, CONVEX, PMP timing
+#   multi     every visible GPU (N >= 2): nvlink peak, default bench (C3 placement),
+#             C2 ED-local, C4 ED-local, C5 (one VW per GPU), C5E / HVD transports,
+#             multi-GPU parity
+#   knobs     GPU parity under the non-default tuning knobs (1 GPU)
+set -u
+JOB=${1:?job}
+TAG=${2:-$JOB}
+D=gpurun_out/$TAG
+mkdir -p "$D"
+st() { echo "$1=$2" >> "$D/status.txt"; }
+NG=$(python -c "import torch; print(torch.cuda.device_count())")
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+NOX="--no-e2e --no-cpu-baseline"
+
+case "$JOB" in
+validate)
+  python -c "import __graft_entry__ as g; g.build(); g.smoke()" > "$D/smoke.log" 2>&1; st smoke $?
+  timeout 1500 python -m pytest tests -m gpu -q > "$D/pytest_gpu.log" 2>&1; st pytest $?
+  CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py > "$D/bench_n1.json" 2> "$D/bench_n1.err"; st bench1 $?
+  CUDA_VISIBLE_DEVICES=0 timeout 600 python bench.py --impl reference > "$D/ref_n1.json" 2>/dev/null; st ref $?
+  CUDA_VISIBLE_DEVICES=0 timeout 600 python bench.py --config C1 --no-cpu-baseline > "$D/bench_c1.json" 2> "$D/bench_c1.err"; st c1 $?
+  ;;
+ncu)
+  CMD="python bench.py --steps 3 --warmup 3 $NOX --profile-steps 1"
+  CUDA_VISIBLE_DEVICES=0 $CMD > "$D/plain.log" 2>&1; st plain $?
+  CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file "$D/launches.csv" $CMD > "$D/ncu_list.log" 2>&1; st ncu_list $?
+  CUDA_VISIBLE_DEVICES=0 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:tick_kernel \
+    -s 18 -c 6 -o "$D/tick_full" $CMD > "$D/ncu_full.log" 2>&1; st ncu_full $?
+  ;;
+ncu_c1)
+  CMD="python bench.py --config C1 --steps 40 --warmup 5 $NOX --graph 0 --profile-steps 1"
+  CUDA_VISIBLE_DEVICES=0 $CMD > "$D/plain.log" 2>&1; st plain $?
+  CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tick \
+    -s 60 -c 3 -o "$D/c1_full" $CMD > "$D/ncu_full.log" 2>&1; st ncu_full $?
+  ;;
+single)
+  for c in C3 C4 C5; do
+    CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --config $c --steps 40 $NOX > "$D/bench_${c}_n1.json" 2>> "$D/err.log"; st "$c" $?
+  done
+  CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --update-freq 2 --steps 40 $NOX > "$D/bench_c2_f2.json" 2>> "$D/err.log"; st f2 $?
+  CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --grad convex --steps 40 $NOX > "$D/bench_c2_convex.json" 2>> "$D/err.log"; st convex $?
+  CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --timing pmp --steps 40 $NOX > "$D/bench_c2_pmp.json" 2>> "$D/err.log"; st pmp $?
+  ;;
+multi)
+  [ "$NG" -ge 2 ] || { st multi_needs_2_gpus 1; exit 0; }
+  timeout 600 python scripts/nvlink_peak.py --out "$D/nvlink_peak.json" > "$D/nvlink_peak.log" 2>&1; st nvlink_peak $?
+  P=29760
+  run() { P=$((P+1)); name=$1; shift; timeout 1200 $TR --nproc-per-node "$NG" --master-port $P bench.py --gpus "$NG" "$@" > "$D/$name.json" 2>> "$D/err.log"; st "$name" $?; }
+  run bench_default
+  run c2_edlocal --config C2 --span 0 $NOX --steps 100
+  run c4_edlocal --config C4 --span 0 $NOX --steps 60
+  run c3_k1 --config C3 --span 1 $NOX --steps 40
+  run c5 --config C5 --span 1 $NOX --steps 20
+  run c5e_nvls --config C5E --span 1 --transport nvls $NOX --steps 20
+  run c5e_nccl --config C5E --span 1 --transport nccl $NOX --steps 20
+  run hvd_nvls --config HVD --span 1 --transport nvls $NOX --steps 40
+  timeout 1500 python -m pytest tests/test_gpu_multi.py -q > "$D/pytest_multi.log" 2>&1; st multi_parity $?
+  ;;
+knobs)
+  for kv in "HP_TICK_U=1" "HP_GRID=1" "HP_PDL=0" "HP_DYN=0" "HP_PREFETCH=0" "HP_DYN_MIN_N=0"; do
+    env $kv timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu > "$D/parity_${kv}.log" 2>&1; st "$kv" $?
+  done
+  ;;
+*)
+  echo "unknown job $JOB" >&2; exit 2 ;;
+esac

@@ -60,17 +60,23 @@ def main():
             print(f"{model} G={G}: largest shard {big / b[-1]:.3f} of the model = "
                   f"{big * G / b[-1]:.2f} x mean")
     print()
-    print("# B200 runs (profiles/r01_bench_*.json): measured NVLink ingress per rank per step")
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r01_bench_*g*.json"))):
+    print("# B200 runs (profiles/r0*_bench_*.json): ALGORITHMIC NVLink bytes per rank per step "
+          "(from the descriptors, hp_stats.nvl_bytes); NVML-counted bytes where the run has them")
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r0*_bench_*g*.json")) +
+                    glob.glob(os.path.join(ROOT, "profiles", "r02_multi", "*.json"))):
         try:
             d = json.loads(open(f).read().strip().splitlines()[-1])
         except Exception:
             continue
         c = d["config"]
-        nv = d.get("nvlink", {})
+        nv = d.get("nvlink") or {}
+        alg = nv.get("alg_bytes_per_step_max_rank", nv.get("bytes_per_step_max_rank", 0))
+        meas = nv.get("measured") or {}
+        mtxt = (f", NVML tx {meas['tx_bytes_per_step_max_rank'] / MB:.0f} / rx "
+                f"{meas['rx_bytes_per_step_max_rank'] / MB:.0f} MB/step" if meas else "")
         print(f"{os.path.basename(f)}: {c['workload']} N={c['num_vw']} G={d['n_gpus']} "
               f"{c.get('placement')} transport={c.get('transport')} ps={c.get('ps_shards')}: "
-              f"{nv.get('bytes_per_step_max_rank', 0) / MB:.0f} MB/step, {d['ms_per_step']:.3f} ms/step")
+              f"algorithmic {alg / MB:.0f} MB/step{mtxt}, {d['ms_per_step']:.3f} ms/step")
 
 
 if __name__ == "__main__":

@@ -25,8 +25,8 @@ void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
 }
 
 float draw_u(const TickDesc& d, int gm, uint32_t v, uint32_t p, int64_t i, const float* grad,
-             const float* stash) {
-  if (gm == 2) return d.neg_lr * grad[i];
+             const float* stash, float nl) {
+  if (gm == 2) return nl * grad[i];
   const int64_t gi = d.blk_base * 4 + i;
   uint32_t c[4] = {(uint32_t)(gi >> 2), v, p, 0u};
   philox(c, d.key0, d.key1);
@@ -38,10 +38,10 @@ float draw_u(const TickDesc& d, int gm, uint32_t v, uint32_t p, int64_t i, const
     const float xi = (float)(x >> 8) * 0x1p-24f - 0.5f;
     const float t1 = d.conv_a * (stash[i] - b);
     const float t2 = d.conv_sigma * xi;
-    return d.neg_lr * (t1 + t2);
+    return nl * (t1 + t2);
   }
   const float g = gm == 1 ? (float)((int)(x >> 28) - 8) : (float)(x >> 8) * 0x1p-24f - 0.5f;
-  return d.neg_lr * g;
+  return nl * g;
 }
 
 const float* seg(const TickDesc& d, int b, int e, int64_t i) {
@@ -68,7 +68,7 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
     for (int k = 0; k < d.na; ++k) app(d, mom, wg, m, seg(d, d.a[k].seg_begin, d.a[k].seg_end, i)[i]);
     for (int j = 0; j < d.nc; ++j) {
       const DComplete& c = d.c[j];
-      const float u = draw_u(d, gm, c.v, c.p, i, c.grad, c.stash);
+      const float u = draw_u(d, gm, c.v, c.p, i, c.grad, c.stash, c.neg_lr);
       if (c.flags & kSnapAcc) c.snap[i] = c.acc[i];
       const float a = (c.flags & kFirst) ? u : c.acc[i] + u;
       if (c.flags & kStoreAcc) c.acc[i] = a;
@@ -91,7 +91,7 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
       for (int f = G.f_begin; f < G.f_end; ++f) {
         const DFold& F = d.f[f];
         if (gm == 3 && F.op == 1) F.stash[i] = w;            // STASH: a START reads w
-        else w = w + draw_u(d, gm, F.v, F.p, i, F.grad, F.stash);
+        else w = w + draw_u(d, gm, F.v, F.p, i, F.grad, F.stash, F.neg_lr);
       }
       G.wl[i] = w;
     }
@@ -115,6 +115,12 @@ int launch_nvls(const NvlsDesc& d, void*, int) {
 
 int preload_kernels() { return 0; }
 int launch_empty(void*) { return 0; }
+int launch_multi_tick(const TickDesc* descs, int count, int64_t, int grad_mode, bool momentum,
+                      void* stream) {
+  for (int k = 0; k < count; ++k)
+    if (int e = launch_tick(descs[k], grad_mode, momentum, stream, 0)) return e;
+  return 0;
+}
 
 // HP_STRESS spin: a no-op here (emulated kernels run at launch on the host)
 int launch_spin(unsigned long long, void*) { return 0; }

@@ -151,3 +151,9 @@ def test_update_frequency_blocked_strict(hp, F, Nm, D, tau, mode):
 @pytest.mark.parametrize("seed", range(24))
 def test_external_gradients_random(hp, seed):
     G.test_external_gradients_random(hp, seed)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_theorem1_schedule(hp, seed):
+    """NEXT-2: Theorem 1's per-op step sizes through the engine's descriptors."""
+    G.test_theorem1_schedule_random_bit_exact(hp, seed)

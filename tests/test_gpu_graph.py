@@ -8,7 +8,6 @@ import numpy as np
 import pytest
 
 from oracle import run_schedule
-from placement_check import check, run_colocated
 from workloads import C1, C1_SKEW, C2, C3, WSPConfig
 
 pytestmark = pytest.mark.gpu
@@ -46,13 +45,19 @@ def _run_graphs(hp, cfg, pieces, **over):
     return trace, wg, wl, m
 
 
+@pytest.mark.parametrize("batch", ["1", "0"], ids=["multitick", "per-tick"])
 @pytest.mark.parametrize("cfg,pieces", [
     (C1, 1), (C1, 16), (C1_SKEW, 5),
     (C2.replace(nparams=40_003, waves=6, momentum=0.9), 3),
     (C3.replace(nparams=20_000, waves=7), 4),
+    (C3.replace(nparams=100_003, waves=5), 2),          # above the multi-tick size limit
     (WSPConfig("cf", 3, 2, 1, 4099, 5, (3, 5, 4), grad_mode=3, lr=0.05, F=2), 2),
-], ids=["C1-1", "C1-16", "C1skew-5", "C2mom-3", "C3-4", "convexF-2"])
-def test_graph_capture_bit_exact(hp, cfg, pieces):
+    (WSPConfig("th", 2, 2, 1, 4099, 9, (3, 5), grad_mode=3, lr=0.3, lr_schedule=1), 3),
+], ids=["C1-1", "C1-16", "C1skew-5", "C2mom-3", "C3-4", "C3big-2", "convexF-2", "thm1-3"])
+def test_graph_capture_bit_exact(hp, monkeypatch, cfg, pieces, batch):
+    """Captured ticks -- through the multi-tick kernel for small contexts
+    (HP_TICK_BATCH=1, default) or as per-tick launches -- equal the oracle."""
+    monkeypatch.setenv("HP_TICK_BATCH", batch)
     o = run_schedule(cfg)
     trace, wg, wl, m = _run_graphs(hp, cfg, pieces)
     assert trace == o.trace
@@ -78,44 +83,16 @@ def test_graph_refuses_reads_before_launch(hp):
     ctx.close()
 
 
-def test_graph_capture_colocated_placement(hp):
-    """A distributed context's capture forks the accumulation / exchange
-    streams from the context stream and joins them back: two co-located ranks
-    (threads on this GPU, flag barriers) capture and launch their rounds."""
-    import threading
-
+def test_graph_capture_refused_for_distributed_context(hp):
+    """Distributed contexts issue their exchange directly (a captured flag
+    barrier would spin inside a graph)."""
     import torch
-    from placement_check import collect
-    cfg, G, k = C3.replace(nparams=20_000, waves=6), 2, 1
-    keep, ctxs = [], []
-    for r in range(G):
-        c = hp.config_from(cfg, world=G, rank=r, vw_span=k)
-        t = torch.empty(hp.arena_bytes(c), dtype=torch.uint8, device="cuda:0")
-        keep.append(t)
-        c.arena = t.data_ptr()
-        ctxs.append(hp.Context(c))
-    bases = [c.cfg.arena for c in ctxs]
-    out, errs = [None] * G, []
-
-    def work(r):
-        try:
-            ctx = ctxs[r]
-            ctx.connect_symmetric(bases, 0, None)
-            ctx.schedule_begin(cfg.tau, cfg.latency())
-            for step in range(1, cfg.waves + 1):
-                g = ctx.schedule_capture(cfg.num_vw * step)
-                g.launch()
-                g.close()
-            out[r] = collect(ctx, cfg, G, k, r)
-        except Exception as e:
-            errs.append((r, e))
-
-    th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(G)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join(300)
-    assert not errs, errs
-    check(cfg, G, k, out)
-    for c in ctxs:
-        c.close()
+    cfg, G = C3.replace(nparams=4096, waves=2), 2
+    c = hp.config_from(cfg, world=G, rank=0, vw_span=1)
+    t = torch.empty(hp.arena_bytes(c), dtype=torch.uint8, device="cuda:0")
+    c.arena = t.data_ptr()
+    ctx = hp.Context(c)
+    ctx.schedule_begin(cfg.tau, cfg.latency())
+    with pytest.raises(hp.HetPipeError, match="HP_ERR_STATE"):
+        ctx.schedule_capture(2)
+    ctx.close()

@@ -367,6 +367,28 @@ def test_convex_random_bit_exact(hp, seed):
         assert np.array_equal(m, o.m)
 
 
+@pytest.mark.parametrize("seed", range(24))
+def test_theorem1_schedule_random_bit_exact(hp, seed):
+    """NEXT-2: Theorem 1's step sizes eta_t = sigma / sqrt(t), t = (p-1)N + v + 1
+    (reading Z26), per op on the device (host-computed fp32, in
+    each complete / fold), on the CONVEX and the FLOAT workloads, EXTERNAL
+    excluded: identical traces, bit-exact arrays."""
+    rng = random.Random(9100 + seed)
+    base = _rand_cfg(seed)
+    convex = rng.random() < 0.6
+    cfg = base.replace(lr_schedule=1, lr=rng.choice([0.05, 0.3]),
+                       grad_mode=GRAD_CONVEX if convex else GRAD_FLOAT,
+                       conv_sigma=rng.choice([0.0, 0.5]), w0_mode=W0_PHILOX,
+                       F=rng.choice([1, 1, 2]))
+    o = run_schedule(cfg)
+    trace, wg, wl, m, _ = run_device(hp, cfg, apply_mode=rng.randint(0, 1),
+                                     acc_slots=rng.choice([2, 3]),
+                                     merge_ticks=rng.randint(0, 1))
+    assert_same(o, trace, wg, wl)
+    if cfg.momentum:
+        assert np.array_equal(m, o.m)
+
+
 def test_convex_per_tick_states(hp):
     """CONVEX: the device w_local after every commit equals the oracle's."""
     cfg = C2.replace(nparams=2053, waves=6, D=1, tau=(5, 7, 9, 12), grad_mode=GRAD_CONVEX,

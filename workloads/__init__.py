@@ -38,6 +38,10 @@ W0_PHILOX = 1
 PULL_EAGER = 0
 PULL_LAZY = 1
 
+# lr_schedule
+LR_CONSTANT = 0
+LR_THEOREM1 = 1
+
 # local_semantics
 LOCAL_STRICT = 0
 LOCAL_AT_LEAST = 1
@@ -72,6 +76,8 @@ class WSPConfig:
     conv_sigma: float = 1.0                 # GRAD_CONVEX noise scale sigma
     F: int = 1                              # update frequency factor (NEXT-4): one clock
                                             # = F waves; `waves` counts clocks
+    lr_schedule: int = 0                    # 0: constant lr; 1: Theorem 1's eta_t =
+                                            # lr / sqrt(t), t = (p-1)*N + v + 1 (NEXT-2)
 
     def latency(self) -> Tuple[int, ...]:
         if self.lat is not None:
