@@ -456,6 +456,7 @@ def profiled_pass(ctx, N, done_steps, prof_steps, stream, barrier):
                         for t, by, sy in zip(l_ms, l_bytes, l_sync) if by > 0))
     s_ms, s_vw, s_waited = ctx.profile_sync_latency()
     l_link = ctx.profile_link()
+    l_stream = ctx.profile_streams()
     mix = {}
     for t_ms, by, sh in zip(l_ms, l_bytes, l_shape):
         sh = int(sh) & 0xFFFFFFFF
@@ -471,7 +472,10 @@ def profiled_pass(ctx, N, done_steps, prof_steps, stream, barrier):
         e[2] += float(by)
     st1 = ctx.stats()
     ctx.profile_enable(False)
-    return {"prof_ms": ms, "kern_ms": kern_ms, "kern_bytes": kern_bytes,
+    timeline = [{"start_ms": float(a), "ms": float(t), "shape": int(sh) & 0xFFFFFFFF,
+                 "stream": int(sid), "bytes": float(by), "link_bytes": float(lk)}
+                for a, t, sh, sid, by, lk in zip(l_t0, l_ms, l_shape, l_stream, l_bytes, l_link)]
+    return {"prof_ms": ms, "timeline": timeline, "kern_ms": kern_ms, "kern_bytes": kern_bytes,
             "kern_launches": kern_launches, "busy_ms": busy_ms, "sync_ms": sync_ms,
             "pcommits": st1.commits - st0.commits,
             "sync_us": [1e3 * float(x) for x in s_ms],
@@ -590,6 +594,9 @@ def main():
                     help="N>1: GPUs per VW of the distributed placement (k<N exchanges over "
                          "NVLink); 0 = ED-local shards (no exchange); -1 (default) = the "
                          "SURVEY 8(d) placement of the config (C3: k=1 at 2/4 GPUs, k=2 at 8)")
+    ap.add_argument("--timeline", default="",
+                    help="write the profiled pass's per-launch records (start, duration, "
+                         "shape, stream, bytes) of every rank to PATH.rank<r>.json")
     ap.add_argument("--graph", type=int, default=-1,
                     help="1: the timed rounds' device work is captured by hp_schedule_capture "
                          "before the timed region and launched as one CUDA graph; -1 (default) "
@@ -628,6 +635,10 @@ def main():
     prof_steps = max(1, min(args.steps, args.profile_steps))
     res = measure(cfg, span, args, ws, rank, local, stream, args.steps, args.warmup, prof_steps,
                   graph, extra, sampler=True, nvml=nvml)
+    if args.timeline and res.get("timeline") is not None:
+        with open(f"{args.timeline}.rank{rank}.json", "w") as f:
+            json.dump({"rank": rank, "config": cfg.name, "span": span, "steps": prof_steps,
+                       "launches": res["timeline"]}, f)
     # link bytes this rank's GPU moved in the timed region (max over ranks)
     nv_meas = None
     if res["nvml"] is not None:

@@ -348,6 +348,10 @@ hp_status hp_profile_launches(hp_ctx* ctx, int64_t max, float* ms, double* alg_b
    peer / multicast accesses or NCCL collective move through this GPU's links;
    0 for launches that touch only local memory. */
 hp_status hp_profile_link(hp_ctx* ctx, int64_t max, double* link_bytes, int64_t* n);
+/* Per-launch stream of the same window: 0 = context stream, 1 = exchange
+   stream, 2 = second exchange stream (NVLS split), 3+v = accumulation stream
+   of VW v, 3+num_vw+v = its fold stream (distributed placements). */
+hp_status hp_profile_streams(hp_ctx* ctx, int64_t max, int32_t* stream_ids, int64_t* n);
 
 /* Wave-sync latency of the same window, one record per
    (VW, wave) whose push and pull both fall in it: device time from the start

@@ -522,6 +522,12 @@ hp_status hp_profile_link(hp_ctx* ctx, int64_t max, double* link_bytes, int64_t*
   HP_EXIT(ctx)
 }
 
+hp_status hp_profile_streams(hp_ctx* ctx, int64_t max, int32_t* stream_ids, int64_t* n) {
+  HP_ENTRY(ctx)
+  return ctx->eng->profile_streams(max, stream_ids, n);
+  HP_EXIT(ctx)
+}
+
 hp_status hp_profile_sync_latency(hp_ctx* ctx, int64_t max, float* ms, int32_t* vw,
                                   int32_t* waited, int64_t* n) {
   HP_ENTRY(ctx)

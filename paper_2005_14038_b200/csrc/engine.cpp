@@ -646,7 +646,7 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   if (dyn_env && loads >= dyn_min && n >= dyn_n && (dyn_pulls || d.ng == 0))
     tile_slot(st, &d.ctr, &d.done);
   if (capturing_ && batch_ok_ && st == stream_) {
-    batch_.push_back(d);
+    batch_.push_back(TickDescPad{d});
     alg_bytes_ += bytes;
     if (batch_.size() >= kTickBatch) return flush_batch();
     return HP_OK;
@@ -786,6 +786,26 @@ void Engine::prof_end(cudaStream_t st, double bytes, double sync_bytes, int32_t 
   prof_launch_sync_.push_back(sync_bytes);
   prof_launch_shape_.push_back(shape);
   prof_launch_link_.push_back(link_bytes);
+  prof_launch_stream_.push_back(stream_id(st));
+}
+
+int32_t Engine::stream_id(cudaStream_t st) const {
+  if (st == stream_) return 0;
+  if (st == xs_) return 1;
+  if (st == xs2_) return 2;
+  for (int v = 0; v < (int)vs_.size(); ++v) {
+    if (st == vs_[v]) return 3 + v;
+    if (fs_[v] && st == fs_[v]) return 3 + N_ + v;
+  }
+  return -1;
+}
+
+hp_status Engine::profile_streams(int64_t max, int32_t* ids, int64_t* n) {
+  if (sticky_) return sticky_;
+  const int64_t cnt = std::min<int64_t>(max, (int64_t)prof_launch_stream_.size());
+  for (int64_t i = 0; i < cnt && ids; ++i) ids[i] = prof_launch_stream_[i];
+  if (n) *n = cnt;
+  return HP_OK;
 }
 
 hp_status Engine::profile_link(int64_t max, double* link_bytes, int64_t* n) {
@@ -1066,7 +1086,7 @@ hp_status Engine::capture_end(bool ok, cudaGraphExec_t* exec) {
 // device buffer the graph owns, and the launch is recorded into the graph.
 hp_status Engine::flush_batch() {
   if (batch_.empty()) return HP_OK;
-  const size_t bytes = batch_.size() * sizeof(TickDesc);
+  const size_t bytes = batch_.size() * sizeof(TickDescPad);
   void* dev = nullptr;
   if (cudaMalloc(&dev, bytes) != cudaSuccess) {
     cudaGetLastError();
@@ -1078,7 +1098,7 @@ hp_status Engine::flush_batch() {
   if (int e = cudaMemcpyAsync(dev, batch_.data(), bytes, cudaMemcpyHostToDevice, up_))
     return check_cuda(e, "tick batch upload");
   if (int e = cudaStreamSynchronize(up_)) return check_cuda(e, "tick batch upload");
-  const int err = launch_multi_tick((const TickDesc*)dev, (int)batch_.size(), n_, cfg_.grad_mode,
+  const int err = launch_multi_tick((const TickDescPad*)dev, (int)batch_.size(), n_, cfg_.grad_mode,
                                     m_ != nullptr, stream_);
   launches_++;
   batch_.clear();
@@ -1173,6 +1193,7 @@ hp_status Engine::profile_enable(bool on) {
   prof_launch_sync_.clear();
   prof_launch_link_.clear();
   prof_launch_shape_.clear();
+  prof_launch_stream_.clear();
   push_launch_.assign(N_, -1);
   sync_recs_.clear();
   return HP_OK;

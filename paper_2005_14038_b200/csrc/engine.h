@@ -117,6 +117,7 @@ class Engine {
   hp_status profile_launches(int64_t max, float* ms, double* bytes, int32_t* shape,
                              double* sync_bytes, float* start_ms, int64_t* n);
   hp_status profile_link(int64_t max, double* link_bytes, int64_t* n);
+  hp_status profile_streams(int64_t max, int32_t* ids, int64_t* n);
   int64_t ticks = 0;
 
  private:
@@ -236,7 +237,7 @@ class Engine {
   // (launch_multi_tick): the captured ticks' descriptors are collected and run
   // by one multi-tick kernel per batch; their device copies belong to the graph.
   bool batch_ok_ = false;             // context qualifies (set at init)
-  std::vector<TickDesc> batch_;
+  std::vector<TickDescPad> batch_;
   std::vector<void*> graph_bufs_;     // descriptor buffers of the capture in progress
   cudaStream_t up_ = nullptr;         // upload stream (never captured)
   hp_status flush_batch();
@@ -278,6 +279,9 @@ class Engine {
   std::vector<double> prof_launch_sync_;
   std::vector<double> prof_launch_link_;   // NVLink bytes per direction (max of in, out)
   std::vector<int32_t> prof_launch_shape_;
+  std::vector<int32_t> prof_launch_stream_;   // 0 context, 1 exchange, 2 second exchange,
+                                              // 3+v accumulation of VW v, 3+N+v its fold stream
+  int32_t stream_id(cudaStream_t st) const;
   // wave-sync latency: profiled launch that carried VW v's wave-end COMPLETE
   // (its u~ final = the push) -> the launch that wrote its pulled w_local
   std::vector<int64_t> push_launch_;

@@ -461,9 +461,9 @@ __global__ void __launch_bounds__(256, 4) tick_kernel_o4(const __grid_constant__
 // stays hot in the SMs' instruction caches across ticks (ncu on the one-tick
 // C1 launches: stalls on instruction fetch dominate, 2.3 us active in 5.7 us).
 template <int GM, bool MOM>
-__global__ void __launch_bounds__(256) multi_tick_kernel(const TickDesc* __restrict__ descs,
+__global__ void __launch_bounds__(256) multi_tick_kernel(const TickDescPad* __restrict__ descs,
                                                          int count) {
-  constexpr int kWords = (int)((sizeof(TickDesc) + 15) / 16);
+  constexpr int kWords = (int)(sizeof(TickDescPad) / 16);
   static_assert(kWords <= 256, "one 16-byte word of the descriptor per thread");
   __shared__ __align__(16) uint4 sbuf[kWords];
   const TickDesc& sd = *reinterpret_cast<const TickDesc*>(sbuf);
@@ -720,7 +720,7 @@ int launch_nvls_u(const NvlsDesc& d, cudaStream_t s, int max_blocks) {
   return (int)cudaGetLastError();
 }
 
-int launch_multi_tick(const TickDesc* descs, int count, int64_t n, int grad_mode, bool momentum,
+int launch_multi_tick(const TickDescPad* descs, int count, int64_t n, int grad_mode, bool momentum,
                       void* stream) {
   if (count <= 0 || n <= 0) return 0;
   int64_t blocks = (((n + 3) >> 2) + 255) / 256;

@@ -121,6 +121,12 @@ struct TickDesc {
 
 static_assert(sizeof(TickDesc) <= 4096, "TickDesc must fit a kernel parameter");
 
+// A TickDesc in device memory (multi-tick batches): 16-byte aligned stride, so
+// the kernel stages it with one 16-byte load per thread.
+struct alignas(16) TickDescPad {
+  TickDesc d;
+};
+
 // Buffer passes of one launch (each = 4 bytes per param): the algorithmic
 // bytes the fused tick must move, used for the roofline.
 inline int tick_streams(const TickDesc& d) {
@@ -185,7 +191,7 @@ int launch_flag_barrier(const FlagBarrier& fb, void* stream);
 // Run `count` tick descriptors (device memory, in order) in one launch over
 // [0, n) of a single-rank context (static element -> thread map; FLOAT,
 // DYADIC, CONVEX). Returns a cudaError_t as int.
-int launch_multi_tick(const TickDesc* descs, int count, int64_t n, int grad_mode, bool momentum,
+int launch_multi_tick(const TickDescPad* descs, int count, int64_t n, int grad_mode, bool momentum,
                       void* stream);
 // Load every kernel instance now (once per process; lazy module loading could
 // otherwise stall a spinning flag barrier). Returns a cudaError_t as int.

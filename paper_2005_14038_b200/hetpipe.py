@@ -110,6 +110,7 @@ EXPORTS = {
                                       C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.POINTER(C.c_int64)]),
     "hp_profile_link": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_int64)]),
+    "hp_profile_streams": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_int64)]),
     "hp_profile_sync_latency": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.POINTER(C.c_int64)]),
     "hp_partition": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
@@ -418,6 +419,17 @@ def _profile_link(self, max_records: int = 1 << 16):
 
 
 Context.profile_link = _profile_link
+
+
+def _profile_streams(self, max_records: int = 1 << 16):
+    out = np.zeros(max_records, dtype=np.int32)
+    n = C.c_int64()
+    self._chk(self.lib.hp_profile_streams(self.h, max_records, out.ctypes.data_as(C.c_void_p),
+                                          C.byref(n)))
+    return out[:n.value]
+
+
+Context.profile_streams = _profile_streams
 
 
 def comm_unique_id(lib: Optional[C.CDLL] = None) -> bytes:

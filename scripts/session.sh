@@ -15,6 +15,7 @@
 #   multi     every visible GPU (N >= 2): nvlink peak, default bench (C3 placement),
 #             C2 ED-local, C4 ED-local, C5 (one VW per GPU), C5E / HVD transports,
 #             multi-GPU parity
+#   overlap   a9 overlap variants (split folds, bounded grids) with per-launch timelines
 #   knobs     GPU parity under the non-default tuning knobs (1 GPU)
 set -u
 JOB=${1:?job}
@@ -70,6 +71,22 @@ multi)
   run c5e_nccl --config C5E --span 1 --transport nccl $NOX --steps 20
   run hvd_nvls --config HVD --span 1 --transport nvls $NOX --steps 40
   timeout 1500 python -m pytest tests/test_gpu_multi.py -q > "$D/pytest_multi.log" 2>&1; st multi_parity $?
+  ;;
+overlap)
+  # a9 overlap experiments on every visible GPU: C3 (default placement) and
+  # C5E (NVLS) with split acc / fold launches and bounded grids; per-launch
+  # timelines of every rank (bench.py --timeline)
+  [ "$NG" -ge 2 ] || { st overlap_needs_2_gpus 1; exit 0; }
+  P=29800
+  for cfg in "C3" "C5E --transport nvls"; do
+    name=$(echo "$cfg" | cut -d' ' -f1)
+    for env in "X=0" "HP_SPLIT_FOLDS=1" "HP_XBLOCKS=80 HP_ABLOCKS=216" "HP_SPLIT_FOLDS=1 HP_XBLOCKS=48 HP_ABLOCKS=240" "HP_SPLIT_FOLDS=1 HP_XBLOCKS=80 HP_ABLOCKS=216"; do
+      P=$((P+1)); tag=$(echo "$env" | tr ' =' '__')
+      env $env timeout 900 $TR --nproc-per-node "$NG" --master-port $P bench.py --gpus "$NG" --config $cfg --span 1 \
+        $NOX --steps 30 --profile-steps 6 --no-extras --timeline "$D/tl_${name}_${tag}" > "$D/${name}_${tag}.json" 2>> "$D/err.log"
+      st "${name}_${tag}" $?
+    done
+  done
   ;;
 knobs)
   for kv in "HP_TICK_U=1" "HP_GRID=1" "HP_PDL=0" "HP_DYN=0" "HP_PREFETCH=0" "HP_DYN_MIN_N=0"; do

@@ -115,10 +115,10 @@ int launch_nvls(const NvlsDesc& d, void*, int) {
 
 int preload_kernels() { return 0; }
 int launch_empty(void*) { return 0; }
-int launch_multi_tick(const TickDesc* descs, int count, int64_t, int grad_mode, bool momentum,
+int launch_multi_tick(const TickDescPad* descs, int count, int64_t, int grad_mode, bool momentum,
                       void* stream) {
   for (int k = 0; k < count; ++k)
-    if (int e = launch_tick(descs[k], grad_mode, momentum, stream, 0)) return e;
+    if (int e = launch_tick(descs[k].d, grad_mode, momentum, stream, 0)) return e;
   return 0;
 }
 
