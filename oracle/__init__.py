@@ -18,7 +18,9 @@ P:846-847, lockstep at D=0), brute force over every interleaving of
 2 VW x 3 waves x 8 params (also with F = 2 and with heavy-ball momentum;
 the s_global floor and the D+1 clock distance shown tight); the weight-dependent CONVEX
 workload's BSP closed form and delayed recurrence, the section-6
-decomposition and Lemma 1 (tests/test_oracle_convex.py); s_global with F
+decomposition and Lemma 1 (tests/test_oracle_convex.py); Theorem 1's step
+sizes eta_t = sigma/sqrt(t) in closed form and its regret bound on oracle runs
+(P:1546-1554, App. A; tests/test_oracle_regret.py); s_global with F
 (tests/test_oracle_update_freq.py); the pipeline partitioner / simulator
 oracle (oracle/pipeline.py, tests/test_pipeline_schedule.py). Parity
 unpinned: the exact bits of FLOAT-mode intermediate w_local snapshots with
@@ -27,8 +29,8 @@ values to within Higham's summation bound).
 """
 from .philox import philox4x32_10, philox_words
 from .wsp import (OracleRun, WSPOracle, convex_target, gradient, initial_weights,
-                  run_schedule, s_global, version_floor, wave_range)
+                  run_schedule, s_global, step_size, version_floor, wave_range)
 
 __all__ = ["philox4x32_10", "philox_words", "OracleRun", "WSPOracle", "convex_target",
-           "gradient", "initial_weights", "run_schedule", "s_global", "version_floor",
-           "wave_range"]
+           "gradient", "initial_weights", "run_schedule", "s_global", "step_size",
+           "version_floor", "wave_range"]

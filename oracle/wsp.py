@@ -130,7 +130,7 @@ def step_size(vw: int, p: int, cfg: WSPConfig) -> np.float32:
     """eta of minibatch p of VW vw: the constant lr (Z2), or Theorem 1's
     schedule eta_t = sigma / sqrt(t) (App. A)
     with sigma = cfg.lr and the updates numbered worker-fastest,
-    t = (p - 1) * N + vw + 1 (the loop "over the workers (t mod N)" of P:1516-1520;
+    t = (p - 1) * N + vw + 1 (the loop "over the workers (t mod N)" of P:1511-1515;
     reading Z26). float32: fl(sigma / fl(sqrt(t))), t exact."""
     if getattr(cfg, "lr_schedule", 0) == 0:
         return F32(cfg.lr)

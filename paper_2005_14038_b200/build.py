@@ -24,6 +24,13 @@ NVCC_FLAGS = [
 ]
 
 
+# A/B variants (tuning experiments only): HP_BUILD_DEFINES="-DX=1 ..." and
+# HP_BUILD_OUT=<path> build another copy that bench/tests load via HP_LIB.
+if os.environ.get("HP_BUILD_OUT"):
+    LIB = os.path.abspath(os.environ["HP_BUILD_OUT"])
+NVCC_FLAGS += os.environ.get("HP_BUILD_DEFINES", "").split()
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True

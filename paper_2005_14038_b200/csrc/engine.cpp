@@ -111,9 +111,9 @@ RankLayout Engine::layout_of(int q) const {
       }
     }
   }
-  if (G_ > 1) {                       // K7 flags: one uint64 per source rank
-    L.flag_off = off;
-    off += align256(2 * G_);
+  if (G_ > 1) {                       // K7 flags: barrier, arrive, done; one uint64
+    L.flag_off = off;                 // per source rank each
+    off += align256(6 * G_);
   }
   L.bytes = off;
   return L;
@@ -243,7 +243,7 @@ hp_status Engine::init() {
     st = check_cuda(cudaMemsetAsync(tiles_, 0, kTileSlots * 128, stream_), "tile counters");
   }
   if (st == HP_OK && G_ > 1)            // K7 flags start at epoch 0 (before hp_connect's barrier)
-    st = check_cuda(cudaMemsetAsync(base + L.flag_off, 0, (size_t)G_ * 8, stream_), "flags");
+    st = check_cuda(cudaMemsetAsync(base + L.flag_off, 0, (size_t)G_ * 24, stream_), "flags");
   for (auto& v : vw_)                 // CONVEX: minibatches 1..Nm read w0
     for (float* sl : v.stash)
       if (st == HP_OK)
@@ -632,6 +632,10 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
       loads += (d.f[k].grad ? 1 : 0) + ((d.f[k].stash && d.f[k].op != 1) ? 1 : 0);
   }
   d.pf = (remote == 0 && loads <= pf_max) ? pf_env : 0;
+  // completes-only launches take the lean (phase B) instance (HP_LEAN=0: off)
+  static const int lean_env = getenv("HP_LEAN") ? atoi(getenv("HP_LEAN")) : 1;
+  d.lean = (lean_env && d.nc > 0 && d.na == 0 && d.ng == 0 && d.np == 0 && !d.wg_load &&
+            !d.wg_store) ? 1 : 0;
   // dynamic tile scheduling (HP_DYN, default on) for launches with at least
   // HP_DYN_MINLOADS load streams (HP_DYN_PULLS: also launches with pull groups):
   // counters of this launch stream

@@ -215,6 +215,15 @@ class Engine {
   int ablocks_ = 0;                   // grid bound of accumulation launches (HP_ABLOCKS)
   bool flag_barrier_ = true;          // K7 device flags (HP_FLAG_BARRIER=0: NCCL barrier)
   uint64_t epoch_ = 0;                // barriers issued (identical on every rank)
+  // Point-to-point readiness flags (HP_P2P, default on with the flag
+  // barrier): an apply batch waits only for the ranks it involves.
+  bool p2p_ = true;
+  uint64_t xepoch_ = 0;               // apply batches exchanged by flags (replicated)
+  uint64_t last_apply_epoch_ = 0;
+  std::vector<char> readers_;         // ranks that read w_global shards since the last apply
+  unsigned long long* flag_word(int q, int kind, int src) const;   // kind 0 barrier, 1 arrive, 2 done
+  hp_status flag_ops(cudaStream_t st, std::vector<unsigned long long*> sig,
+                     std::vector<const unsigned long long*> wait, uint64_t val);
   int* flag_err_ = nullptr;           // device: set if a flag wait timed out
   // dynamic tile scheduling of the tick kernel: one (counter, done) pair per
   // launch stream, 128 bytes apart, zero between launches (TickDesc::ctr)

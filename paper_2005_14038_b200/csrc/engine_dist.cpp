@@ -212,13 +212,37 @@ hp_status Engine::dist_apply(std::vector<Prim>* prims_out, bool* fuse_out) {
   for (size_t k2 = 0; k2 < ba_.size(); k2 += kMaxA) ++n_apply_launches;
   if (n_apply_launches > 1) desc_splits_ += n_apply_launches - 1;
   const double x_link = n_apply_launches ? std::max(x_in, x_out) / n_apply_launches : 0.0;
+  // ranks this batch involves: every stage of a pushing VW (its u~ is read by
+  // every owner; its acc slot is reused only after all owners read it), every
+  // stage of a pulled VW (its w_local is written by every owner, after its own
+  // folds), and the ranks that read w_global shards since the last apply (WAR)
+  std::vector<char> inv(G_, 0);
+  for (const BApply& a : ba_)
+    for (int q = 0; q < G_; ++q) inv[q] |= lay_[q].has[a.v];
+  for (int v : bpull_)
+    for (int q = 0; q < G_; ++q) inv[q] |= lay_[q].has[v];
+  for (int q = 0; q < G_; ++q) inv[q] |= readers_[q];
+  const bool p2p = p2p_ && flag_barrier_;
   if (!ba_.empty()) {
     for (const BApply& a : ba_) xs_wait(a.v);
     for (int v : bpull_) {
       xs_wait(v);
       xs_wait_wl(v);
     }
-    if (hp_status st = xbarrier()) return st;
+    const uint64_t ep = p2p ? ++xepoch_ : 0;
+    if (p2p) {
+      // ARRIVE: an involved rank announces its producers are done to every
+      // owner; every owner (all ranks) waits for the involved ranks only
+      std::vector<unsigned long long*> sig;
+      std::vector<const unsigned long long*> wait;
+      if (inv[rank_])
+        for (int q = 0; q < G_; ++q) sig.push_back(flag_word(q, 1, rank_));
+      for (int q = 0; q < G_; ++q)
+        if (inv[q]) wait.push_back(flag_word(rank_, 1, q));
+      if (hp_status st = flag_ops(xs_, sig, wait, ep)) return st;
+    } else if (hp_status st = xbarrier()) {
+      return st;
+    }
     size_t k = 0;
     while (k < ba_.size()) {
       TickDesc d;
@@ -240,7 +264,22 @@ hp_status Engine::dist_apply(std::vector<Prim>* prims_out, bool* fuse_out) {
     }
     applied_ += (int64_t)ba_.size();
     apply_batches_++;
-    if (hp_status st = xbarrier()) return st;
+    if (p2p) {
+      // DONE: every owner tells every rank its applies (and owner-side pull
+      // stores) are complete; an involved rank waits for every owner -- an
+      // uninvolved one does not wait at all (a later reader-side pull of it
+      // waits on the same words)
+      std::vector<unsigned long long*> sig;
+      std::vector<const unsigned long long*> wait;
+      for (int q = 0; q < G_; ++q) sig.push_back(flag_word(q, 2, rank_));
+      if (inv[rank_])
+        for (int q = 0; q < G_; ++q) wait.push_back(flag_word(rank_, 2, q));
+      if (hp_status st = flag_ops(xs_, sig, wait, ep)) return st;
+      last_apply_epoch_ = ep;
+      std::fill(readers_.begin(), readers_.end(), 0);
+    } else if (hp_status st = xbarrier()) {
+      return st;
+    }
     cudaEvent_t e = pool_event();       // acc slots read by the applies are free
     cudaEventRecord(e, xs_);
     for (const BApply& a : ba_)
@@ -352,6 +391,18 @@ hp_status Engine::dist_pull(const std::vector<Prim>& prims, bool fuse_pull) {
         }
     }
     r_link = std::max(r_in, r_out) / (double)pranges.size();
+  }
+  if (p2p_ && flag_barrier_ && !fuse_pull && !bpull_.empty()) {
+    // reader-side pulls read every owner's w_global: after its last apply
+    // (this rank may not have been involved in that batch), and the readers
+    // hold off the owners' next apply (readers_, replicated on every rank)
+    if (!pranges.empty() && last_apply_epoch_ > 0) {
+      std::vector<const unsigned long long*> wait;
+      for (int q = 0; q < G_; ++q) wait.push_back(flag_word(rank_, 2, q));
+      if (hp_status st = flag_ops(xs_, {}, wait, last_apply_epoch_)) return st;
+    }
+    for (int v : bpull_)
+      for (int q = 0; q < G_; ++q) readers_[q] |= lay_[q].has[v];
   }
   for (auto& rg : pranges) {
     TickDesc d;
@@ -597,6 +648,30 @@ hp_status Engine::flush_lockstep(int slot) {
   return HP_OK;
 }
 
+unsigned long long* Engine::flag_word(int q, int kind, int src) const {
+  return (unsigned long long*)(peer_[q] + lay_[q].flag_off) + (size_t)kind * G_ + src;
+}
+
+// Flag publications and waits on stream st (chunks of 8), profiled like the
+// barrier (shape nf = 126).
+hp_status Engine::flag_ops(cudaStream_t st, std::vector<unsigned long long*> sig,
+                           std::vector<const unsigned long long*> wait, uint64_t val) {
+  size_t i = 0, j = 0;
+  while (i < sig.size() || j < wait.size()) {
+    FlagOps fo;
+    memset(&fo, 0, sizeof fo);
+    fo.val = val;
+    fo.err = flag_err_;
+    for (; i < sig.size() && fo.nsig < 8; ++i) fo.sig[fo.nsig++] = sig[i];
+    for (; j < wait.size() && fo.nwait < 8; ++j) fo.wait[fo.nwait++] = wait[j];
+    stress(st);
+    prof_begin(st);
+    if (int e = launch_flag_ops(fo, st)) return check_cuda(e, "flag ops");
+    prof_end(st, 0.0, 0.0, 126 << 24);
+  }
+  return HP_OK;
+}
+
 void Engine::fork_streams() {
   if (forked_) return;
   cudaEvent_t e = pool_event();
@@ -680,6 +755,8 @@ hp_status Engine::connect_symmetric(const void* const* bases, void* mc, const vo
 
 hp_status Engine::finish_connect(const void* comm_id) {
   if (const char* fb = getenv("HP_FLAG_BARRIER")) flag_barrier_ = atoi(fb) != 0;
+  if (const char* pp = getenv("HP_P2P")) p2p_ = atoi(pp) != 0;
+  readers_.assign(G_, 0);
   if (comm_id) {
     std::string err;
     comm_ = comm_create(comm_id, G_, rank_, &err);
@@ -729,6 +806,10 @@ hp_status Engine::finish_connect(const void* comm_id) {
     }
   if (const char* xb = getenv("HP_XBLOCKS")) xblocks_ = atoi(xb);
   if (const char* ab = getenv("HP_ABLOCKS")) ablocks_ = atoi(ab);
+  // HP_AGRID=1: accumulation launches non-persistent (CTAs retire every U
+  // chunks), so the high-priority exchange stream's launches start promptly
+  if (const char* ag = getenv("HP_AGRID"))
+    if (atoi(ag) == 1) ablocks_ = -1;
   // everyone's init writes are complete before anyone reads a peer (without a
   // communicator: the first flag barrier, epoch 1 on every rank -- the flag
   // arrays were zeroed by every rank's hp_init_ex, which the caller ordered

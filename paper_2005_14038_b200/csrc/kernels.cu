@@ -171,7 +171,7 @@ __device__ __forceinline__ void complete_load(const DComplete& c, int64_t q0, in
   }
 }
 // ... and the rest: u, the wave aggregate, apply-now, inline fold.
-template <int GM, bool MOM, int U, int CNT>
+template <int GM, bool MOM, int U, int CNT, bool LEAN = false>
 __device__ __forceinline__ void complete_finish(const TickDesc& d, const DComplete& c, int64_t q0,
                                                 int64_t qs, const float4* ain, const float4* win,
                                                 const float4* gin, float4* wg, float4* mm) {
@@ -186,7 +186,7 @@ __device__ __forceinline__ void complete_finish(const TickDesc& d, const DComple
     if (fl & kSnapAcc) st4<CNT>(c.snap, q, ain[x]);          // F > 1: acc at the gate
     const float4 a = (fl & kFirst) ? u : f4add(ain[x], u);   // wave aggregate
     if (fl & kStoreAcc) st4<CNT>(c.acc, q, a);
-    if (fl & kApplyNow) apply<MOM>(wg[x], mm[x], a, d.mu);
+    if (!LEAN && (fl & kApplyNow)) apply<MOM>(wg[x], mm[x], a, d.mu);
     if (fl & kFoldInline) {
       const float4 w = f4add(win[x], u);
       st4<CNT>(c.wl, q, w);
@@ -199,8 +199,20 @@ __device__ __forceinline__ void complete_finish(const TickDesc& d, const DComple
 // tick_desc.h. Inside each op the loads of all U chunks are issued together,
 // so a thread keeps U (or 2U-3U) 16-byte requests in flight per op while its
 // register footprint stays independent of the number of ops in the tick.
-template <int GM, bool MOM, int U, int CNT>
+template <int GM, bool MOM, int U, int CNT, bool LEAN = false>
 __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64_t qs) {
+  if constexpr (LEAN) {
+    // completes only (no applies, w_global, groups or pull stores: Engine
+    // picks this instance only for such launches): phase B alone, so the
+    // w_global / momentum registers are never live -- fewer registers, more
+    // CTAs per SM, more loads in flight for the 1-3 stream launches
+    for (int j = 0; j < d.nc; ++j) {
+      float4 ain[U], win[U], gin[U];
+      complete_load<GM, U, CNT>(d.c[j], q0, qs, ain, win, gin);
+      complete_finish<GM, false, U, CNT, true>(d, d.c[j], q0, qs, ain, win, gin, nullptr, nullptr);
+    }
+    return;
+  }
   float4 wg[U], mm[U];
 #pragma unroll
   for (int x = 0; x < U; ++x) {
@@ -367,7 +379,7 @@ __device__ __forceinline__ void prefetch_round(const TickDesc& d, int64_t qb, in
   }
 }
 
-template <int GM, bool MOM, int U, bool PF, bool DYN>
+template <int GM, bool MOM, int U, bool PF, bool DYN, bool LEAN = false>
 __device__ __forceinline__ void tick_body(const TickDesc& d) {
   // Programmatic dependent launch: this grid may start while the previous tick
   // kernel drains; it touches no global memory before the previous grid has
@@ -400,10 +412,10 @@ __device__ __forceinline__ void tick_body(const TickDesc& d) {
       const int j1 = j == 2 ? 0 : j + 1, j2 = j1 == 2 ? 0 : j1 + 1;
       if (PF && nxt[j1] < T) prefetch_round<GM, MOM, U, 256>(d, nxt[j1] * 256 * U, 256, threadIdx.x);
       if (threadIdx.x == 0) nxt[j2] = (long long)atomicAdd(d.ctr, 1ull);
-      tick_chunks<GM, MOM, U, 4>(d, k * 256 * U + threadIdx.x, 256);
+      tick_chunks<GM, MOM, U, 4, LEAN>(d, k * 256 * U + threadIdx.x, 256);
       __syncthreads();
     }
-    for (q = T * 256 * U + t0; q < nfull; q += S) tick_chunks<GM, MOM, 1, 4>(d, q, S);
+    for (q = T * 256 * U + t0; q < nfull; q += S) tick_chunks<GM, MOM, 1, 4, LEAN>(d, q, S);
   } else {
     const int64_t groups = nfull / (S * U);          // rounds where every thread has U chunks
     const int64_t cta0 = (int64_t)blockIdx.x * blockDim.x;   // this CTA's first chunk, round 0
@@ -412,18 +424,18 @@ __device__ __forceinline__ void tick_body(const TickDesc& d) {
         prefetch_round<GM, MOM, U, 256>(d, cta0 + r * S * U, S, threadIdx.x);
       for (int64_t r = 0; r < groups; ++r, q += S * U) {
         if (r + d.pf < groups) prefetch_round<GM, MOM, U, 256>(d, cta0 + (r + d.pf) * S * U, S, threadIdx.x);
-        tick_chunks<GM, MOM, U, 4>(d, q, S);
+        tick_chunks<GM, MOM, U, 4, LEAN>(d, q, S);
       }
     } else {
-      for (int64_t r = 0; r < groups; ++r, q += S * U) tick_chunks<GM, MOM, U, 4>(d, q, S);
+      for (int64_t r = 0; r < groups; ++r, q += S * U) tick_chunks<GM, MOM, U, 4, LEAN>(d, q, S);
     }
-    for (; q < nfull; q += S) tick_chunks<GM, MOM, 1, 4>(d, q, S);
+    for (; q < nfull; q += S) tick_chunks<GM, MOM, 1, 4, LEAN>(d, q, S);
   }
   if (t0 == 0) {
     switch (d.n & 3) {
-      case 1: tick_chunks<GM, MOM, 1, 1>(d, nfull, 0); break;
-      case 2: tick_chunks<GM, MOM, 1, 2>(d, nfull, 0); break;
-      case 3: tick_chunks<GM, MOM, 1, 3>(d, nfull, 0); break;
+      case 1: tick_chunks<GM, MOM, 1, 1, LEAN>(d, nfull, 0); break;
+      case 2: tick_chunks<GM, MOM, 1, 2, LEAN>(d, nfull, 0); break;
+      case 3: tick_chunks<GM, MOM, 1, 3, LEAN>(d, nfull, 0); break;
       default: break;
     }
   }
@@ -443,9 +455,24 @@ template <int GM, bool MOM, int U, bool PF, bool DYN>
 __global__ void __launch_bounds__(256) tick_kernel(const __grid_constant__ TickDesc d) {
   tick_body<GM, MOM, U, PF, DYN>(d);
 }
+// (with momentum the U = 2 body needs more than 64 registers -- it spilled 16
+// bytes under the 4-CTA cap -- so those instances are capped for 3 CTAs/SM)
+#ifndef HP_MOM_O4_CTAS
+#define HP_MOM_O4_CTAS 3
+#endif
 template <int GM, bool MOM, int U, bool PF, bool DYN>
-__global__ void __launch_bounds__(256, 4) tick_kernel_o4(const __grid_constant__ TickDesc d) {
+__global__ void __launch_bounds__(256, (MOM ? HP_MOM_O4_CTAS : 4))
+    tick_kernel_o4(const __grid_constant__ TickDesc d) {
   tick_body<GM, MOM, U, PF, DYN>(d);
+}
+// Completes-only launches (TickDesc::lean): phase B alone, capped for 4
+// resident CTAs per SM (the general U = 4 instances hold 124 registers, 2 CTAs);
+// 3 for the EXTERNAL / CONVEX gradients, which load one more stream per
+// complete and would spill under 64 registers.
+template <int GM, bool PF, bool DYN>
+__global__ void __launch_bounds__(256, (GM >= 2 ? 3 : 4))
+    tick_kernel_lean(const __grid_constant__ TickDesc d) {
+  tick_body<GM, false, 4, PF, DYN, true>(d);
 }
 
 // Multi-tick kernel for launch-bound (small) models (hp_schedule_capture on a
@@ -609,6 +636,32 @@ __global__ void flag_barrier_kernel(const __grid_constant__ FlagBarrier fb) {
   __syncthreads();
 }
 
+// Point-to-point flags (FlagOps): lane i < nsig publishes val into sig[i]
+// (release, system scope, after a system fence), lane i < nwait waits for
+// wait[i] >= val (acquire); 10 s deadline as the barrier.
+__global__ void flag_ops_kernel(const __grid_constant__ FlagOps fo) {
+  const int i = threadIdx.x;
+  if (i < fo.nsig) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fo.sig[i]), "l"(fo.val) : "memory");
+  }
+  if (i < fo.nwait) {
+    unsigned long long t0, t, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(fo.wait[i]) : "memory");
+      if (v >= fo.val) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) {
+        if (fo.err) atomicExch(fo.err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
 // w0 (Z8): zero or Philox stream 1, counter (i>>2, 0, 0, 1).
 __global__ void init_kernel(float* out, int64_t n, int64_t param_begin, int w0_mode,
                             int grad_mode, uint32_t k0, uint32_t k1) {
@@ -631,10 +684,11 @@ int g_u_override = -1;   // HP_TICK_U: tuning override of chunks per thread
 int g_pdl = 1;           // HP_PDL=0 disables programmatic dependent launch
 int g_grid = 0;          // HP_GRID=1: one round of U chunks per thread (non-persistent)
 
-template <int GM, bool MOM, int U, bool PF, bool DYN>
+template <int GM, bool MOM, int U, bool PF, bool DYN, bool LEAN = false>
 int launch_u(const TickDesc& d, cudaStream_t s, int max_blocks) {
   void (*kern)(const TickDesc);
-  if constexpr (DYN && U == 2 && GM != 3) kern = tick_kernel_o4<GM, MOM, U, PF, DYN>;
+  if constexpr (LEAN) kern = tick_kernel_lean<GM, PF, DYN>;
+  else if constexpr (DYN && U == 2 && GM != 3) kern = tick_kernel_o4<GM, MOM, U, PF, DYN>;
   else kern = tick_kernel<GM, MOM, U, PF, DYN>;
   static int grid_max = 0;
   if (grid_max == 0) {
@@ -645,8 +699,11 @@ int launch_u(const TickDesc& d, cudaStream_t s, int max_blocks) {
     grid_max = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int64_t chunks = (d.n + 3) >> 2;
-  int64_t blocks = g_grid == 1 ? (chunks + 256 * U - 1) / (256 * U) : (chunks + 255) / 256;
-  if (g_grid != 1 && blocks > grid_max) blocks = grid_max;
+  // max_blocks < 0: this launch non-persistent (one round of U chunks per
+  // thread), so a higher-priority stream's kernel gets SMs as its CTAs retire
+  const bool np = g_grid == 1 || max_blocks < 0;
+  int64_t blocks = np ? (chunks + 256 * U - 1) / (256 * U) : (chunks + 255) / 256;
+  if (!np && blocks > grid_max) blocks = grid_max;
   if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   if (blocks > 0x7fffffff) blocks = 0x7fffffff;
   if (blocks < 1) blocks = 1;
@@ -674,6 +731,10 @@ int launch_gm(const TickDesc& d, cudaStream_t s, int mb) {
   // their code; the engine asks for it only on launches with few load streams
   // (complete-only, hence U = 4)
   const bool dyn = d.ctr != nullptr;
+  if (u >= 4 && d.lean) {
+    if (d.pf > 0) return dyn ? launch_u<GM, false, 4, true, true, true>(d, s, mb) : launch_u<GM, false, 4, true, false, true>(d, s, mb);
+    return dyn ? launch_u<GM, false, 4, false, true, true>(d, s, mb) : launch_u<GM, false, 4, false, false, true>(d, s, mb);
+  }
   if (u >= 4) {
     if (d.pf > 0) return dyn ? launch_u<GM, MOM, 4, true, true>(d, s, mb) : launch_u<GM, MOM, 4, true, false>(d, s, mb);
     return dyn ? launch_u<GM, MOM, 4, false, true>(d, s, mb) : launch_u<GM, MOM, 4, false, false>(d, s, mb);
@@ -812,6 +873,12 @@ void preload_gm() {
   if constexpr (GM != 3) cudaFuncGetAttributes(&a, tick_kernel_o4<GM, MOM, 2, false, true>);
   else cudaFuncGetAttributes(&a, tick_kernel<GM, MOM, 2, false, true>);
   cudaFuncGetAttributes(&a, tick_kernel<GM, MOM, 2, false, false>);
+  if (!MOM) {
+    cudaFuncGetAttributes(&a, tick_kernel_lean<GM, true, true>);
+    cudaFuncGetAttributes(&a, tick_kernel_lean<GM, true, false>);
+    cudaFuncGetAttributes(&a, tick_kernel_lean<GM, false, true>);
+    cudaFuncGetAttributes(&a, tick_kernel_lean<GM, false, false>);
+  }
 }
 
 int preload_kernels() {
@@ -831,6 +898,7 @@ int preload_kernels() {
                    nvls_kernel<4, false>, nvls_kernel<8, true>, nvls_kernel<8, false>})
       cudaFuncGetAttributes(&a, k);
     cudaFuncGetAttributes(&a, flag_barrier_kernel);
+    cudaFuncGetAttributes(&a, flag_ops_kernel);
     for (auto k : {multi_tick_kernel<0, false>, multi_tick_kernel<0, true>,
                    multi_tick_kernel<1, false>, multi_tick_kernel<1, true>,
                    multi_tick_kernel<3, false>, multi_tick_kernel<3, true>})
@@ -845,6 +913,11 @@ int preload_kernels() {
 
 int launch_flag_barrier(const FlagBarrier& fb, void* stream) {
   flag_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(fb);
+  return (int)cudaGetLastError();
+}
+
+int launch_flag_ops(const FlagOps& fo, void* stream) {
+  flag_ops_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(fo);
   return (int)cudaGetLastError();
 }
 

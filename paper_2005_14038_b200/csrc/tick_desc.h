@@ -113,6 +113,8 @@ struct TickDesc {
   int32_t np;                   // store targets of the owner-side pull
   int32_t pf;                   // L2 prefetch distance in chunk rounds (0 = off;
                                 // only when every load of the launch is local)
+  int32_t lean;                 // completes only (no applies / w_global / groups /
+                                // pull stores): the phase-B-only kernel instance
   unsigned long long* ctr;      // dynamic tile scheduling (nullptr = static grid
   unsigned int* done;           // stride): tile counter and finished-CTA count of
                                 // the launch stream, both 0 between launches
@@ -188,6 +190,20 @@ struct FlagBarrier {
   int32_t G, me;
 };
 int launch_flag_barrier(const FlagBarrier& fb, void* stream);
+
+// Point-to-point readiness flags (engine_dist.cpp): one
+// tiny kernel that publishes `val` into up to 8 flag words (after a system
+// fence: everything earlier on the stream is visible to whoever sees a flag)
+// and waits until up to 8 flag words hold >= `val`. Flags are monotonic
+// epochs, so a later signal satisfies an earlier wait.
+struct FlagOps {
+  unsigned long long* sig[8];
+  const unsigned long long* wait[8];
+  unsigned long long val;
+  int* err;                    // device int set to 1 if a wait timed out
+  int32_t nsig, nwait;
+};
+int launch_flag_ops(const FlagOps& fo, void* stream);
 // Run `count` tick descriptors (device memory, in order) in one launch over
 // [0, n) of a single-rank context (static element -> thread map; FLOAT,
 // DYADIC, CONVEX). Returns a cudaError_t as int.

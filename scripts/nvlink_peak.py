@@ -27,16 +27,23 @@ sys.path.insert(0, ROOT)
 
 
 def timed(pairs, nbytes, reps=5):
-    """Concurrent copies src -> dst for (src, dst) in pairs; GB/s per copy."""
+    """Concurrent copies src -> dst for (src, dst) in pairs: (GB/s of one copy
+    alone by its own CUDA events -- the slowest, and the aggregate GB/s of all
+    copies over the host wall time from the first issue to the last
+    completion, every device synchronised on both sides)."""
+    import time
     bufs = []
     for s, d in pairs:
         a = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{s}")
         b = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{d}")
         st = torch.cuda.Stream(device=s)
         bufs.append((a, b, st, s))
-    out = []
+    per, agg = [], []
     for rep in range(reps + 1):
+        for d in range(torch.cuda.device_count()):
+            torch.cuda.synchronize(d)
         evs = []
+        t0 = time.perf_counter()
         for a, b, st, s in bufs:
             with torch.cuda.device(s), torch.cuda.stream(st):
                 e0 = torch.cuda.Event(enable_timing=True)
@@ -47,9 +54,40 @@ def timed(pairs, nbytes, reps=5):
                 evs.append((e0, e1))
         for d in range(torch.cuda.device_count()):
             torch.cuda.synchronize(d)
+        dt = time.perf_counter() - t0
         if rep:
-            out.append(min(nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9 for e0, e1 in evs))
-    return statistics.median(out)
+            per.append(min(nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9 for e0, e1 in evs))
+            agg.append(len(bufs) * nbytes / dt / 1e9)
+    return statistics.median(per), statistics.median(agg)
+
+
+def nvml_probe(index=0):
+    """What NVML reports for this GPU's NVLinks (states, and the data
+    counters bench.py reads), to debug an unsupported field."""
+    out = {}
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        states = {}
+        for link in range(18):
+            try:
+                states[link] = int(pynvml.nvmlDeviceGetNvLinkState(h, link))
+            except Exception as e:
+                states[link] = repr(e)[:60]
+        out["link_state"] = states
+        for fid in (138, 139, 140, 141, 202, 204):
+            res = {}
+            for scope in (0, 1, 0xFFFFFFFF):
+                try:
+                    v = pynvml.nvmlDeviceGetFieldValues(h, [(fid, scope)])[0]
+                    res[str(scope)] = [int(v.nvmlReturn), int(v.value.ullVal)]
+                except Exception as e:
+                    res[str(scope)] = repr(e)[:80]
+            out[f"field_{fid}"] = res
+    except Exception as e:
+        out["error"] = repr(e)
+    return out
 
 
 def main():
@@ -67,18 +105,19 @@ def main():
     import bench
     nv = bench.NvlinkCounters(0)
     c0 = nv.read()
-    uni = timed([(0, 1)], n)
+    uni, _ = timed([(0, 1)], n)
     c1 = nv.read()
-    bidir = timed([(0, 1), (1, 0)], n)
-    ingress = timed([(q, 0) for q in range(1, G)], n)
-    egress = timed([(0, q) for q in range(1, G)], n)
+    bidir, bidir_agg = timed([(0, 1), (1, 0)], n)
+    ing1, ingress = timed([(q, 0) for q in range(1, G)], n)
+    eg1, egress = timed([(0, q) for q in range(1, G)], n)
     res = {
         "gpus": G, "name": torch.cuda.get_device_name(0), "bytes": n,
-        "uni_GBps": uni, "bidir_GBps_per_direction": bidir,
-        "ingress_GBps_per_source": ingress, "ingress_GBps_total": ingress * (G - 1),
-        "egress_GBps_per_dest": egress, "egress_GBps_total": egress * (G - 1),
-        # the per-direction peak of one GPU's links: the best of the measured forms
-        "peer_copy_GBps_per_direction": max(uni, bidir, ingress * (G - 1), egress * (G - 1)),
+        "uni_GBps": uni, "bidir_GBps_per_direction": bidir_agg / 2,
+        "ingress_GBps_total": ingress, "ingress_slowest_copy_GBps": ing1,
+        "egress_GBps_total": egress, "egress_slowest_copy_GBps": eg1,
+        # the per-direction peak of one GPU's links: the best aggregate measured
+        "peer_copy_GBps_per_direction": max(uni, bidir_agg / 2, ingress, egress),
+        "nvml_probe": nvml_probe(0),
         "nvml_counter_check": (None if c0 is None or c1 is None else
                                {"field": nv.field, "tx_bytes": c1[0] - c0[0],
                                 "rx_bytes": c1[1] - c0[1],

@@ -3,6 +3,8 @@
 // tests check the engine's host logic against the oracle. Compiled with
 // -ffp-contract=off so every float op rounds once, as __fadd_rn/__fmul_rn do.
 #include <stdint.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../../paper_2005_14038_b200/csrc/tick_desc.h"
 
@@ -126,6 +128,19 @@ int launch_multi_tick(const TickDescPad* descs, int count, int64_t, int grad_mod
 int launch_spin(unsigned long long, void*) { return 0; }
 
 // K7 flag barrier on host threads (ranks are threads of one process here)
+int launch_flag_ops(const FlagOps& fo, void*) {
+  for (int i = 0; i < fo.nsig; ++i) __atomic_store_n(fo.sig[i], fo.val, __ATOMIC_RELEASE);
+  for (int i = 0; i < fo.nwait; ++i) {
+    long spins = 0;
+    while (__atomic_load_n(fo.wait[i], __ATOMIC_ACQUIRE) < fo.val) {
+      if (++spins == 2000000000L && getenv("HP_EMU_DEBUG"))
+        fprintf(stderr, "flag wait stuck: word %p val %llu have %llu\n", (void*)fo.wait[i],
+                fo.val, (unsigned long long)__atomic_load_n(fo.wait[i], __ATOMIC_ACQUIRE));
+    }
+  }
+  return 0;
+}
+
 int launch_flag_barrier(const FlagBarrier& fb, void*) {
   for (int q = 0; q < fb.G; ++q) __atomic_store_n(fb.flags[q] + fb.me, fb.epoch, __ATOMIC_RELEASE);
   for (int q = 0; q < fb.G; ++q)

@@ -29,6 +29,9 @@ CASES = [
     ("C5-G4-mom", C5.replace(nparams=3001, waves=3, D=4, num_vw=4, tau=C5.tau[:4]), 4, 1, {}),
     ("convexF", WSPConfig("cf", 3, 2, 1, 2053, 4, (3, 5, 4), grad_mode=3, lr=0.05, F=2), 3, 1, {}),
     ("split-F2", WSPConfig("sf", 3, 2, 1, 1030, 4, (3, 7, 4), F=2), 2, 1, {"split": "1"}),
+    ("barriers", C3.replace(nparams=4099, waves=5), 4, 1, {"HP_P2P": "0"}),
+    ("reader-F3", WSPConfig("r3", 4, 1, 0, 333, 4, (3, 9, 4, 8), momentum=0.9, F=3), 3, 2,
+     {"HP_PULL_PUSH": "0"}),
 ]
 
 
@@ -37,6 +40,9 @@ def test_colocated_emu_parity(emu, monkeypatch, name, cfg, G, k, env):
     hetpipe, lib = emu
     if env.get("split"):
         monkeypatch.setenv("HP_SPLIT_FOLDS", "1")
+    for k_, v_ in env.items():
+        if k_.startswith("HP_"):
+            monkeypatch.setenv(k_, v_)
     out = run_colocated(hetpipe, cfg, G, k, host_alloc, lib=lib, timeout=120)
     check(cfg, G, k, out)
 

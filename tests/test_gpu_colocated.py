@@ -80,6 +80,11 @@ CASES = [
      {"HP_SPLIT_FOLDS": "1"}),
     ("lazy-split-G2", WSPConfig("ls", 3, 3, 1, 12_345, 7, (3, 5, 4), pull_policy=1,
                                 local_semantics=1), 2, 1, False, {"HP_SPLIT_FOLDS": "1"}),
+    # the all-rank barriers instead of the point-to-point flags (DESIGN 9h), and
+    # non-persistent accumulation grids
+    ("C3-G4-barriers", C3.replace(nparams=40_000, waves=6), 4, 1, False, {"HP_P2P": "0"}),
+    ("C5-G4-barriers", C5.replace(nparams=40_003, waves=3, D=4), 4, 1, False, {"HP_P2P": "0"}),
+    ("C3-G4-k2-agrid", C3.replace(nparams=40_000, waves=6), 4, 2, False, {"HP_AGRID": "1"}),
     # bounded exchange / accumulation grids (co-scheduling knobs of DESIGN 9f)
     ("C3-G4-grids", C3.replace(nparams=40_000, waves=6), 4, 1, False,
      {"HP_XBLOCKS": "80", "HP_ABLOCKS": "216"}),
