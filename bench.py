@@ -373,6 +373,7 @@ def measure(cfg, span, args, ws, rank, local, stream, steps, warmup, profile_ste
         g.close()
     else:
         ctx.schedule_advance(N * warmup)
+        ctx.flush()
     torch.cuda.synchronize()
     barrier()
     st0 = ctx.stats()
@@ -389,6 +390,7 @@ def measure(cfg, span, args, ws, rank, local, stream, steps, warmup, profile_ste
     else:
         for k in range(steps):
             ctx.schedule_advance(N * (warmup + k + 1))
+        ctx.flush()                  # join the side streams before the end event
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -435,6 +437,7 @@ def profiled_pass(ctx, N, done_steps, prof_steps, stream, barrier):
     pe0.record(stream)
     for k in range(prof_steps):
         ctx.schedule_advance(N * (done_steps + k + 1))
+    ctx.flush()
     pe1.record(stream)
     torch.cuda.synchronize()
     barrier()

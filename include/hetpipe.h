@@ -242,7 +242,9 @@ hp_status hp_pull(hp_ctx* ctx, int32_t vw);
    disjoint VW state and launched at the latest by hp_flush / hp_sync /
    hp_read_weights / the return of hp_schedule_advance. */
 hp_status hp_tick_end(hp_ctx* ctx);
-/* Launch every pending fused op batch (asynchronous; no stream sync). */
+/* Launch every pending fused op batch and order all launched work (also a
+   distributed context's side streams) before later work on the context stream
+   (asynchronous; no host sync). */
 hp_status hp_flush(hp_ctx* ctx);
 
 /* Stamp subsequent trace records with tick t (wait accounting uses it). */
@@ -254,7 +256,12 @@ hp_status hp_set_tick(hp_ctx* ctx, int64_t t);
    tau, lat: host int64[num_vw]; lat NULL = N_m * tau. */
 hp_status hp_schedule_begin(hp_ctx* ctx, const int64_t* tau, const int64_t* lat);
 /* Run ticks until the commit log holds >= target_commits pushes or the run is
-   complete; *commits (may be NULL) receives the count reached. */
+   complete; *commits (may be NULL) receives the count reached. Every op of
+   those ticks is launched on return. A distributed context's accumulation /
+   exchange / fold streams are NOT joined to the context stream here (the next
+   call's accumulation may overlap this one's exchange, row a9): call hp_flush
+   (or hp_sync) before work on the context stream that must follow them, e.g.
+   a timing event. */
 hp_status hp_schedule_advance(hp_ctx* ctx, int64_t target_commits, int64_t* commits);
 /* CUDA-graph form of hp_schedule_advance, for launch-bound (small) models on
    single-rank contexts (world = 1; a distributed context gets HP_ERR_STATE):

@@ -50,7 +50,10 @@ class Controller {
       if (events_.empty()) return e_->fail(HP_ERR_STATE, "deadlock: no pending completion");
       if (hp_status st = tick()) return st;
     }
-    return e_->flush_pending();   // everything committed so far is enqueued
+    // everything committed so far is launched; distributed contexts leave
+    // their side streams running (the next advance's accumulation may overlap
+    // this one's exchange): hp_flush / hp_sync join them to the context stream
+    return e_->flush_queued();
   }
   void set_host_grads(const float* const* bufs, int n) { host_.assign(bufs, bufs + n); }
   bool host_grads() const { return !host_.empty(); }

@@ -1034,13 +1034,20 @@ hp_status Engine::sync() {
   if (hp_status st = join_exchange()) return st;
   if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "sync")) return st;
   if (flag_err_) {                     // a K7 flag wait ran past its deadline
-    int bad = 0;
-    if (hp_status st = check_cuda(cudaMemcpy(&bad, flag_err_, sizeof bad, cudaMemcpyDeviceToHost),
+    int bad[8] = {0};
+    if (hp_status st = check_cuda(cudaMemcpy(bad, flag_err_, sizeof bad, cudaMemcpyDeviceToHost),
                                   "flag error"))
       return st;
-    if (bad) {
+    if (bad[0]) {
       sticky_ = HP_ERR_COMM;
-      return fail(HP_ERR_COMM, "K7 readiness flag wait timed out (a rank stopped issuing barriers)");
+      char buf[256];
+      snprintf(buf, sizeof buf,
+               "K7 readiness flag wait timed out (a rank stopped issuing barriers): rank %d "
+               "waited for epoch %d, word held %d (wait %d of %d, %d signals; epochs: barrier "
+               "%llu, apply %llu)",
+               rank_, bad[1], bad[2], bad[3], bad[5], bad[4], (unsigned long long)epoch_,
+               (unsigned long long)xepoch_);
+      return fail(HP_ERR_COMM, buf);
     }
   }
   return HP_OK;

@@ -83,9 +83,15 @@ class Engine {
   bool distributed() const { return dist_; }
   int64_t local_len(int which) const;
   double nvl_bytes() const { return nvl_bytes_; }
-  hp_status flush_pending() {
+  // launch every queued op (side streams keep running)
+  hp_status flush_queued() {
     if (!(bc_.empty() && ba_.empty() && bpull_.empty() && !has_due_folds()))
       if (hp_status st = flush()) return st;
+    return HP_OK;
+  }
+  // ... and order all of it before later work on the context stream
+  hp_status flush_pending() {
+    if (hp_status st = flush_queued()) return st;
     return join_exchange();
   }
   hp_status sync();

@@ -770,8 +770,8 @@ hp_status Engine::finish_connect(const void* comm_id) {
       return fail(HP_ERR_STATE, "HP_XPORT_NCCL needs a communicator id");
   }
   if (flag_barrier_) {
-    if (int e = cudaMalloc((void**)&flag_err_, sizeof(int))) return check_cuda(e, "flag error");
-    if (int e = cudaMemset(flag_err_, 0, sizeof(int))) return check_cuda(e, "flag error");
+    if (int e = cudaMalloc((void**)&flag_err_, 8 * sizeof(int))) return check_cuda(e, "flag error");
+    if (int e = cudaMemset(flag_err_, 0, 8 * sizeof(int))) return check_cuda(e, "flag error");
   }
   // Stream priorities (HP_PRIO, default on): the exchange and the folds that
   // wait for it are the round's critical path; the accumulation of the next

@@ -455,10 +455,11 @@ template <int GM, bool MOM, int U, bool PF, bool DYN>
 __global__ void __launch_bounds__(256) tick_kernel(const __grid_constant__ TickDesc d) {
   tick_body<GM, MOM, U, PF, DYN>(d);
 }
-// (with momentum the U = 2 body needs more than 64 registers -- it spilled 16
-// bytes under the 4-CTA cap -- so those instances are capped for 3 CTAs/SM)
+// (with momentum the U = 2 body spills 16 bytes under the 4-CTA cap; capping
+// it for 3 CTAs/SM instead measured 3% slower on C5's momentum round-end
+// launch, 4536 vs 4659 GB/s, profiles/r02/c5_1gpu_mom_cap.txt -- kept at 4)
 #ifndef HP_MOM_O4_CTAS
-#define HP_MOM_O4_CTAS 3
+#define HP_MOM_O4_CTAS 4
 #endif
 template <int GM, bool MOM, int U, bool PF, bool DYN>
 __global__ void __launch_bounds__(256, (MOM ? HP_MOM_O4_CTAS : 4))
@@ -653,7 +654,13 @@ __global__ void flag_ops_kernel(const __grid_constant__ FlagOps fo) {
       if (v >= fo.val) break;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t - t0 > 10000000000ull) {
-        if (fo.err) atomicExch(fo.err, 1);
+        if (fo.err && atomicExch(fo.err, 1) == 0) {   // first timeout: what it waited for
+          fo.err[1] = (int)fo.val;
+          fo.err[2] = (int)v;
+          fo.err[3] = i;
+          fo.err[4] = fo.nsig;
+          fo.err[5] = fo.nwait;
+        }
         break;
       }
       __nanosleep(64);
