@@ -291,6 +291,11 @@ hp_status hp_run_schedule(hp_ctx* ctx, const int64_t* tau, const int64_t* lat);
    the device. */
 hp_status hp_schedule_set_host_grads(hp_ctx* ctx, const float* const* host_bufs, int32_t n);
 
+/* Wait for all LAUNCHED work (hp_flush, then synchronise the context stream):
+   unlike hp_sync, applies deferred to their first observer stay deferred
+   (reading Z4), so the batching is the one the run would have had anyway.
+   HP_ERR_COMM if a K7 flag wait timed out. */
+hp_status hp_drain(hp_ctx* ctx);
 /* Flush every pending op and apply, then synchronise the stream. */
 hp_status hp_sync(hp_ctx* ctx);
 

@@ -458,6 +458,12 @@ hp_status hp_schedule_set_host_grads(hp_ctx* ctx, const float* const* bufs, int3
   HP_EXIT(ctx)
 }
 
+hp_status hp_drain(hp_ctx* ctx) {
+  HP_ENTRY(ctx)
+  return ctx->eng->drain();
+  HP_EXIT(ctx)
+}
+
 hp_status hp_sync(hp_ctx* ctx) {
   HP_ENTRY(ctx)
   return ctx->eng->sync();

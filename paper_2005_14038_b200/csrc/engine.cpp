@@ -1025,6 +1025,14 @@ hp_status Engine::flush_applies() {
   return flush();
 }
 
+hp_status Engine::drain() {
+  if (sticky_) return sticky_;
+  if (capturing_ || graph_pending_) return fail(HP_ERR_STATE, "a captured graph has not been launched");
+  if (hp_status st = flush_pending()) return st;
+  if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "drain")) return st;
+  return check_flag_err();
+}
+
 hp_status Engine::sync() {
   if (sticky_) return sticky_;
   if (capturing_ || graph_pending_) return fail(HP_ERR_STATE, "a captured graph has not been launched");
@@ -1033,6 +1041,10 @@ hp_status Engine::sync() {
   if (hp_status st = flush_applies()) return st;
   if (hp_status st = join_exchange()) return st;
   if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "sync")) return st;
+  return check_flag_err();
+}
+
+hp_status Engine::check_flag_err() {
   if (flag_err_) {                     // a K7 flag wait ran past its deadline
     int bad[8] = {0};
     if (hp_status st = check_cuda(cudaMemcpy(bad, flag_err_, sizeof bad, cudaMemcpyDeviceToHost),

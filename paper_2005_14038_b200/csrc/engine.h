@@ -95,6 +95,8 @@ class Engine {
     return join_exchange();
   }
   hp_status sync();
+  hp_status drain();                  // launched work done (deferred applies stay deferred)
+  hp_status check_flag_err();         // HP_ERR_COMM if a K7 flag wait timed out
   hp_status read(int which, int64_t off, int64_t cnt, float* dst);
   // CUDA-graph capture of the device work of a controller advance
   // (hp_schedule_capture): begin -> the caller advances -> end(graph exec)

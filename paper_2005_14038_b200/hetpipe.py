@@ -98,6 +98,7 @@ EXPORTS = {
     "hp_graph_launch": (C.c_int, [C.c_void_p]),
     "hp_graph_destroy": (None, [C.c_void_p]),
     "hp_launch_floor": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_float)]),
+    "hp_drain": (C.c_int, [C.c_void_p]),
     "hp_sync": (C.c_int, [C.c_void_p]),
     "hp_read_weights": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]),
     "hp_trace_dump": (C.c_int, [C.c_void_p, C.c_char_p]),
@@ -320,6 +321,10 @@ class Context:
 
     def sync(self) -> None:
         self._chk(self.lib.hp_sync(self.h))
+
+    def drain(self) -> None:
+        """hp_drain: launched work finished; deferred applies stay deferred."""
+        self._chk(self.lib.hp_drain(self.h))
 
     def read_weights(self, which: int, offset: int = 0, count: Optional[int] = None,
                      out: Optional[np.ndarray] = None) -> np.ndarray:

@@ -103,7 +103,7 @@ def check(cfg, G, k, objs, sampled=None, exact=True):
 
 
 def run_colocated(hetpipe, cfg, G, k, alloc, lib=None, sampled=None, bounds=None,
-                  host_grads=None, timeout=600.0, **over):
+                  host_grads=None, timeout=600.0, rounds_per_chunk=2, **over):
     """G ranks of a distributed placement as G threads of THIS process, each
     driving its own context; the arenas come from alloc(nbytes) -> (address,
     keepalive) (torch device memory on the GPU, numpy for the host emulation)
@@ -130,7 +130,20 @@ def run_colocated(hetpipe, cfg, G, k, alloc, lib=None, sampled=None, bounds=None
                 ctx.connect_symmetric(bases, 0, None)
                 if host_grads is not None:
                     ctx.schedule_set_host_grads(host_grads)
-                ctx.run_schedule(cfg.tau, cfg.latency())
+                # advance a bounded number of rounds at a time, then drain: the
+                # co-located ranks share ONE CUDA context, so one rank's host
+                # must not run so far ahead that its queued launches (blocked
+                # behind a flag wait for another rank) fill the context's
+                # command queue before the other rank has issued its signal
+                # (separate processes / GPUs have separate queues)
+                ctx.schedule_begin(cfg.tau, cfg.latency())
+                total = cfg.num_vw * cfg.waves
+                for target in range(cfg.num_vw * rounds_per_chunk, total + 1,
+                                    cfg.num_vw * rounds_per_chunk):
+                    ctx.schedule_advance(target)
+                    ctx.drain()
+                ctx.schedule_advance(total)
+                ctx.sync()
                 out[r] = collect(ctx, cfg, G, k, r, sampled, bounds)
             except Exception as e:  # reported below
                 errs.append((r, e))
