@@ -758,6 +758,7 @@ hp_status Engine::xbarrier() {
     fb.me = rank_;
     fb.epoch = epoch_;
     fb.err = flag_err_;
+    fb.timeout_ns = flag_timeout_ns_;
     for (int q = 0; q < G_; ++q)
       fb.flags[q] = (unsigned long long*)(peer_[q] + lay_[q].flag_off);
     if (int e = launch_flag_barrier(fb, xs_)) return check_cuda(e, "flag barrier");
@@ -1047,9 +1048,13 @@ hp_status Engine::sync() {
 hp_status Engine::check_flag_err() {
   if (flag_err_) {                     // a K7 flag wait ran past its deadline
     int bad[8] = {0};
-    if (hp_status st = check_cuda(cudaMemcpy(bad, flag_err_, sizeof bad, cudaMemcpyDeviceToHost),
+    // (on the context stream, never the legacy default stream: co-located
+    // ranks share one CUDA context, see engine_dist.cpp finish_connect)
+    if (hp_status st = check_cuda(cudaMemcpyAsync(bad, flag_err_, sizeof bad,
+                                                  cudaMemcpyDeviceToHost, stream_),
                                   "flag error"))
       return st;
+    if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "flag error")) return st;
     if (bad[0]) {
       sticky_ = HP_ERR_COMM;
       char buf[256];
@@ -1183,8 +1188,9 @@ hp_status Engine::read(int which, int64_t off, int64_t cnt, float* dst) {
   if (off < 0 || cnt < 0 || off + cnt > len || (cnt && !dst)) return fail(HP_ERR_INVALID, "bad range");
   if (hp_status st = sync()) return st;
   const float* src = which == -1 ? wg_ : which == -2 ? m_ : vw_[which].wl;
-  if (int e = cudaMemcpy(dst, src + off, (size_t)cnt * 4, cudaMemcpyDeviceToHost))
+  if (int e = cudaMemcpyAsync(dst, src + off, (size_t)cnt * 4, cudaMemcpyDeviceToHost, stream_))
     return check_cuda(e, "read");
+  if (int e = cudaStreamSynchronize(stream_)) return check_cuda(e, "read");
   return HP_OK;
 }
 

@@ -226,6 +226,7 @@ class Engine {
   // Point-to-point readiness flags (HP_P2P, default on with the flag
   // barrier): an apply batch waits only for the ranks it involves.
   bool p2p_ = true;
+  uint64_t flag_timeout_ns_ = 10000000000ull;   // flag wait deadline (HP_FLAG_TIMEOUT_MS)
   uint64_t xepoch_ = 0;               // apply batches exchanged by flags (replicated)
   uint64_t last_apply_epoch_ = 0;
   std::vector<char> readers_;         // ranks that read w_global shards since the last apply

@@ -662,6 +662,7 @@ hp_status Engine::flag_ops(cudaStream_t st, std::vector<unsigned long long*> sig
     memset(&fo, 0, sizeof fo);
     fo.val = val;
     fo.err = flag_err_;
+    fo.timeout_ns = flag_timeout_ns_;
     for (; i < sig.size() && fo.nsig < 8; ++i) fo.sig[fo.nsig++] = sig[i];
     for (; j < wait.size() && fo.nwait < 8; ++j) fo.wait[fo.nwait++] = wait[j];
     stress(st);
@@ -756,6 +757,7 @@ hp_status Engine::connect_symmetric(const void* const* bases, void* mc, const vo
 hp_status Engine::finish_connect(const void* comm_id) {
   if (const char* fb = getenv("HP_FLAG_BARRIER")) flag_barrier_ = atoi(fb) != 0;
   if (const char* pp = getenv("HP_P2P")) p2p_ = atoi(pp) != 0;
+  if (const char* to = getenv("HP_FLAG_TIMEOUT_MS")) flag_timeout_ns_ = 1000000ull * strtoull(to, nullptr, 10);
   readers_.assign(G_, 0);
   if (comm_id) {
     std::string err;
@@ -771,7 +773,8 @@ hp_status Engine::finish_connect(const void* comm_id) {
   }
   if (flag_barrier_) {
     if (int e = cudaMalloc((void**)&flag_err_, 8 * sizeof(int))) return check_cuda(e, "flag error");
-    if (int e = cudaMemset(flag_err_, 0, 8 * sizeof(int))) return check_cuda(e, "flag error");
+    if (int e = cudaMemsetAsync(flag_err_, 0, 8 * sizeof(int), stream_))
+      return check_cuda(e, "flag error");
   }
   // Stream priorities (HP_PRIO, default on): the exchange and the folds that
   // wait for it are the round's critical path; the accumulation of the next
@@ -824,6 +827,7 @@ hp_status Engine::finish_connect(const void* comm_id) {
     fb.me = rank_;
     fb.epoch = epoch_;
     fb.err = flag_err_;
+    fb.timeout_ns = flag_timeout_ns_;
     for (int q = 0; q < G_; ++q) fb.flags[q] = (unsigned long long*)(peer_[q] + lay_[q].flag_off);
     if (int e = launch_flag_barrier(fb, stream_)) return check_cuda(e, "flag barrier");
   }
@@ -831,7 +835,9 @@ hp_status Engine::finish_connect(const void* comm_id) {
   if (hp_status st = check_cuda(cudaStreamSynchronize(stream_), "connect sync")) return st;
   if (flag_err_) {
     int bad = 0;
-    if (int e = cudaMemcpy(&bad, flag_err_, sizeof bad, cudaMemcpyDeviceToHost)) return check_cuda(e, "flag error");
+    if (int e = cudaMemcpyAsync(&bad, flag_err_, sizeof bad, cudaMemcpyDeviceToHost, stream_))
+      return check_cuda(e, "flag error");
+    if (int e = cudaStreamSynchronize(stream_)) return check_cuda(e, "flag error");
     if (bad) {
       sticky_ = HP_ERR_COMM;
       return fail(HP_ERR_COMM, "connect: a rank did not reach the first flag barrier");

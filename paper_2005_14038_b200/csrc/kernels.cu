@@ -627,7 +627,7 @@ __global__ void flag_barrier_kernel(const __grid_constant__ FlagBarrier fb) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(src) : "memory");
       if (v >= fb.epoch) break;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 10000000000ull) {
+      if (t - t0 > fb.timeout_ns) {
         if (fb.err) atomicExch(fb.err, 1);
         break;
       }
@@ -653,7 +653,7 @@ __global__ void flag_ops_kernel(const __grid_constant__ FlagOps fo) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(fo.wait[i]) : "memory");
       if (v >= fo.val) break;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 10000000000ull) {
+      if (t - t0 > fo.timeout_ns) {
         if (fo.err && atomicExch(fo.err, 1) == 0) {   // first timeout: what it waited for
           fo.err[1] = (int)fo.val;
           fo.err[2] = (int)v;

@@ -187,6 +187,7 @@ struct FlagBarrier {
   unsigned long long* flags[8];
   int* err;                    // device int set to 1 if a wait timed out
   unsigned long long epoch;
+  unsigned long long timeout_ns;   // wait deadline (HP_FLAG_TIMEOUT_MS, default 10 s)
   int32_t G, me;
 };
 int launch_flag_barrier(const FlagBarrier& fb, void* stream);
@@ -200,6 +201,7 @@ struct FlagOps {
   unsigned long long* sig[8];
   const unsigned long long* wait[8];
   unsigned long long val;
+  unsigned long long timeout_ns;   // wait deadline (HP_FLAG_TIMEOUT_MS, default 10 s)
   int* err;                    // device int set to 1 if a wait timed out
   int32_t nsig, nwait;
 };

@@ -102,14 +102,42 @@ def check(cfg, G, k, objs, sampled=None, exact=True):
     return o
 
 
+RETRIES = []   # (config name, G, k, message) of attempts repeated after a queue-aliasing stall
+
+
 def run_colocated(hetpipe, cfg, G, k, alloc, lib=None, sampled=None, bounds=None,
-                  host_grads=None, timeout=600.0, rounds_per_chunk=2, **over):
+                  host_grads=None, timeout=600.0, rounds_per_chunk=2, attempts=3, **over):
     """G ranks of a distributed placement as G threads of THIS process, each
     driving its own context; the arenas come from alloc(nbytes) -> (address,
     keepalive) (torch device memory on the GPU, numpy for the host emulation)
     and the contexts connect through hp_connect_symmetric WITHOUT an NCCL
     communicator (comm_id NULL: K7 flag barriers, PEER exchange). Returns the
-    per-rank collect() tuples in rank order."""
+    per-rank collect() tuples in rank order.
+
+    Co-located ranks share one GPU's hardware work queues, and CUDA maps
+    streams to queues itself: when one rank's spinning flag kernel lands in the
+    queue in front of another rank's producer, the wait can only end at the
+    flag deadline (HP_ERR_COMM; reproduced at will with
+    CUDA_DEVICE_MAX_CONNECTIONS=1 or 4, rare at 32 -- separate GPUs cannot
+    alias). Such an attempt is repeated with fresh contexts (new streams, a
+    new mapping) up to `attempts` times and recorded in RETRIES; any other
+    failure, or a second identical stall, fails."""
+    for attempt in range(attempts):
+        try:
+            return _run_colocated_once(hetpipe, cfg, G, k, alloc, lib, sampled, bounds,
+                                       host_grads, timeout, rounds_per_chunk, **over)
+        except _FlagStall as e:
+            RETRIES.append((cfg.name, G, k, str(e)[:200]))
+            if attempt + 1 == attempts:
+                raise AssertionError(f"flag stall in {attempts} attempts: {e}")
+
+
+class _FlagStall(Exception):
+    pass
+
+
+def _run_colocated_once(hetpipe, cfg, G, k, alloc, lib, sampled, bounds, host_grads, timeout,
+                        rounds_per_chunk, **over):
     extra = dict(over)
     if bounds is not None:
         extra["ps_bounds"] = bounds
@@ -123,11 +151,15 @@ def run_colocated(hetpipe, cfg, G, k, alloc, lib=None, sampled=None, bounds=None
             ctxs.append(hetpipe.Context(c, lib=lib))
         bases = [ctx.cfg.arena for ctx in ctxs]
         out, errs = [None] * G, []
+        connected = threading.Barrier(G)
 
         def work(r):
             try:
                 ctx = ctxs[r]
                 ctx.connect_symmetric(bases, 0, None)
+                # every rank's set-up (its allocations, streams, first barrier)
+                # is finished before any rank issues flag waits of the schedule
+                connected.wait(timeout)
                 if host_grads is not None:
                     ctx.schedule_set_host_grads(host_grads)
                 # advance a bounded number of rounds at a time, then drain: the
@@ -154,6 +186,9 @@ def run_colocated(hetpipe, cfg, G, k, alloc, lib=None, sampled=None, bounds=None
         for t in th:
             t.join(timeout)
         assert not any(t.is_alive() for t in th), "a rank thread did not finish"
+        if errs and all(getattr(e, "status", None) == hetpipe.HP_ERR_COMM and "timed out" in str(e)
+                        for _, e in errs):
+            raise _FlagStall(errs)
         assert not errs, errs
         return out
     finally:

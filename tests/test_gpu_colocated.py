@@ -34,7 +34,19 @@ def hp():
     from paper_2005_14038_b200 import build, hetpipe
     build.build()
     hetpipe.load()
-    return hetpipe
+    # a flag wait stalled by hardware-queue aliasing (placement_check.run_colocated)
+    # ends at this deadline and the attempt is repeated
+    old = os.environ.get("HP_FLAG_TIMEOUT_MS")
+    os.environ["HP_FLAG_TIMEOUT_MS"] = "3000"
+    yield hetpipe
+    import placement_check
+    if placement_check.RETRIES:
+        print(f"\nco-located attempts repeated after a queue-aliasing stall: "
+              f"{len(placement_check.RETRIES)} {placement_check.RETRIES}")
+    if old is None:
+        os.environ.pop("HP_FLAG_TIMEOUT_MS", None)
+    else:
+        os.environ["HP_FLAG_TIMEOUT_MS"] = old
 
 
 def dev_alloc(nbytes):
