@@ -478,7 +478,12 @@ def profiled_pass(ctx, N, done_steps, prof_steps, stream, barrier):
     timeline = [{"start_ms": float(a), "ms": float(t), "shape": int(sh) & 0xFFFFFFFF,
                  "stream": int(sid), "bytes": float(by), "link_bytes": float(lk)}
                 for a, t, sh, sid, by, lk in zip(l_t0, l_ms, l_shape, l_stream, l_bytes, l_link)]
-    return {"prof_ms": ms, "timeline": timeline, "kern_ms": kern_ms, "kern_bytes": kern_bytes,
+    # distributed placements: device time of the exchange streams (barriers /
+    # flags, the owners' apply + owner-side pull launches, reader-side pulls) --
+    # push + apply + pull measured on their own streams
+    xs_ms = sum(float(t) for t, sid in zip(l_ms, l_stream) if int(sid) in (1, 2))
+    return {"prof_ms": ms, "timeline": timeline, "xs_ms": xs_ms, "kern_ms": kern_ms,
+            "kern_bytes": kern_bytes,
             "kern_launches": kern_launches, "busy_ms": busy_ms, "sync_ms": sync_ms,
             "pcommits": st1.commits - st0.commits,
             "sync_us": [1e3 * float(x) for x in s_ms],
@@ -782,6 +787,15 @@ def main():
             "launches": res["launches"],
             "alg_bytes_per_launch": res["alg_bytes"] / max(res["launches"], 1)},
         "exchange_roofline": xch,
+        "exchange_stream": ({"ms_per_step": res["xs_ms"] / prof_steps,
+                             "synced_params_per_s": res["pcommits"] * cfg.nparams /
+                             (res["xs_ms"] / 1e3) if res.get("xs_ms") else None,
+                             "def": "distributed placements, rank 0, profiled pass: device time "
+                                    "of the exchange stream(s) -- flag waits, the PS shard's apply "
+                                    "launches with the owner-side pull stores, reader-side pulls "
+                                    "-- i.e. push + apply + pull measured on their own stream "
+                                    "(waits for the other ranks included)"}
+                            if placed and res.get("xs_ms") else None),
         "nvlink": {"alg_bytes_per_step_max_rank": nvl_alg_max / args.steps,
                    "alg_GBps_over_step": nvl_alg_max / (res["ms_max"] / 1e3) / 1e9,
                    "measured": nv_meas,
