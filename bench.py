@@ -327,7 +327,8 @@ class Run:
         self.keep = None
         xport = {"peer": 0, "nccl": 1, "nvls": 2}[args.transport]
         self.placed = ws > 1 and span > 0
-        kw = dict(merge_ticks=args.merge_ticks, apply_mode=args.apply_mode)
+        kw = dict(merge_ticks=args.merge_ticks, apply_mode=args.apply_mode,
+                  acc_slots=args.acc_slots)
         kw.update(over)
         if self.placed and args.transport == "nvls":
             self.ctx, self.keep = hdist.symmetric_context(cfg, rank, ws, span, device=local,
@@ -570,6 +571,9 @@ def main():
                     help="N>1: skip the extra ED-local C2 and same-config 1-GPU measurements")
     ap.add_argument("--ref-params", type=int, default=1 << 18)
     ap.add_argument("--merge-ticks", type=int, default=1)
+    ap.add_argument("--acc-slots", type=int, default=2,
+                    help="acc ring depth R per VW (hp_config.acc_slots, 2..8): wave c uses "
+                         "slot c mod R; R > 2 lets a VW run further ahead of its unapplied pushes")
     ap.add_argument("--apply-mode", type=int, default=0,
                     help="0: defer PS applies to the observing pull; 1: apply on arrival")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl", "nvls"],
@@ -751,6 +755,7 @@ def main():
                             if args.grad == "convex" else "Philox FLOAT in-kernel"),
                    "pull": args.pull.upper(), "local": "STRICT",
                    "apply": "on arrival" if args.apply_mode else "deferred to the observing pull",
+                   "acc_slots": args.acc_slots,
                    "transport": args.transport if placed else None,
                    "ps_shards": args.ps if placed else None,
                    "lockstep_batches": res["lockstep"] if placed else None,

@@ -690,6 +690,7 @@ __global__ void init_kernel(float* out, int64_t n, int64_t param_begin, int w0_m
 int g_u_override = -1;   // HP_TICK_U: tuning override of chunks per thread
 int g_pdl = 1;           // HP_PDL=0 disables programmatic dependent launch
 int g_grid = 0;          // HP_GRID=1: one round of U chunks per thread (non-persistent)
+int g_apply_u = 0;       // HP_APPLY_U: chunks per thread of launches with >= 2 applies
 
 template <int GM, bool MOM, int U, bool PF, bool DYN, bool LEAN = false>
 int launch_u(const TickDesc& d, cudaStream_t s, int max_blocks) {
@@ -733,6 +734,11 @@ int launch_gm(const TickDesc& d, cudaStream_t s, int mb) {
   // per thread; launches with pull groups (more ops per chunk, more Philox
   // folds) with 2, which keeps 3 CTAs/SM resident.
   int u = d.ng > 0 ? 2 : 4;
+  // launches with >= 2 memory applies (the distributed owners' exchange: remote
+  // u~ loads) at U = 2 take phase A's triple-source path: 3 sources x 2 chunks
+  // in flight per thread at 4 CTAs/SM instead of 4 chunks of one source at 2
+  // (HP_APPLY_U, tuning; 0 = as other launches)
+  if (g_apply_u > 0 && d.na >= 2) u = g_apply_u;
   if (g_u_override > 0) u = g_u_override;
   // the L2 prefetch (d.pf > 0) is a separate instance, so the plain kernels keep
   // their code; the engine asks for it only on launches with few load streams
@@ -760,6 +766,8 @@ int launch_tick(const TickDesc& d, int grad_mode, bool momentum, void* stream, i
     g_pdl = p ? atoi(p) : 1;
     const char* g = getenv("HP_GRID");
     g_grid = g ? atoi(g) : 0;
+    const char* au = getenv("HP_APPLY_U");
+    g_apply_u = au ? atoi(au) : 0;
   }
   if (d.n <= 0) return 0;
   switch (grad_mode) {
