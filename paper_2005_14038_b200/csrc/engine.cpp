@@ -632,10 +632,7 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
       loads += (d.f[k].grad ? 1 : 0) + ((d.f[k].stash && d.f[k].op != 1) ? 1 : 0);
   }
   d.pf = (remote == 0 && loads <= pf_max) ? pf_env : 0;
-  // completes-only launches take the lean (phase B) instance (HP_LEAN=0: off)
-  static const int lean_env = getenv("HP_LEAN") ? atoi(getenv("HP_LEAN")) : 1;
-  d.lean = (lean_env && d.nc > 0 && d.na == 0 && d.ng == 0 && d.np == 0 && !d.wg_load &&
-            !d.wg_store) ? 1 : 0;
+  // (completes-only launches take the lean instance, set below with the tiles)
   // dynamic tile scheduling (HP_DYN, default on) for launches with at least
   // HP_DYN_MINLOADS load streams (HP_DYN_PULLS: also launches with pull groups):
   // counters of this launch stream
@@ -647,7 +644,15 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   static const int64_t dyn_n = getenv("HP_DYN_MIN_N") ? atoll(getenv("HP_DYN_MIN_N")) : (1 << 20);
   d.ctr = nullptr;
   d.done = nullptr;
-  if (dyn_env && loads >= dyn_min && n >= dyn_n && (dyn_pulls || d.ng == 0))
+  // completes-only launches take the lean instance; HP_LEAN_DYN=1 gives them
+  // dynamic tiles whatever their load streams (the 1-stream backlog complete
+  // otherwise runs a static grid and ends with its slowest CTA)
+  static const int lean_env = getenv("HP_LEAN") ? atoi(getenv("HP_LEAN")) : 1;
+  static const int lean_dyn = getenv("HP_LEAN_DYN") ? atoi(getenv("HP_LEAN_DYN")) : 0;
+  d.lean = (lean_env && d.nc > 0 && d.na == 0 && d.ng == 0 && d.np == 0 && !d.wg_load &&
+            !d.wg_store) ? 1 : 0;
+  if (dyn_env && (loads >= dyn_min || (d.lean && lean_dyn)) && n >= dyn_n &&
+      (dyn_pulls || d.ng == 0))
     tile_slot(st, &d.ctr, &d.done);
   if (capturing_ && batch_ok_ && st == stream_) {
     batch_.push_back(TickDescPad{d});

@@ -807,7 +807,21 @@ hp_status Engine::finish_connect(const void* comm_id) {
         if (int e = cudaStreamCreateWithPriority(&fs_[v], cudaStreamNonBlocking, prio_hi))
           return check_cuda(e, "stream");
     }
-  if (const char* xb = getenv("HP_XBLOCKS")) xblocks_ = atoi(xb);
+  if (const char* xb = getenv("HP_XBLOCKS")) {
+    xblocks_ = atoi(xb);
+  } else if (cfg_.transport == HP_XPORT_PEER && cfg_.momentum == 0.f) {
+    // one VW stage per GPU, SGD (C3 at 4 GPUs, C3 with two-stage VWs at 8):
+    // the owners' apply launches on 128 CTAs measured 5% faster per round
+    // (1.09 vs 1.15 ms, profiles/r02/multi_g4_knobs/); with several stages per
+    // GPU (C3 at 2 GPUs) or heavy-ball momentum (C5) the bound cost 10-15%
+    int most = 0;
+    for (int q = 0; q < G_; ++q) {
+      int cnt = 0;
+      for (int v = 0; v < N_; ++v) cnt += lay_[q].has[v] ? 1 : 0;
+      most = std::max(most, cnt);
+    }
+    if (most <= 1) xblocks_ = 128;
+  }
   if (const char* ab = getenv("HP_ABLOCKS")) ablocks_ = atoi(ab);
   // HP_AGRID=1: accumulation launches non-persistent (CTAs retire every U
   // chunks), so the high-priority exchange stream's launches start promptly

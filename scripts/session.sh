@@ -89,8 +89,13 @@ overlap)
   done
   ;;
 knobs)
-  for kv in "HP_TICK_U=1" "HP_GRID=1" "HP_PDL=0" "HP_DYN=0" "HP_PREFETCH=0" "HP_DYN_MIN_N=0"; do
-    env $kv timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu > "$D/parity_${kv}.log" 2>&1; st "$kv" $?
+  for kv in "HP_TICK_U=1" "HP_GRID=1" "HP_PDL=0" "HP_DYN=0" "HP_PREFETCH=0" "HP_DYN_MIN_N=0" \
+            "HP_LEAN=0" "HP_APPLY_U=2" "HP_TICK_BATCH=0"; do
+    env $kv timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_graph.py -q -m gpu > "$D/parity_${kv}.log" 2>&1; st "$kv" $?
+  done
+  for kv in "HP_P2P=0" "HP_AGRID=1" "HP_APPLY_U=2 HP_XBLOCKS=128" "HP_SPLIT_FOLDS=1 HP_XBLOCKS=96"; do
+    tag=$(echo "$kv" | tr ' =' '__')
+    env $kv timeout 900 python -m pytest tests/test_gpu_colocated.py -q -m gpu > "$D/colocated_${tag}.log" 2>&1; st "colocated_$tag" $?
   done
   ;;
 *)
