@@ -42,3 +42,18 @@ def test_reference_arm_other_configs():
 def test_reference_arm_nonzero_rank_is_silent():
     lines = _run({"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
     assert lines == []
+
+
+def test_survey_byte_model_matches_survey_numbers():
+    """bench.survey_bytes_per_param restates SURVEY.md 8(d): per VW-wave
+    16*N_m - 12 (accumulate) + 4 (u~ read) + 8 (pull) = 16*N_m, plus 8 per
+    apply batch (+8 with momentum): C2 with the 4 pushes of a round applied in
+    one batch is SURVEY's 264 B/param/round (4x52 + 4x4 + 8 +
+    4x8)."""
+    import bench
+    from workloads import C2, C4, C5
+    assert bench.survey_bytes_per_param(4, 1, C2) == 4 * 52 + 4 * 4 + 8 + 4 * 8 == 264
+    assert bench.survey_bytes_per_param(4, 4, C2) == 4 * 64 + 4 * 8
+    assert bench.survey_bytes_per_param(4, 1, C4) == 4 * (16 * 8 - 12 + 4 + 8) + 8
+    assert bench.survey_bytes_per_param(8, 8, C5) == 8 * 128 + 8 * 16      # momentum
+    assert bench.survey_bytes_per_param(4, 1, C2.replace(F=2)) == 4 * (16 * 8) + 8
