@@ -96,6 +96,10 @@ hp_status Engine::dist_accumulate(const std::vector<bool>& pulled) {
       fst = fs_[v];                     // folds after the pull that rewrote w_local
       wait_clear(fst, xwl_[v]);
       if (lastw_[v]) cudaStreamWaitEvent(fst, lastw_[v], 0);
+      // EXTERNAL gradients: a fold reads the gradient slot its minibatch's
+      // host copy filled on the accumulation stream -- after that copy (the
+      // acc launches follow their copies on vs_, so after the last of them)
+      if (cfg_.grad_mode == HP_GRAD_EXTERNAL && lastc_[v]) cudaStreamWaitEvent(fst, lastc_[v], 0);
     } else {
       for (int j = 0; j < d.nc; ++j) wait_clear(vs_[v], xacc_[v][cslot[j]]);
       wait_clear(vs_[v], xwl_[v]);

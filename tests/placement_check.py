@@ -179,6 +179,7 @@ def _run_colocated_once(hetpipe, cfg, G, k, alloc, lib, sampled, bounds, host_gr
                 out[r] = collect(ctx, cfg, G, k, r, sampled, bounds)
             except Exception as e:  # reported below
                 errs.append((r, e))
+                connected.abort()     # release ranks waiting for this one
 
         th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(G)]
         for t in th:
@@ -186,8 +187,12 @@ def _run_colocated_once(hetpipe, cfg, G, k, alloc, lib, sampled, bounds, host_gr
         for t in th:
             t.join(timeout)
         assert not any(t.is_alive() for t in th), "a rank thread did not finish"
-        if errs and all(getattr(e, "status", None) == hetpipe.HP_ERR_COMM and "timed out" in str(e)
-                        for _, e in errs):
+        def stall(e):      # a flag deadline, in the schedule or at connect
+            return ((getattr(e, "status", None) == hetpipe.HP_ERR_COMM and
+                     ("timed out" in str(e) or "did not reach" in str(e)))
+                    or isinstance(e, threading.BrokenBarrierError))
+        if errs and any(stall(e) for _, e in errs) and all(
+                stall(e) for _, e in errs):
             raise _FlagStall(errs)
         assert not errs, errs
         return out

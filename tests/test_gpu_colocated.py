@@ -125,10 +125,13 @@ def test_colocated_layer_rr_bounds(hp):
     check(cfg, G, 1, out, smp)
 
 
-@pytest.mark.parametrize("G,k", [(2, 1), (4, 2)])
-def test_colocated_external_host_gradients(hp, G, k):
+@pytest.mark.parametrize("G,k,split", [(2, 1, "0"), (4, 2, "0"), (4, 2, "1"), (2, 1, "1")])
+def test_colocated_external_host_gradients(hp, monkeypatch, G, k, split):
     """EXTERNAL: the caller's host gradients; every rank copies its stages of
-    the VWs' whole gradients on the VW's accumulation stream."""
+    the VWs' whole gradients on the VW's accumulation stream. With split
+    acc / fold launches the fold stream must wait for that copy (round 2: a
+    fold once read its slot before the copy landed)."""
+    monkeypatch.setenv("HP_SPLIT_FOLDS", split)
     import torch
     cfg = C3.replace(nparams=20_000, waves=4, D=1)
     # pinned buffers: a pageable cudaMemcpyAsync blocks its host thread until
