@@ -30,6 +30,8 @@ CASES = [
     ("convexF", WSPConfig("cf", 3, 2, 1, 2053, 4, (3, 5, 4), grad_mode=3, lr=0.05, F=2), 3, 1, {}),
     ("split-F2", WSPConfig("sf", 3, 2, 1, 1030, 4, (3, 7, 4), F=2), 2, 1, {"split": "1"}),
     ("barriers", C3.replace(nparams=4099, waves=5), 4, 1, {"HP_P2P": "0"}),
+    ("thm1", WSPConfig("t1", 3, 2, 1, 2053, 6, (3, 5, 4), lr=0.2, lr_schedule=1,
+                       grad_mode=3), 3, 2, {}),
     ("reader-F3", WSPConfig("r3", 4, 1, 0, 333, 4, (3, 9, 4, 8), momentum=0.9, F=3), 3, 2,
      {"HP_PULL_PUSH": "0"}),
 ]

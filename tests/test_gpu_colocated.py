@@ -19,7 +19,7 @@ import random
 import pytest
 
 from placement_check import check, host_gradients, run_colocated
-from workloads import (C3, C5, GRAD_CONVEX, GRAD_EXTERNAL, WSPConfig, even_shards,
+from workloads import (C3, C4, C5, C5E, GRAD_CONVEX, GRAD_EXTERNAL, WSPConfig, even_shards,
                        sample_indices)
 from workloads import models as M
 
@@ -72,6 +72,14 @@ CASES = [
     ("C3-full-G2-k1", C3.replace(waves=3), 2, 1, True, {}),
     # configs[4] (C5: VGG-19 size, 8 VWs, heavy-ball momentum) at full size, 2 VWs per rank
     ("C5-full-G4-mom", C5.replace(waves=2, D=4), 4, 1, True, {}),
+    # G = 8 (the pool never gives 8 GPUs): the placements bench.py runs at
+    # --gpus 8 -- C3 with two-stage VWs (k = 2), C5 with one VW per GPU and
+    # momentum -- as 8 co-located ranks, full size, sampled
+    ("C3-full-G8-k2", C3.replace(waves=3), 8, 2, True, {}),
+    ("C5-full-G8-mom", C5.replace(waves=2, D=4), 8, 1, True, {}),
+    # SURVEY 8(d) C4' (VGG-19 size, each VW on 2 GPUs, PS even over 8)
+    ("C4prime-full-G8-k2", C4.replace(waves=2), 8, 2, True, {}),
+    ("C5E-G8-lockstep-peer", C5E.replace(nparams=80_000, waves=3, num_vw=8), 8, 1, False, {}),
     ("C3-G4-k1", C3.replace(nparams=40_000, waves=8), 4, 1, False, {}),
     ("C3-G4-k2-mom", C3.replace(nparams=40_003, waves=8, momentum=0.9), 4, 2, False, {}),
     ("lazy-atleast-G3", WSPConfig("lazy", 3, 3, 1, 12_345, 7, (3, 5, 4), pull_policy=1,
@@ -81,6 +89,11 @@ CASES = [
     ("convex-G4-k2", C3.replace(nparams=20_000, waves=5, grad_mode=GRAD_CONVEX, lr=0.05),
      4, 2, False, {}),
     ("F2-strict-G2", WSPConfig("f2", 3, 2, 1, 33_333, 5, (3, 7, 4), F=2), 2, 1, False, {}),
+    # Theorem 1's step sizes (NEXT-2) through the distributed descriptors
+    ("thm1-convex-G4-k2", C3.replace(nparams=20_000, waves=5, grad_mode=GRAD_CONVEX, lr=0.3,
+                                     lr_schedule=1), 4, 2, False, {}),
+    ("thm1-float-G3", WSPConfig("t1", 3, 2, 1, 12_345, 6, (3, 5, 4), lr=0.2, lr_schedule=1),
+     3, 1, False, {}),
     # reader-side pulls everywhere (HP_PULL_PUSH=0) and split acc / fold launches
     # (HP_SPLIT_FOLDS=1, incl. F = 2 STRICT whose pull reads the open clock's
     # aggregate while later completes join it: ADVICE round 1)
