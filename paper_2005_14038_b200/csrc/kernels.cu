@@ -276,7 +276,9 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
   }
   // ---- B. completes --------------------------------------------------------
   // (pairing two completes' loads as in phase A needs ~45 more registers at
-  // U = 2: it spills under the 4-CTA cap, so the completes stay sequential)
+  // U = 2: it spills under the 4-CTA cap, so the completes stay sequential;
+  // round 2 re-checked: 113 registers uncapped, 144 spilled bytes under the
+  // 64-register cap)
   for (int j = 0; j < d.nc; ++j) {
     float4 ain[U], win[U], gin[U];
     complete_load<GM, U, CNT>(d.c[j], q0, qs, ain, win, gin);
