@@ -268,12 +268,19 @@ hp_status hp_schedule_advance(hp_ctx* ctx, int64_t target_commits, int64_t* comm
    the controller advances to target_commits NOW on the host (protocol state,
    trace, stats move exactly as hp_schedule_advance), but the device work of
    those ticks -- every fused tick launch -- is captured into one CUDA graph
-   (stream capture of the context stream, relaxed mode) instead of running. hp_graph_launch then runs
-   it ONCE on the context stream (a graph holds those ticks' descriptors; a
+   (stream capture of the context stream, relaxed mode) instead of running.
+   A context of at most HP_TICK_BATCH_MAX_N (default 2^16) params captures its
+   ticks as multi-tick launches instead: up to 512 tick descriptors uploaded to
+   a device buffer the graph owns, run in order by one kernel each (every
+   param's chunk owned by one thread for all ticks, so each tick's loads and
+   stores are exactly the per-tick launch's). hp_graph_launch then runs it
+   ONCE on the context stream (a graph holds those ticks' descriptors; a
    second launch would redo them, so it is refused: HP_ERR_STATE). Until that
-   launch, do not read weights or capture again (HP_ERR_STATE). Not allowed with
-   host gradients (pageable copies cannot be captured) or while per-launch
-   profiling is on (HP_ERR_STATE). *out owned by the caller: hp_graph_destroy. */
+   launch, do not read weights or capture again (HP_ERR_STATE). Launch it
+   before hp_finalize of its context. Not allowed with host gradients
+   (pageable copies cannot be captured) or while per-launch profiling is on
+   (HP_ERR_STATE). *out owned by the caller: hp_graph_destroy (waits for a
+   launched graph to finish before freeing its buffers). */
 typedef struct hp_graph hp_graph;
 hp_status hp_schedule_capture(hp_ctx* ctx, int64_t target_commits, int64_t* commits,
                               hp_graph** out);
