@@ -879,7 +879,7 @@ int launch_spin(unsigned long long ns, void* stream) {
 // deadlock until the barrier's deadline (the CUDA guide's lazy-loading caveat
 // for kernels that wait on each other) -- first seen with co-located ranks on
 // one GPU. So every kernel instance the launchers can pick is loaded up front,
-// once per process (cudaFuncGetAttributes forces the load).
+// once per device (cudaFuncGetAttributes forces the load).
 template <int GM, bool MOM>
 void preload_gm() {
   cudaFuncAttributes a;
@@ -899,9 +899,16 @@ void preload_gm() {
 }
 
 int preload_kernels() {
-  static int err = -1;
-  static std::once_flag once;
-  std::call_once(once, [] {
+  // once per device (module loading is per context; the caller has set the
+  // device)
+  static std::mutex mu;
+  static unsigned long long done = 0;
+  int dev = 0;
+  if (int e = (int)cudaGetDevice(&dev)) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && (done >> dev) & 1ull) return 0;
+  int err = 0;
+  {
     cudaFuncAttributes a;
     preload_gm<0, false>();
     preload_gm<0, true>();
@@ -924,7 +931,8 @@ int preload_kernels() {
     cudaFuncGetAttributes(&a, empty_kernel);
     cudaFuncGetAttributes(&a, init_kernel);
     err = (int)cudaGetLastError();
-  });
+  }
+  if (!err && dev < 64) done |= 1ull << dev;
   return err;
 }
 
