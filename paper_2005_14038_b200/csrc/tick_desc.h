@@ -211,7 +211,7 @@ int launch_flag_ops(const FlagOps& fo, void* stream);
 // DYADIC, CONVEX). Returns a cudaError_t as int.
 int launch_multi_tick(const TickDescPad* descs, int count, int64_t n, int grad_mode, bool momentum,
                       void* stream);
-// Load every kernel instance now (once per process; lazy module loading could
+// Load every kernel instance now (once per device; lazy module loading could
 // otherwise stall a spinning flag barrier). Returns a cudaError_t as int.
 int preload_kernels();
 // hp_launch_floor: an empty one-CTA kernel launched with the PDL attribute.
