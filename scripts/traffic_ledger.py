@@ -2,7 +2,7 @@
 the paper's printed figures (context: units not stated, reading
 Z19) and the B200 runs' measured NVLink ingress.
 
-    python scripts/traffic_ledger.py > profiles/r01_traffic_ledger.txt
+    python scripts/traffic_ledger.py > profiles/r02/traffic_ledger.txt
 """
 import glob
 import json
@@ -51,6 +51,10 @@ def main():
               f"{horovod_bytes(P) / MB:.1f} MB (paper {paper_hvd}) | ED-local activations across "
               f"nodes per minibatch, cuts {list(cuts)} = {edl / MB:.1f} MB (paper {paper_edl}) | "
               f"ED default PS push+pull per VW-wave ~ {default_ps_bytes(model) / MB:.1f} MB")
+    print("# (the paper prints no partitions: the ED-local cuts above are hp_partition's min-max\n"
+          "#  compute/communication split under reading Z23, so the activation bytes differ from the\n"
+          "#  paper's -- for ResNet-152 even in direction, 196 < 215 MB here vs 298 > 211 MB printed;\n"
+          "#  the Horovod figure depends only on the model size and matches)")
     print()
     print("# PS shard imbalance of the layer round-robin placement (largest shard / mean)")
     for model in ("vgg19", "resnet152"):
