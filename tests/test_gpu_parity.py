@@ -254,8 +254,11 @@ def test_zero_and_tiny_sizes(hp):
                                  C5.replace(waves=2, D=4),
                                  C2.replace(waves=3, grad_mode=GRAD_CONVEX, lr=0.05),
                                  C2.replace(waves=2, F=2, D=1),
-                                 C4.replace(waves=2, grad_mode=GRAD_CONVEX, lr=0.05, F=2)],
-                         ids=["C2", "C3", "C5", "C2-convex", "C2-F2", "C4-convex-F2"])
+                                 C4.replace(waves=2, grad_mode=GRAD_CONVEX, lr=0.05, F=2),
+                                 C2.replace(waves=3, grad_mode=GRAD_CONVEX, lr=0.3,
+                                            lr_schedule=1)],
+                         ids=["C2", "C3", "C5", "C2-convex", "C2-F2", "C4-convex-F2",
+                              "C2-convex-theorem1"])
 def test_full_size_sampled(hp, cfg):
     """Full model sizes in the bench's launch configuration: sampled params
     (stride 4099 + both ends) against the oracle restricted to that sample."""
