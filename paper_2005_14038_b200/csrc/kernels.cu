@@ -278,36 +278,8 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
   // (pairing two completes' loads as in phase A needs ~45 more registers at
   // U = 2: it spills under the 4-CTA cap, so the completes stay sequential;
   // round 2 re-checked: 113 registers uncapped, 144 spilled bytes under the
-  // 64-register cap)
-#ifdef HP_ACC_LOOKAHEAD
-  // U <= 2: the next complete's acc slot is loaded before this complete's
-  // Philox / finish, so two acc loads are in flight per chunk (the round-end
-  // launches have several completes whose only load is their acc slot)
-  if (U <= 2 && d.nc > 1) {
-    float4 anext[U];
-    if (d.c[0].flags & kLoadAcc) {
-#pragma unroll
-      for (int x = 0; x < U; ++x) anext[x] = ld4<CNT>(d.c[0].acc, q0 + x * qs);
-    }
-    for (int j = 0; j < d.nc; ++j) {
-      const DComplete& c = d.c[j];
-      float4 ain[U], win[U], gin[U];
-#pragma unroll
-      for (int x = 0; x < U; ++x) {
-        ain[x] = anext[x];
-        const int64_t q = q0 + x * qs;
-        if (c.flags & kFoldInline) win[x] = ld4<CNT>(c.wl, q);
-        if (GM == 2) gin[x] = ld4<CNT>(c.grad, q);
-        if (GM == 3) gin[x] = ld4<CNT>(c.stash, q);
-      }
-      if (j + 1 < d.nc && (d.c[j + 1].flags & kLoadAcc)) {
-#pragma unroll
-        for (int x = 0; x < U; ++x) anext[x] = ld4<CNT>(d.c[j + 1].acc, q0 + x * qs);
-      }
-      complete_finish<GM, MOM, U, CNT>(d, c, q0, qs, ain, win, gin, wg, mm);
-    }
-  } else
-#endif
+  // 64-register cap; loading only the next complete's acc slot ahead spills
+  // 48 bytes and ran 10% slower on C2's round-end launch, 6043 -> 5467 GB/s)
   for (int j = 0; j < d.nc; ++j) {
     float4 ain[U], win[U], gin[U];
     complete_load<GM, U, CNT>(d.c[j], q0, qs, ain, win, gin);
