@@ -279,8 +279,21 @@ __device__ __forceinline__ void tick_chunks(const TickDesc& d, int64_t q0, int64
   // U = 2: it spills under the 4-CTA cap, so the completes stay sequential;
   // round 2 re-checked: 113 registers uncapped, 144 spilled bytes under the
   // 64-register cap; loading only the next complete's acc slot ahead spills
-  // 48 bytes and ran 10% slower on C2's round-end launch, 6043 -> 5467 GB/s)
-  for (int j = 0; j < d.nc; ++j) {
+  // 48 bytes and ran 10% slower on C2's round-end launch, 6043 -> 5467 GB/s).
+  // At U = 1 (the multi-tick kernel's chunks, the tails) registers are cheap:
+  // two completes are loaded and drawn together, so their Philox chains
+  // interleave -- the latency-bound C1 tick is two such chains long.
+  int j0 = 0;
+  if constexpr (U == 1) {
+    for (; j0 + 1 < d.nc; j0 += 2) {
+      float4 ain0[1], win0[1], gin0[1], ain1[1], win1[1], gin1[1];
+      complete_load<GM, 1, CNT>(d.c[j0], q0, qs, ain0, win0, gin0);
+      complete_load<GM, 1, CNT>(d.c[j0 + 1], q0, qs, ain1, win1, gin1);
+      complete_finish<GM, MOM, 1, CNT>(d, d.c[j0], q0, qs, ain0, win0, gin0, wg, mm);
+      complete_finish<GM, MOM, 1, CNT>(d, d.c[j0 + 1], q0, qs, ain1, win1, gin1, wg, mm);
+    }
+  }
+  for (int j = j0; j < d.nc; ++j) {
     float4 ain[U], win[U], gin[U];
     complete_load<GM, U, CNT>(d.c[j], q0, qs, ain, win, gin);
     complete_finish<GM, MOM, U, CNT>(d, d.c[j], q0, qs, ain, win, gin, wg, mm);
