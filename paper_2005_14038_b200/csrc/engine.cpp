@@ -644,11 +644,12 @@ hp_status Engine::emit(TickDesc& d, int64_t begin, int64_t n, cudaStream_t st, i
   static const int64_t dyn_n = getenv("HP_DYN_MIN_N") ? atoll(getenv("HP_DYN_MIN_N")) : (1 << 20);
   d.ctr = nullptr;
   d.done = nullptr;
-  // completes-only launches take the lean instance; HP_LEAN_DYN=1 gives them
-  // dynamic tiles whatever their load streams (the 1-stream backlog complete
-  // otherwise runs a static grid and ends with its slowest CTA)
+  // completes-only launches take the lean instance, with dynamic tiles
+  // whatever their load streams (HP_LEAN_DYN, default on: the 1-stream
+  // complete otherwise runs a static grid and ends with its slowest CTA; C3 at
+  // 4 GPUs 1.091 -> 1.074 ms, C2 neutral, profiles/r02/lean_dyn_ab/)
   static const int lean_env = getenv("HP_LEAN") ? atoi(getenv("HP_LEAN")) : 1;
-  static const int lean_dyn = getenv("HP_LEAN_DYN") ? atoi(getenv("HP_LEAN_DYN")) : 0;
+  static const int lean_dyn = getenv("HP_LEAN_DYN") ? atoi(getenv("HP_LEAN_DYN")) : 1;
   d.lean = (lean_env && d.nc > 0 && d.na == 0 && d.ng == 0 && d.np == 0 && !d.wg_load &&
             !d.wg_store) ? 1 : 0;
   if (dyn_env && (loads >= dyn_min || (d.lean && lean_dyn)) && n >= dyn_n &&
