@@ -30,6 +30,13 @@ import sys
 import tempfile
 import time
 
+# hardware work queues per CUDA context, read once at context creation (before
+# torch initialises CUDA): the distributed engine runs the exchange, the
+# accumulation and the fold launches on separate streams, which the default 8
+# queues alias (the library's split acc / fold default asks for
+# >= 16, include/hetpipe.h hp_connect)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
@@ -756,6 +763,7 @@ def main():
                    "pull": args.pull.upper(), "local": "STRICT",
                    "apply": "on arrival" if args.apply_mode else "deferred to the observing pull",
                    "acc_slots": args.acc_slots,
+                   "cuda_device_max_connections": os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS"),
                    "transport": args.transport if placed else None,
                    "ps_shards": args.ps if placed else None,
                    "lockstep_batches": res["lockstep"] if placed else None,

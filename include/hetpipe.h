@@ -167,7 +167,14 @@ void hp_config_default(hp_config* cfg);
    -- NVLink loads and stores inside the tick kernels, ordered by a
    stream-ordered barrier: device readiness flags in every arena (release /
    acquire over NVLink; HP_FLAG_BARRIER=0: a 4-byte NCCL
-   all-reduce). */
+   all-reduce). Each local VW's accumulation, the exchange and (split acc /
+   fold launches) the folds run on separate streams: set
+   CUDA_DEVICE_MAX_CONNECTIONS >= 16 (e.g. 32) in the environment before the
+   process creates its CUDA context, or the runtime's default 8 hardware
+   queues serialise them. With a communicator, >= 16 queues, the PEER
+   transport, SGD and at most one VW stage per GPU, the accumulation and the
+   folds are split into separate launches by default (HP_SPLIT_FOLDS=0/1
+   overrides). */
 hp_status hp_comm_unique_id(void* out128);
 hp_status hp_ipc_handle(hp_ctx* ctx, void* out64);
 hp_status hp_connect(hp_ctx* ctx, const void* handles, const void* comm_id);

@@ -698,7 +698,9 @@ void Engine::note_sync(const TickDesc& d) {
   if (!prof_on_ || prof_launches_ == 0) return;
   const int64_t idx = prof_launches_ - 1;
   for (int j = 0; j < d.nc; ++j)
-    if (d.c[j].p % (uint32_t)U_ == 0 && push_launch_[d.c[j].v] < 0) push_launch_[d.c[j].v] = idx;
+    if (d.c[j].flags != kFoldInline &&          // (a fold-only complete pushes nothing)
+        d.c[j].p % (uint32_t)U_ == 0 && push_launch_[d.c[j].v] < 0)
+      push_launch_[d.c[j].v] = idx;
   std::vector<int> pulled;
   for (int g = 0; g < d.ng; ++g)
     if (d.g[g].pull)

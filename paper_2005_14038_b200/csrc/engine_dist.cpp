@@ -100,6 +100,21 @@ hp_status Engine::dist_accumulate(const std::vector<bool>& pulled) {
       // host copy filled on the accumulation stream -- after that copy (the
       // acc launches follow their copies on vs_, so after the last of them)
       if (cfg_.grad_mode == HP_GRAD_EXTERNAL && lastc_[v]) cudaStreamWaitEvent(fst, lastc_[v], 0);
+      // a single FOLD is the inline fold of a complete without its
+      // acc part: it takes the lean completes-only instance (4 chunks per
+      // thread, 4 CTAs/SM) instead of the group path, whose 2-chunk / 3-CTA
+      // shape leaves a one-buffer launch latency-bound (HP_FOLD_LEAN=0: group)
+      static const int fold_lean = getenv("HP_FOLD_LEAN") ? atoi(getenv("HP_FOLD_LEAN")) : 1;
+      if (fold_lean && folds.size() == 1 && folds[0] > 0) {
+        DComplete& c = d.c[d.nc++];
+        c.wl = s.wl;
+        c.grad = fold_grad(v, folds[0]);
+        c.v = (uint32_t)v;
+        c.p = (uint32_t)folds[0];
+        c.flags = kFoldInline;
+        c.neg_lr = neg_lr_of(v, folds[0]);
+        folds.clear();
+      }
     } else {
       for (int j = 0; j < d.nc; ++j) wait_clear(vs_[v], xacc_[v][cslot[j]]);
       wait_clear(vs_[v], xwl_[v]);
@@ -130,7 +145,7 @@ hp_status Engine::dist_accumulate(const std::vector<bool>& pulled) {
     if (hp_status st = emit(d, s.a0, s.len, fst, ablocks_)) return st;
     cudaEvent_t e = pool_event();
     cudaEventRecord(e, fst);
-    if (d.nc || fst == vs_[v]) lastc_[v] = e;
+    if (fst == vs_[v]) lastc_[v] = e;   // (fs_ launches write no acc slot)
     lastw_[v] = e;
   }
   return HP_OK;
@@ -800,7 +815,31 @@ hp_status Engine::finish_connect(const void* comm_id) {
   lastw_.assign(N_, nullptr);
   vs_.assign(N_, nullptr);
   fs_.assign(N_, nullptr);
-  if (const char* sf = getenv("HP_SPLIT_FOLDS")) split_folds_ = atoi(sf) != 0;
+  // the most VW stages any GPU holds (1: C3 at 4 GPUs, C3 with two-stage VWs
+  // at 8, one VW per GPU)
+  int most = 0;
+  for (int q = 0; q < G_; ++q) {
+    int cnt = 0;
+    for (int v = 0; v < N_; ++v) cnt += lay_[q].has[v] ? 1 : 0;
+    most = std::max(most, cnt);
+  }
+  const bool one_stage_sgd = cfg_.transport == HP_XPORT_PEER && cfg_.momentum == 0.f && most <= 1;
+  // Split acc / fold launches by default (row a9) where they measured faster:
+  // one VW stage per GPU, SGD, peer exchange, one process per GPU (a
+  // communicator), and at least 16 hardware work queues
+  // (CUDA_DEVICE_MAX_CONNECTIONS, read by the CUDA runtime at context
+  // creation; with the default 8 the fold stream shares a queue with the
+  // exchange or accumulation stream and the split launches serialise behind
+  // it). C3 at 4 GPUs: 1.074 -> 1.012-1.016 ms per round with the
+  // accumulation grid at 2.5 CTAs per SM (profiles/r02/c3_overlap_g4/).
+  bool auto_split = false;
+  if (const char* sf = getenv("HP_SPLIT_FOLDS")) {
+    split_folds_ = atoi(sf) != 0;
+  } else {
+    const char* mc = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    auto_split = one_stage_sgd && comm_ && !convex_ && mc && atoi(mc) >= 16;
+    split_folds_ = auto_split;
+  }
   if (const char* pp = getenv("HP_PULL_PUSH")) push_pull_ = atoi(pp) != 0;
   for (int v = 0; v < N_; ++v)
     if (vw_[v].here)
@@ -813,20 +852,24 @@ hp_status Engine::finish_connect(const void* comm_id) {
     }
   if (const char* xb = getenv("HP_XBLOCKS")) {
     xblocks_ = atoi(xb);
-  } else if (cfg_.transport == HP_XPORT_PEER && cfg_.momentum == 0.f) {
+  } else if (one_stage_sgd) {
     // one VW stage per GPU, SGD (C3 at 4 GPUs, C3 with two-stage VWs at 8):
     // the owners' apply launches on 128 CTAs measured 5% faster per round
     // (1.09 vs 1.15 ms, profiles/r02/multi_g4_knobs/); with several stages per
     // GPU (C3 at 2 GPUs) or heavy-ball momentum (C5) the bound cost 10-15%
-    int most = 0;
-    for (int q = 0; q < G_; ++q) {
-      int cnt = 0;
-      for (int v = 0; v < N_; ++v) cnt += lay_[q].has[v] ? 1 : 0;
-      most = std::max(most, cnt);
-    }
-    if (most <= 1) xblocks_ = 128;
+    xblocks_ = 128;
   }
-  if (const char* ab = getenv("HP_ABLOCKS")) ablocks_ = atoi(ab);
+  if (const char* ab = getenv("HP_ABLOCKS")) {
+    ablocks_ = atoi(ab);
+  } else if (auto_split) {
+    // the split accumulation launches on 2.5 CTAs per SM leave room beside
+    // them for the exchange launch's CTAs (2 per SM: 1.033 ms, 3: 1.10,
+    // full grid: 1.15; profiles/r02/c3_overlap_g4/)
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    ablocks_ = sms > 0 ? sms * 5 / 2 : 0;
+  }
   // HP_AGRID=1: accumulation launches non-persistent (CTAs retire every U
   // chunks), so the high-priority exchange stream's launches start promptly
   if (const char* ag = getenv("HP_AGRID"))

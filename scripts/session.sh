@@ -17,6 +17,9 @@
 #             multi-GPU parity
 #   overlap   a9 overlap variants (split folds, bounded grids) with per-launch timelines
 #   knobs     GPU parity under the non-default tuning knobs (1 GPU)
+#   cosched   C3 exchange / completes SM co-scheduling knobs with timelines, N >= 2
+#   splitdef  split acc / fold default A/B + multi-GPU parity, N >= 2
+#   accov     HP_ACC_OVERLAP A/B (completes-only launches under the exchange), N >= 2
 set -u
 JOB=${1:?job}
 TAG=${2:-$JOB}
@@ -87,6 +90,60 @@ overlap)
       st "${name}_${tag}" $?
     done
   done
+  ;;
+accov)
+  # a9: completes-only launches under the exchange (HP_ACC_OVERLAP) A/B on
+  # every visible GPU, alternating, plus timelines of the default
+  [ "$NG" -ge 2 ] || { st accov_needs_2_gpus 1; exit 0; }
+  P=29900
+  for cfg in "C3" "C5E --transport nvls" "C5" "C3 --span 2" "C3"; do
+    name=$(echo "$cfg" | tr -d ' -')
+    for ov in 1 0; do
+      P=$((P+1))
+      HP_ACC_OVERLAP=$ov timeout 900 $TR --nproc-per-node "$NG" --master-port $P bench.py --gpus "$NG" --config $cfg \
+        $NOX --steps 100 --no-extras > "$D/${name}_ov${ov}_$P.json" 2>> "$D/err.log"
+      st "${name}_ov${ov}_$P" $?
+    done
+  done
+  P=$((P+1))
+  timeout 900 $TR --nproc-per-node "$NG" --master-port $P bench.py --gpus "$NG" $NOX --steps 30 --profile-steps 6 \
+    --no-extras --timeline "$D/tl_c3" > "$D/c3_timeline.json" 2>> "$D/err.log"; st tl $?
+  CUDA_VISIBLE_DEVICES=0 timeout 1200 python -m pytest tests/test_gpu_colocated.py -q -m gpu > "$D/colocated.log" 2>&1; st colocated $?
+  timeout 1500 python -m pytest tests/test_gpu_multi.py -q > "$D/pytest_multi.log" 2>&1; st multi_parity $?
+  ;;
+cosched)
+  # C3 at N GPUs: SM co-scheduling of the owners' exchange with the VW's own
+  # completes (grid bounds, non-persistent completes, priorities), timelines;
+  # COSCHED_ENVS overrides the list (one entry per variant, '+' joins variables)
+  [ "$NG" -ge 2 ] || { st cosched_needs_2_gpus 1; exit 0; }
+  P=29950
+  for env in ${COSCHED_ENVS:-"X=0" "HP_ABLOCKS=296" "HP_ABLOCKS=148" "HP_AGRID=1" "HP_XBLOCKS=256" "HP_PRIO=0" "X=0"}; do
+    P=$((P+1)); tag=$(echo "$env" | tr ' =+@' '____')
+    # BENCH_ARGS: a leading '@args@' token of an entry ('@--acc-slots+3@HP_X=1')
+    # passes bench arguments ('+' = space)
+    bargs=""
+    case "$env" in @*@*) bargs=$(echo "$env" | cut -d@ -f2 | tr '+' ' '); env=$(echo "$env" | cut -d@ -f3);; esac
+    env $(echo "$env" | tr '+' ' ') timeout 900 $TR --nproc-per-node "$NG" --master-port $P bench.py --gpus "$NG" $NOX --steps 100 \
+      --no-extras $bargs --timeline "$D/tl_${tag}_$P" > "$D/c3_${tag}_$P.json" 2>> "$D/err.log"
+    st "c3_${tag}_$P" $?
+  done
+  ;;
+splitdef)
+  # the split acc / fold default (one VW stage per GPU, SGD, peer): A/B
+  # against HP_SPLIT_FOLDS=0, the other one-stage placements, multi-GPU parity
+  [ "$NG" -ge 2 ] || { st splitdef_needs_2_gpus 1; exit 0; }
+  P=30100
+  run() { P=$((P+1)); ev=$1; name=$2; shift 2; env $ev timeout 900 $TR --nproc-per-node "$NG" --master-port $P bench.py --gpus "$NG" "$@" > "$D/$name.json" 2>> "$D/err.log"; st "$name" $?; }
+  run X=0 c3_default $NOX --steps 300
+  run HP_SPLIT_FOLDS=0 c3_fused $NOX --steps 300
+  run X=0 c3_default2 $NOX --steps 300
+  run X=0 c5e_peer --config C5E --span 1 --transport peer $NOX --steps 40
+  run HP_SPLIT_FOLDS=0 c5e_peer_fused --config C5E --span 1 --transport peer $NOX --steps 40
+  run X=0 hvd_peer --config HVD --span 1 --transport peer $NOX --steps 40
+  run HP_SPLIT_FOLDS=0 hvd_peer_fused --config HVD --span 1 --transport peer $NOX --steps 40
+  run X=0 c5e_nvls --config C5E --span 1 --transport nvls $NOX --steps 40
+  timeout 1500 python -m pytest tests/test_gpu_multi.py -q > "$D/pytest_multi.log" 2>&1; st multi_parity $?
+  CUDA_VISIBLE_DEVICES=0 timeout 1200 python -m pytest tests/test_gpu_colocated.py -q -m gpu > "$D/colocated.log" 2>&1; st colocated $?
   ;;
 knobs)
   for kv in "HP_TICK_U=1" "HP_GRID=1" "HP_PDL=0" "HP_DYN=0" "HP_PREFETCH=0" "HP_DYN_MIN_N=0" \

@@ -3,6 +3,7 @@
 // tested against the oracle on a CPU-only machine. "Device" memory is host
 // memory. Never used by libhetpipe.so (see tests/emu/build_emu.py).
 #pragma once
+#include <atomic>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -61,8 +62,14 @@ inline cudaError_t cudaMemcpy(void* d, const void* s, size_t n, cudaMemcpyKind) 
   return cudaSuccess;
 }
 inline cudaError_t cudaStreamSynchronize(cudaStream_t) { return cudaSuccess; }
+inline cudaError_t cudaGetDevice(int* d) { *d = 0; return cudaSuccess; }
+enum cudaDeviceAttr { cudaDevAttrMultiProcessorCount = 16 };
+inline cudaError_t cudaDeviceGetAttribute(int* v, cudaDeviceAttr, int) { *v = 148; return cudaSuccess; }
 inline cudaError_t cudaEventCreate(cudaEvent_t* e) {
-  *e = (cudaEvent_t)(uintptr_t)1;
+  // distinct handles, so the engine's bookkeeping of stored events sees
+  // distinct events (the emulation never waits on them)
+  static std::atomic<uintptr_t> next{1};
+  *e = (cudaEvent_t)(next.fetch_add(1) * 16);
   return cudaSuccess;
 }
 inline cudaError_t cudaEventDestroy(cudaEvent_t) { return cudaSuccess; }

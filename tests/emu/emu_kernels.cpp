@@ -72,7 +72,9 @@ int launch_tick(const TickDesc& d, int gm, bool mom, void*, int) {
       const DComplete& c = d.c[j];
       const float u = draw_u(d, gm, c.v, c.p, i, c.grad, c.stash, c.neg_lr);
       if (c.flags & kSnapAcc) c.snap[i] = c.acc[i];
-      const float a = (c.flags & kFirst) ? u : c.acc[i] + u;
+      // (the acc is loaded only with kLoadAcc, as on the device: a fold-only
+      // complete -- kFoldInline alone -- has no acc slot)
+      const float a = (c.flags & kFirst) ? u : (c.flags & kLoadAcc) ? c.acc[i] + u : u;
       if (c.flags & kStoreAcc) c.acc[i] = a;
       if (c.flags & kApplyNow) app(d, mom, wg, m, a);
       if (c.flags & kFoldInline) {

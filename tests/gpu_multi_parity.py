@@ -7,8 +7,11 @@ import os
 import random
 import sys
 
+# as bench.py: enough hardware queues for the engine's streams (the library's
+# split acc / fold default needs >= 16), before CUDA initialises
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
-import torch
+import torch  # noqa: E402
 import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
