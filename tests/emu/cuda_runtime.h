@@ -24,7 +24,9 @@ inline cudaError_t cudaSetDevice(int) { return cudaSuccess; }
 inline cudaError_t cudaGetLastError() { return cudaSuccess; }
 inline const char* cudaGetErrorString(cudaError_t) { return "emulated"; }
 inline cudaError_t cudaStreamCreateWithFlags(cudaStream_t* s, unsigned) {
-  *s = (cudaStream_t)(uintptr_t)1;
+  // distinct handles, as on the device (the engine tells its streams apart)
+  static std::atomic<uintptr_t> next{1};
+  *s = (cudaStream_t)(next.fetch_add(1) * 16);
   return cudaSuccess;
 }
 inline cudaError_t cudaStreamCreateWithPriority(cudaStream_t* s, unsigned f, int) {

@@ -239,3 +239,61 @@ def test_placement_external_host_gradients(lib, G, k):
             bufs[(v * last_p + p) % n][:] = gradient(idx, v, p, cfg)
     out = run_placement(lib, cfg, G, k, host_grads=bufs, grad_mode=GRAD_EXTERNAL)
     check(cfg, G, k, out)
+
+
+def _fold_stream_launches(lib, cfg, G, k, **over):
+    """Launches rank 0 issued on fold streams (HP_SPLIT_FOLDS: acc and folds
+    in separate launches) over a whole schedule, via hp_profile_streams."""
+    from paper_2005_14038_b200 import hetpipe
+    cid = hetpipe.comm_unique_id(lib)
+    ctxs = [hetpipe.Context(hetpipe.config_from(cfg, world=G, rank=r, vw_span=k, **over), lib=lib)
+            for r in range(G)]
+    handles = [c.ipc_handle() for c in ctxs]
+    ids, errs = [None] * G, []
+
+    def work(r):
+        try:
+            c = ctxs[r]
+            c.connect(handles, cid)
+            c.profile_enable(True)
+            c.run_schedule(cfg.tau, cfg.latency())
+            ids[r] = c.profile_streams()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(120)
+    assert not errs, errs
+    for c in ctxs:
+        c.close()
+    return int(np.sum(np.asarray(ids[0]) >= 3 + cfg.num_vw))
+
+
+@pytest.mark.parametrize("conns,env,momentum,G,split", [
+    ("32", {}, 0.0, 4, True),                       # C3 at 4 GPUs: one stage per GPU, SGD
+    ("8", {}, 0.0, 4, False),                       # too few hardware queues
+    (None, {}, 0.0, 4, False),                      # runtime default (8)
+    ("32", {"HP_SPLIT_FOLDS": "0"}, 0.0, 4, False),  # explicit off
+    ("32", {}, 0.9, 4, False),                      # heavy-ball momentum
+    ("32", {}, 0.0, 2, False),                      # two VW stages per GPU
+    ("8", {"HP_SPLIT_FOLDS": "1"}, 0.0, 2, True),   # explicit on
+])
+def test_split_folds_default_rule(lib, monkeypatch, conns, env, momentum, G, split):
+    """The split acc / fold default (engine_dist.cpp finish_connect, DESIGN.md
+    9h): on only for the peer exchange with SGD, at most one VW stage per GPU,
+    a communicator and CUDA_DEVICE_MAX_CONNECTIONS >= 16; HP_SPLIT_FOLDS
+    overrides. Parity of both forms: the placement cases above and
+    tests/test_colocated_emu.py."""
+    if conns is None:
+        monkeypatch.delenv("CUDA_DEVICE_MAX_CONNECTIONS", raising=False)
+    else:
+        monkeypatch.setenv("CUDA_DEVICE_MAX_CONNECTIONS", conns)
+    monkeypatch.delenv("HP_SPLIT_FOLDS", raising=False)
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    cfg = C3.replace(nparams=4096, waves=4, momentum=momentum)
+    n = _fold_stream_launches(lib, cfg, G, 1)
+    assert (n > 0) == split, n
