@@ -216,7 +216,8 @@ class Engine {
   std::vector<cudaEvent_t> lastw_;    // its last w_local-writing launch (vs_ or fs_)
   std::vector<cudaStream_t> vs_;      // per local VW: accumulation stream
   std::vector<cudaStream_t> fs_;      // per local VW: fold stream
-  bool split_folds_ = false;          // HP_SPLIT_FOLDS=1: acc and folds in separate launches
+  bool split_folds_ = false;          // acc and folds in separate launches (HP_SPLIT_FOLDS;
+                                      // default rule in finish_connect)
   bool push_pull_ = true;             // owner-side pull (HP_PULL_PUSH=0: reader-side)
   bool forked_ = false;               // side streams ordered after the context stream
   int xblocks_ = 0;                   // grid bound of exchange launches (HP_XBLOCKS)
